@@ -1,0 +1,206 @@
+/*
+ * dd.h -- C ABI of the B200-native fine-grained domain-decomposition ILU0
+ * library (arXiv 2508.04917, "Mapping Sparse Triangular Solves to GPUs via
+ * Fine-grained Domain Decomposition").
+ *
+ * Citations: P:a-b = PAPER.md lines a-b (section / algorithm named);
+ * Rn = reading n in DESIGN.md section 3 (where the paper is silent/garbled).
+ *
+ * Operation (P:41-46 problem statement; Alg. 1 inputs P:139):
+ *   dd_setup    partition (Alg. 2) -> stable row permutation
+ *                -> block reorder (Alg. 3) -> drop the
+ *               inter-subdomain blocks (sec. 3.2) -> per-subdomain
+ *               block ILU0 + ILDU0 (Alg. 7) -> level sets (Alg. 5
+ *               semantics P:448-508) -> device-resident factor slabs.
+ *   dd_apply    z = M^-1 r with M = L D U_unit: fused forward unit-lower
+ *               sweep, 3x3 block-diagonal scaling, backward unit-upper sweep,
+ *               one CTA per subdomain with the subdomain vector in shared
+ *               memory (Alg. 4 P:410-441 / Alg. 6, sec. 4.3
+ *               P:653-678, sec. 4.4).
+ *   dd_spmv     y = A_r x with the reordered, UN-dropped matrix (R10).
+ *   dd_bicgstab right-preconditioned BiCGSTAB (Alg. 1, K1 = I,
+ *               K2 = M; R20-R25).
+ *
+ * Data layout
+ *   BSR3: row_ptr int64[n+1], col_idx int32[nnzb] ascending and unique per
+ *   row, vals double[9*nnzb], each 3x3 block row-major. Block dim fixed = 3.
+ *   Vectors: double[3*n], component c of block row i at index 3*i + c.
+ *   Device vectors passed to dd_apply / dd_spmv / dd_bicgstab live in the
+ *   REORDERED, subdomain-contiguous space (the paper solves there),
+ *   restricted to this rank's rows (dd_local_range); use dd_permute /
+ *   dd_unpermute to map from/to the user's original ordering.
+ *
+ * Ownership
+ *   dd_setup copies A; the caller may free it on return. The context owns
+ *   every host and device buffer it allocates; dd_destroy frees them.
+ *   Vector pointers are caller-owned, device memory on the context's device,
+ *   16-byte aligned, 3*n_local doubles; dd_apply may read r up to the next
+ *   16-byte boundary past its end (any cudaMalloc / torch allocation
+ *   satisfies this).
+ *
+ * Streams: dd_apply, dd_spmv, dd_permute, dd_unpermute are ordered on the
+ *   given cudaStream_t (passed as void*, NULL = legacy default stream) and do
+ *   not synchronise the host unless stated. dd_bicgstab returns when the
+ *   solve is done (it synchronises the stream once per half-iteration to
+ *   test convergence).
+ *
+ * Errors: every call returns a dd_status and never aborts; dd_last_error()
+ *   gives a thread-local message for the last failing call. dd_setup failure
+ *   leaves *out = NULL. No call falls back to a CPU path.
+ *
+ * Multi-GPU (sec. 4.5 P:730-734 extended to the solver): one process per GPU;
+ *   rank r owns a contiguous, count-balanced range of subdomains (R32).
+ *   Every rank passes the same full host matrix. dd_setup, dd_spmv and
+ *   dd_bicgstab are collective when world > 1 (NCCL: halo exchange for SpMV,
+ *   all-gather of double-double dot partials). dd_apply never communicates.
+ */
+#ifndef DD_H
+#define DD_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DD_OK = 0,
+    DD_E_INVALID_ARG = 1,       /* NULL pointer, bad size, bad option         */
+    DD_E_NOT_SQUARE = 2,        /* reserved (BSR3 input is square by type)    */
+    DD_E_UNSORTED_OR_DUP = 3,   /* col_idx not strictly ascending in a row    */
+    DD_E_MISSING_DIAG = 4,      /* a block row has no diagonal block          */
+    DD_E_SINGULAR_PIVOT = 5,    /* |det U_ii| < pivot_floor during ILU0 (R15) */
+    DD_E_SUBDOMAIN_TOO_LARGE = 6, /* 24*P bytes + staging exceed shared mem   */
+    DD_E_GRID_NOT_DIVISIBLE = 7,  /* geometric tiles do not tile the grid (R26) */
+    DD_E_CUDA = 8,
+    DD_E_NCCL = 9,
+    DD_E_OOM = 10,
+    DD_E_BREAKDOWN = 11,        /* |rho|, |sigma| or tau < 1e-30 (R25)        */
+    DD_E_MAXITER = 12,
+    DD_E_NO_DEVICE = 13         /* no CUDA device (and host_only not set)     */
+} dd_status;
+
+/* Borrowed BSR3 matrix (copied by dd_setup). */
+typedef struct {
+    int64_t n_block_rows;
+    int64_t nnzb;
+    const int64_t *row_ptr;  /* [n_block_rows + 1]                         */
+    const int32_t *col_idx;  /* [nnzb], ascending, unique per row          */
+    const double *vals;      /* [9 * nnzb], 3x3 row-major blocks           */
+} dd_bsr3;
+
+/* Alg. 2 geometric cuts: grid (nx,ny,nz), natural order i + nx*(j + ny*k);
+ * tile dims (tx,ty,tz) = Alg. 2's nblk_*; P = tx*ty*tz block rows. */
+typedef struct {
+    int32_t nx, ny, nz, tx, ty, tz;
+} dd_grid;
+
+/* Apply-kernel variants (sec. 4.1 vs 4.2). */
+#define DD_LEVELSET 1  /* level sets + CTA barriers between levels (Alg. 6)        */
+#define DD_SPINLOOP 2  /* per-row ready flags in shared memory, no level barriers (Alg. 4) */
+#define DD_DIRECT 4    /* ablation: level-set kernel reading factors straight from HBM  */
+
+typedef struct {
+    int32_t subdomain_rows;   /* P when grid == NULL: contiguous chunks (R26)   */
+    const dd_grid *grid;      /* optional geometric partition                   */
+    int32_t variants;         /* OR of DD_LEVELSET | DD_SPINLOOP | DD_DIRECT to
+                                 build; 0 = DD_LEVELSET                          */
+    int32_t device;           /* CUDA device ordinal                            */
+    int32_t rank, world;      /* world <= 1: single GPU                         */
+    const void *nccl_unique_id; /* 128-byte ncclUniqueId (rank 0 creates, the
+                                   caller broadcasts); NULL if world <= 1       */
+    double pivot_floor;       /* 0 -> 1e-300 (R15)                              */
+    int32_t host_only;        /* 1: run the host setup only (no device work;
+                                 introspection calls work, compute calls
+                                 return DD_E_INVALID_ARG)                       */
+    int32_t n_threads;        /* host setup threads, 0 = all                   */
+} dd_opts;
+
+typedef struct dd_ctx dd_ctx;
+
+typedef struct {
+    double iterations;        /* 0.5 granularity (R22)                          */
+    int32_t n_applies;        /* preconditioner applies (paper-style count)     */
+    int32_t converged;
+    int32_t breakdown;
+    int32_t status;           /* dd_status of the solve                         */
+    double rel_resid;         /* last recursive ||r|| / ||r0||                   */
+    double true_rel_resid;    /* ||b - A x|| / ||b|| after the solve    */
+    double solve_ms;          /* host wall time of the solve                    */
+} dd_report;
+
+/* Setup (collective). Returns DD_OK and *out, or an error and *out = NULL. */
+dd_status dd_setup(const dd_bsr3 *A, const dd_opts *opts, dd_ctx **out);
+void dd_destroy(dd_ctx *ctx);
+
+/* This rank's rows in the reordered global numbering. */
+dd_status dd_local_range(const dd_ctx *ctx, int64_t *first_block_row, int64_t *n_block_rows);
+
+/* z = M^-1 r (this rank's subdomains; no communication). variant = one of
+ * DD_LEVELSET / DD_SPINLOOP / DD_DIRECT built at setup; 0 = DD_LEVELSET. */
+dd_status dd_apply(dd_ctx *ctx, const double *r, double *z, void *stream);
+dd_status dd_apply_variant(dd_ctx *ctx, int32_t variant, const double *r, double *z,
+                           void *stream);
+
+/* y = A_r x (halo exchange inside when world > 1; collective). */
+dd_status dd_spmv(dd_ctx *ctx, const double *x, double *y, void *stream);
+
+/* Solve A_r x = b to ||r|| < tol * ||r0|| (R21). b, x device, reordered,
+ * local. x in: x0, out: solution. resid_hist: nullable host array of
+ * 2*max_iter+1 doubles receiving [||r0||, ||s_1||, ||r_1||, ...].
+ * Returns DD_OK, DD_E_BREAKDOWN or DD_E_MAXITER (rep and x filled in all
+ * three cases). */
+dd_status dd_bicgstab(dd_ctx *ctx, const double *b, double *x, double tol, int32_t max_iter,
+                      double *resid_hist, dd_report *rep, void *stream);
+
+/* End-to-end user call: b_host / x_host are HOST arrays of 3*N doubles in
+ * the ORIGINAL ordering (pinned memory recommended). Copies b in, solves,
+ * copies this rank's part of x out (other entries of x_host untouched). */
+dd_status dd_solve_host(dd_ctx *ctx, const double *b_host, double *x_host, double tol,
+                        int32_t max_iter, dd_report *rep, void *stream);
+
+/* Original-ordering host vector (3*N) -> this rank's reordered device slice,
+ * and back (scatter of the local rows into the host vector). */
+dd_status dd_permute(dd_ctx *ctx, const double *v_orig_host, double *v_reord_dev, void *stream);
+dd_status dd_unpermute(dd_ctx *ctx, const double *v_reord_dev, double *v_orig_host,
+                       void *stream);
+
+/* Introspection for parity (caller-allocated host arrays). */
+dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original order*/,
+                           int32_t *new_to_old /*[N]*/);
+/* which: 0 = L (hmapL), 1 = U (hmapU); local rows, reordered order. */
+dd_status dd_get_levels(const dd_ctx *ctx, int32_t which, int32_t *hmap);
+/* Factors of the local rows in the dropped pattern, reordered local numbering
+ * (columns local too). Pass NULL arrays to query sizes only.
+ *   L: strictly-lower blocks (unit diagonal implied); U: strictly-upper
+ *   blocks of U_unit; Dinv: [9*n_local]. Lrp/Urp: [n_local+1]. */
+dd_status dd_get_factors(const dd_ctx *ctx, int64_t *nnzb_L, int64_t *nnzb_U, int64_t *Lrp,
+                         int32_t *Lci, double *Lv, int64_t *Urp, int32_t *Uci, double *Uv,
+                         double *Dinv);
+/* Halo description for world > 1 (sizes only if arrays NULL):
+ * ghost_rows: reordered global rows this rank reads from other ranks,
+ * ascending; their owner ranks in ghost_owner. */
+dd_status dd_get_halo(const dd_ctx *ctx, int64_t *n_ghost, int64_t *ghost_rows,
+                      int32_t *ghost_owner);
+/* Rows of this rank that peer `peer` reads (its ghosts owned here), local
+ * numbering, ascending; sizes only if rows == NULL. */
+dd_status dd_get_send_rows(const dd_ctx *ctx, int32_t peer, int64_t *n, int32_t *rows);
+/* stats[16]: {nnzb_before, nnzb_after, n_sub_global, n_sub_local, max_levels_L,
+ *   max_levels_U, max_P, slab_bytes_levelset, slab_bytes_spin, spmv_bytes,
+ *   apply_canonical_bytes, spmv_canonical_bytes, n_local, n_ghost, 0, 0};
+ * setup_ms[6]: {partition+permute, reorder+drop, ilu0+ildu0, levels,
+ *   pack, device upload}. Either may be NULL. */
+dd_status dd_stats(const dd_ctx *ctx, int64_t *stats, double *setup_ms);
+/* Apply-kernel launch shape chosen at setup: {grid, threads, smem_bytes,
+ * ring_bytes} for the given variant. */
+dd_status dd_launch_info(const dd_ctx *ctx, int32_t variant, int64_t *info);
+
+/* 128-byte ncclUniqueId for world > 1 (rank 0 calls it; the caller
+ * broadcasts the bytes, e.g. with torch.distributed). */
+dd_status dd_nccl_unique_id(void *out128);
+
+const char *dd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

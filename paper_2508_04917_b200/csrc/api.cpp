@@ -1,0 +1,581 @@
+// api.cpp -- the C ABI of include/dd.h: context lifetime, device upload,
+// apply / SpMV entry points, the BiCGSTAB driver (Alg. 1, right
+// preconditioning R20) and the NCCL plumbing for world > 1 (sec. 8e).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dd_internal.h"
+#include "krylov.cuh"
+
+namespace ddi {
+const char *last_error_c();
+}
+
+using namespace ddi;
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess) {                                                                \
+            set_error(std::string(#x) + ": " + cudaGetErrorString(e_));                         \
+            return e_ == cudaErrorMemoryAllocation ? DD_E_OOM : DD_E_CUDA;                      \
+        }                                                                                       \
+    } while (0)
+
+#define NK(x)                                                                                   \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) {                                                                \
+            set_error(std::string(#x) + ": " + ncclGetErrorString(r_));                         \
+            return DD_E_NCCL;                                                                   \
+        }                                                                                       \
+    } while (0)
+
+namespace {
+
+struct Workspace {
+    int64_t m = 0;  // 3 * n_local
+    double *r = nullptr, *rh = nullptr, *p = nullptr, *v = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr,
+           *t = nullptr, *bd = nullptr, *xd = nullptr;
+    double *sc = nullptr;        // device scalars [S_COUNT]
+    void *partials = nullptr;    // DD [grid * 2]
+    unsigned int *counter = nullptr;
+    double *loc = nullptr;       // [4] rank-local (s, c) pairs
+    double *gathered = nullptr;  // [world * 4]
+    double *h_sc = nullptr;      // pinned [S_COUNT]
+    double *xg = nullptr;        // ghost rows of the SpMV input [3 * n_ghost]
+    double *sendbuf = nullptr;   // [3 * total send rows]
+    int32_t *d_send_idx = nullptr;
+    std::vector<int64_t> send_off;  // [world + 1]
+};
+
+template <class T>
+dd_status dmalloc(T **p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return DD_OK;
+    CK(cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T)));
+    return DD_OK;
+}
+
+#define TRY(x)                        \
+    do {                              \
+        dd_status s_ = (x);           \
+        if (s_ != DD_OK) return s_;   \
+    } while (0)
+
+Workspace *ws_of(dd_ctx *c) { return reinterpret_cast<Workspace *>(c->dev_ws); }
+
+dd_status upload_slab(Slab &sl) {
+    TRY(dmalloc(&sl.d_bytes, sl.bytes.size() + 16));
+    TRY(dmalloc(&sl.d_info, sl.info.size() + 1));
+    if (!sl.bytes.empty()) CK(cudaMemcpy(sl.d_bytes, sl.bytes.data(), sl.bytes.size(), cudaMemcpyHostToDevice));
+    if (!sl.info.empty())
+        CK(cudaMemcpy(sl.d_info, sl.info.data(), sl.info.size() * sizeof(SubInfo), cudaMemcpyHostToDevice));
+    std::vector<uint8_t>().swap(sl.bytes);  // device copy is authoritative
+    return DD_OK;
+}
+
+dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
+    const double t0 = now_ms();
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->world > 1) {
+        ncclComm_t comm;
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        NK(ncclCommInitRank(&comm, ctx->world, id, ctx->rank));
+        ctx->nccl = comm;
+    }
+    TRY(apply_prepare(ctx));
+    const int64_t nl = ctx->n_local;
+    // slabs
+    if (ctx->variants & (DD_LEVELSET | DD_DIRECT)) TRY(upload_slab(ctx->slab_lvl));
+    if (ctx->variants & DD_SPINLOOP) TRY(upload_slab(ctx->slab_spin));
+    // sliced-ELL SpMV operand
+    {
+        auto &S = ctx->spmv;
+        std::vector<int64_t> sp(S.n_slices + 1, 0);
+        for (int64_t s = 0; s < S.n_slices; ++s) {
+            int64_t K = 0;
+            for (int64_t li = 32 * s; li < std::min(nl, 32 * s + 32); ++li)
+                K = std::max(K, ctx->Arp[li + 1] - ctx->Arp[li]);
+            sp[s + 1] = sp[s] + 32 * K;
+        }
+        std::vector<int32_t> cols(S.n_slots, -1);
+        std::vector<double> vals(9 * S.n_slots, 0.0);
+#pragma omp parallel for schedule(static)
+        for (int64_t s = 0; s < S.n_slices; ++s) {
+            for (int lane = 0; lane < 32; ++lane) {
+                const int64_t li = 32 * s + lane;
+                if (li >= nl) break;
+                for (int64_t k = 0; k < ctx->Arp[li + 1] - ctx->Arp[li]; ++k) {
+                    const int64_t p = ctx->Arp[li] + k;
+                    cols[sp[s] + 32 * k + lane] = ctx->Aci[p];
+                    for (int v = 0; v < 9; ++v) vals[9 * (sp[s] + 32 * k) + 32 * v + lane] = ctx->Av[9 * p + v];
+                }
+            }
+        }
+        TRY(dmalloc(&S.slot_ptr, sp.size()));
+        TRY(dmalloc(&S.cols, std::max<int64_t>(1, S.n_slots)));
+        TRY(dmalloc(&S.vals, std::max<int64_t>(1, 9 * S.n_slots)));
+        CK(cudaMemcpy(S.slot_ptr, sp.data(), sp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        if (S.n_slots) {
+            CK(cudaMemcpy(S.cols, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(S.vals, vals.data(), vals.size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
+    }
+    // permutation index of the local rows (original global row of local row li)
+    {
+        std::vector<int32_t> idx(nl);
+        for (int64_t li = 0; li < nl; ++li) idx[li] = ctx->new_to_old[ctx->row_first + li];
+        int32_t *d = nullptr;
+        TRY(dmalloc(&d, std::max<int64_t>(1, nl)));
+        if (nl) CK(cudaMemcpy(d, idx.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice));
+        ctx->d_new_to_old_local = d;
+        TRY(dmalloc(&ctx->d_stage, 3 * ctx->N + 2));
+    }
+    // BiCGSTAB workspace
+    auto *ws = new Workspace();
+    ctx->dev_ws = ws;
+    ws->m = 3 * nl;
+    const size_t mm = (size_t)ws->m + 2;  // +2: 16-byte slack past the end (dd.h)
+    for (double **q : {&ws->r, &ws->rh, &ws->p, &ws->v, &ws->ph, &ws->s, &ws->sh, &ws->t, &ws->bd, &ws->xd})
+        TRY(dmalloc(q, mm));
+    TRY(dmalloc(&ws->sc, ddk::S_COUNT));
+    CK(cudaMemset(ws->sc, 0, ddk::S_COUNT * sizeof(double)));
+    CK(cudaMalloc(&ws->partials, ddk::partials_bytes(ctx)));
+    TRY(dmalloc(&ws->counter, 4));
+    CK(cudaMemset(ws->counter, 0, 4 * sizeof(unsigned int)));
+    TRY(dmalloc(&ws->loc, 4));
+    TRY(dmalloc(&ws->gathered, 4 * (size_t)std::max(1, ctx->world)));
+    CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_sc), ddk::S_COUNT * sizeof(double)));
+    // halo buffers
+    const int64_t ng = (int64_t)ctx->ghost_rows.size();
+    TRY(dmalloc(&ws->xg, std::max<int64_t>(1, 3 * ng)));
+    ws->send_off.assign(ctx->world + 1, 0);
+    std::vector<int32_t> sidx;
+    for (int q = 0; q < ctx->world; ++q) {
+        if (q < (int)ctx->send_rows.size()) sidx.insert(sidx.end(), ctx->send_rows[q].begin(), ctx->send_rows[q].end());
+        ws->send_off[q + 1] = (int64_t)sidx.size();
+    }
+    TRY(dmalloc(&ws->sendbuf, std::max<size_t>(1, 3 * sidx.size())));
+    TRY(dmalloc(&ws->d_send_idx, std::max<size_t>(1, sidx.size())));
+    if (!sidx.empty())
+        CK(cudaMemcpy(ws->d_send_idx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());
+    ctx->setup_ms[5] = now_ms() - t0;
+    return DD_OK;
+}
+
+ddk::RedArgs red_args(dd_ctx *c) {
+    Workspace *ws = ws_of(c);
+    return ddk::RedArgs{reinterpret_cast<ddk::DD *>(ws->partials), ws->counter, ws->sc, ws->loc, c->world <= 1 ? 1 : 0};
+}
+
+// world > 1: all-gather the rank-local (s, c) pairs and finalize in rank order.
+dd_status reduce_across(dd_ctx *c, int nv, int op, cudaStream_t st) {
+    if (c->world <= 1) return DD_OK;
+    Workspace *ws = ws_of(c);
+    NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
+    ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ws->sc, op, st);
+    return DD_OK;
+}
+
+// halo exchange of the SpMV input x (local rows) into ws->xg
+dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
+    if (c->world <= 1) return DD_OK;
+    Workspace *ws = ws_of(c);
+    const int64_t ns = ws->send_off[c->world];
+    if (ns) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
+    auto comm = reinterpret_cast<ncclComm_t>(c->nccl);
+    NK(ncclGroupStart());
+    for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) continue;
+        const int64_t so = ws->send_off[q], sn = ws->send_off[q + 1] - so;
+        const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
+        if (sn) NK(ncclSend(ws->sendbuf + 3 * so, 3 * sn, ncclDouble, q, comm, st));
+        if (rn) NK(ncclRecv(ws->xg + 3 * ro, 3 * rn, ncclDouble, q, comm, st));
+    }
+    NK(ncclGroupEnd());
+    return DD_OK;
+}
+
+dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, cudaStream_t st) {
+    TRY(halo(c, x, st));
+    ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, red_args(c), st);
+    return DD_OK;
+}
+
+dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
+    Workspace *ws = ws_of(c);
+    CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DD_OK;
+}
+
+bool usable(dd_ctx *c) {
+    if (!c) {
+        set_error("NULL context");
+        return false;
+    }
+    if (c->host_only) {
+        set_error("context was set up with host_only = 1");
+        return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dd_last_error(void) { return last_error_c(); }
+
+dd_status dd_nccl_unique_id(void *out128) {
+    if (!out128) return DD_E_INVALID_ARG;
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, sizeof id);
+    return DD_OK;
+}
+
+dd_status dd_setup(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out) {
+    if (!out) {
+        set_error("dd_setup: out is NULL");
+        return DD_E_INVALID_ARG;
+    }
+    *out = nullptr;
+    if (!A || !o) {
+        set_error("dd_setup: NULL argument");
+        return DD_E_INVALID_ARG;
+    }
+    auto *ctx = new dd_ctx();
+    ctx->device = o->device;
+    ctx->rank = o->rank;
+    ctx->world = std::max(1, o->world);
+    ctx->host_only = o->host_only != 0;
+    if (ctx->rank < 0 || ctx->rank >= ctx->world || (ctx->world > 1 && !o->nccl_unique_id && !ctx->host_only)) {
+        set_error("dd_setup: bad rank/world or missing nccl_unique_id");
+        delete ctx;
+        return DD_E_INVALID_ARG;
+    }
+    if (!ctx->host_only) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            set_error("dd_setup: no CUDA device (set host_only for host-side setup only)");
+            delete ctx;
+            return DD_E_NO_DEVICE;
+        }
+    }
+    dd_status st = host_setup(ctx, A, o);
+    if (st == DD_OK && !ctx->host_only) st = device_setup(ctx, o->nccl_unique_id);
+    if (st != DD_OK) {
+        const std::string msg = last_error_c();
+        dd_destroy(ctx);
+        set_error(msg);
+        return st;
+    }
+    *out = ctx;
+    return DD_OK;
+}
+
+void dd_destroy(dd_ctx *c) {
+    if (!c) return;
+    if (!c->host_only) {
+        cudaSetDevice(c->device);
+        cudaDeviceSynchronize();
+        for (Slab *sl : {&c->slab_lvl, &c->slab_spin}) {
+            cudaFree(sl->d_bytes);
+            cudaFree(sl->d_info);
+        }
+        cudaFree(c->spmv.slot_ptr);
+        cudaFree(c->spmv.cols);
+        cudaFree(c->spmv.vals);
+        cudaFree(c->d_new_to_old_local);
+        cudaFree(c->d_stage);
+        if (Workspace *ws = ws_of(c)) {
+            for (double *q : {ws->r, ws->rh, ws->p, ws->v, ws->ph, ws->s, ws->sh, ws->t, ws->bd, ws->xd, ws->sc,
+                              ws->loc, ws->gathered, ws->xg, ws->sendbuf})
+                cudaFree(q);
+            cudaFree(ws->partials);
+            cudaFree(ws->counter);
+            cudaFree(ws->d_send_idx);
+            cudaFreeHost(ws->h_sc);
+            delete ws;
+        }
+        if (c->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->nccl));
+    }
+    delete c;
+}
+
+dd_status dd_local_range(const dd_ctx *c, int64_t *first, int64_t *n) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (first) *first = c->row_first;
+    if (n) *n = c->n_local;
+    return DD_OK;
+}
+
+dd_status dd_apply_variant(dd_ctx *c, int32_t variant, const double *r, double *z, void *stream) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    if ((!r || !z) && c->n_local) {
+        set_error("dd_apply: NULL vector");
+        return DD_E_INVALID_ARG;
+    }
+    return apply_launch(c, variant, r, z, stream);
+}
+
+dd_status dd_apply(dd_ctx *c, const double *r, double *z, void *stream) {
+    return dd_apply_variant(c, DD_LEVELSET, r, z, stream);
+}
+
+dd_status dd_spmv(dd_ctx *c, const double *x, double *y, void *stream) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, y, nullptr, st));
+    CK(cudaGetLastError());
+    return DD_OK;
+}
+
+dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t max_iter, double *hist,
+                      dd_report *rep, void *stream) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    if (!(tol > 0) || max_iter < 1) {
+        set_error("dd_bicgstab: tol must be > 0 and max_iter >= 1");
+        return DD_E_INVALID_ARG;
+    }
+    const double t0 = now_ms();
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Workspace *ws = ws_of(c);
+    const int64_t m = ws->m;
+    const ddk::RedArgs ra = red_args(c);
+    double *sc = ws->h_sc;
+    int nh = 0;
+    double iters = 0.0, rel = 1.0;
+    int napp = 0, status = DD_E_MAXITER, brk = 0;
+
+    // r = b - A x0; rh = r; rho_1 = ||r0||^2
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, st));
+    ddk::launch_init_r(c, m, b, ws->t, ws->r, ws->rh, ra, st);
+    TRY(reduce_across(c, 1, ddk::FIN_INIT, st));
+    TRY(read_scalars(c, st));
+    const double n0 = std::sqrt(sc[ddk::S_N0SQ]);
+    if (hist) hist[nh] = n0;
+    ++nh;
+    if (n0 == 0.0) {
+        status = DD_OK;
+        rel = 0.0;
+    } else {
+        const double thr = tol * n0;
+        iters = max_iter;
+        for (int k = 1; k <= max_iter; ++k) {
+            if (std::fabs(sc[ddk::S_RHO]) < 1e-30) {
+                status = DD_E_BREAKDOWN;
+                brk = 1;
+                iters = k - 1;
+                break;
+            }
+            ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, st);
+            TRY(apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream));
+            ++napp;
+            TRY(spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, st));
+            TRY(reduce_across(c, 1, ddk::FIN_ALPHA, st));
+            ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
+            TRY(reduce_across(c, 1, ddk::FIN_SS, st));
+            TRY(read_scalars(c, st));
+            if (std::fabs(sc[ddk::S_SIGMA]) < 1e-30) {
+                status = DD_E_BREAKDOWN;
+                brk = 2;
+                iters = k - 1;
+                break;
+            }
+            const double ns = std::sqrt(sc[ddk::S_SS]);
+            if (hist) hist[nh] = ns;
+            ++nh;
+            if (ns < thr) {
+                ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, st);
+                status = DD_OK;
+                iters = k - 0.5;
+                rel = ns / n0;
+                break;
+            }
+            TRY(apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream));
+            ++napp;
+            TRY(spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, st));
+            TRY(reduce_across(c, 2, ddk::FIN_OMEGA, st));
+            ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
+            TRY(read_scalars(c, st));  // tau check before the all-gather keeps ranks in step
+            if (!(sc[ddk::S_TT] >= 1e-30)) {
+                status = DD_E_BREAKDOWN;
+                brk = 3;
+                iters = k - 0.5;
+                break;
+            }
+            TRY(reduce_across(c, 2, ddk::FIN_RHO, st));
+            if (c->world > 1) TRY(read_scalars(c, st));
+            const double nr = std::sqrt(sc[ddk::S_RR]);
+            if (hist) hist[nh] = nr;
+            ++nh;
+            rel = nr / n0;
+            if (nr < thr) {
+                status = DD_OK;
+                iters = k;
+                break;
+            }
+        }
+    }
+    // true residual ||b - A x|| / ||b||
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, st));
+    ddk::launch_resid(c, m, b, ws->t, ra, st);
+    TRY(reduce_across(c, 2, ddk::FIN_RESID, st));
+    TRY(read_scalars(c, st));
+    CK(cudaGetLastError());
+    if (rep) {
+        rep->iterations = iters;
+        rep->n_applies = napp;
+        rep->converged = status == DD_OK;
+        rep->breakdown = brk;
+        rep->status = status;
+        rep->rel_resid = rel;
+        rep->true_rel_resid = sc[ddk::S_RES_BB] > 0 ? std::sqrt(sc[ddk::S_RES_TT]) / std::sqrt(sc[ddk::S_RES_BB]) : 0.0;
+        rep->solve_ms = now_ms() - t0;
+    }
+    return (dd_status)status;
+}
+
+dd_status dd_permute(dd_ctx *c, const double *v_orig_host, double *v_reord_dev, void *stream) {
+    if (!usable(c) || !v_orig_host || !v_reord_dev) return DD_E_INVALID_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CK(cudaMemcpyAsync(c->d_stage, v_orig_host, 3 * c->N * sizeof(double), cudaMemcpyHostToDevice, st));
+    ddk::launch_gather3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), c->d_stage,
+                        v_reord_dev, st);
+    CK(cudaGetLastError());
+    return DD_OK;
+}
+
+dd_status dd_unpermute(dd_ctx *c, const double *v_reord_dev, double *v_orig_host, void *stream) {
+    if (!usable(c) || !v_orig_host || !v_reord_dev) return DD_E_INVALID_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (c->world <= 1) {
+        ddk::launch_scatter3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), v_reord_dev,
+                             c->d_stage, st);
+        CK(cudaMemcpyAsync(v_orig_host, c->d_stage, 3 * c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        std::vector<double> tmp(3 * c->n_local);
+        CK(cudaMemcpyAsync(tmp.data(), v_reord_dev, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t li = 0; li < c->n_local; ++li) {
+            const int64_t g = c->new_to_old[c->row_first + li];
+            for (int q = 0; q < 3; ++q) v_orig_host[3 * g + q] = tmp[3 * li + q];
+        }
+    }
+    return DD_OK;
+}
+
+dd_status dd_solve_host(dd_ctx *c, const double *b_host, double *x_host, double tol, int32_t max_iter,
+                        dd_report *rep, void *stream) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Workspace *ws = ws_of(c);
+    TRY(dd_permute(c, b_host, ws->bd, stream));
+    CK(cudaMemsetAsync(ws->xd, 0, ws->m * sizeof(double), st));
+    dd_status s = dd_bicgstab(c, ws->bd, ws->xd, tol, max_iter, nullptr, rep, stream);
+    if (s != DD_OK && s != DD_E_BREAKDOWN && s != DD_E_MAXITER) return s;
+    TRY(dd_unpermute(c, ws->xd, x_host, stream));
+    return s;
+}
+
+dd_status dd_get_partition(const dd_ctx *c, int32_t *labels, int32_t *new_to_old) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (labels) std::memcpy(labels, c->labels.data(), c->N * sizeof(int32_t));
+    if (new_to_old) std::memcpy(new_to_old, c->new_to_old.data(), c->N * sizeof(int32_t));
+    return DD_OK;
+}
+
+dd_status dd_get_levels(const dd_ctx *c, int32_t which, int32_t *hmap) {
+    if (!c || !hmap || (which != 0 && which != 1)) return DD_E_INVALID_ARG;
+    const auto &h = which == 0 ? c->hmapL : c->hmapU;
+    std::memcpy(hmap, h.data(), h.size() * sizeof(int32_t));
+    return DD_OK;
+}
+
+dd_status dd_get_factors(const dd_ctx *c, int64_t *nL, int64_t *nU, int64_t *Lrp, int32_t *Lci, double *Lv,
+                         int64_t *Urp, int32_t *Uci, double *Uv, double *Dinv) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (nL) *nL = (int64_t)c->Lci.size();
+    if (nU) *nU = (int64_t)c->Uci.size();
+    if (Lrp) std::memcpy(Lrp, c->Lrp.data(), c->Lrp.size() * sizeof(int64_t));
+    if (Lci) std::memcpy(Lci, c->Lci.data(), c->Lci.size() * sizeof(int32_t));
+    if (Lv) std::memcpy(Lv, c->Lv.data(), c->Lv.size() * sizeof(double));
+    if (Urp) std::memcpy(Urp, c->Urp.data(), c->Urp.size() * sizeof(int64_t));
+    if (Uci) std::memcpy(Uci, c->Uci.data(), c->Uci.size() * sizeof(int32_t));
+    if (Uv) std::memcpy(Uv, c->Uv.data(), c->Uv.size() * sizeof(double));
+    if (Dinv) std::memcpy(Dinv, c->Dinv.data(), c->Dinv.size() * sizeof(double));
+    return DD_OK;
+}
+
+dd_status dd_get_halo(const dd_ctx *c, int64_t *n_ghost, int64_t *ghost_rows, int32_t *ghost_owner) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (n_ghost) *n_ghost = (int64_t)c->ghost_rows.size();
+    if (ghost_rows) std::memcpy(ghost_rows, c->ghost_rows.data(), c->ghost_rows.size() * sizeof(int64_t));
+    if (ghost_owner) std::memcpy(ghost_owner, c->ghost_owner.data(), c->ghost_owner.size() * sizeof(int32_t));
+    return DD_OK;
+}
+
+dd_status dd_get_send_rows(const dd_ctx *c, int32_t peer, int64_t *n, int32_t *rows) {
+    if (!c || peer < 0 || peer >= c->world) return DD_E_INVALID_ARG;
+    static const std::vector<int32_t> none;
+    const auto &v = peer < (int)c->send_rows.size() ? c->send_rows[peer] : none;
+    if (n) *n = (int64_t)v.size();
+    if (rows) std::memcpy(rows, v.data(), v.size() * sizeof(int32_t));
+    return DD_OK;
+}
+
+dd_status dd_stats(const dd_ctx *c, int64_t *stats, double *setup_ms) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (stats) {
+        const int64_t nL = (int64_t)c->Lci.size(), nU = (int64_t)c->Uci.size(), nl = c->n_local;
+        int64_t slab_l = 0, slab_s = 0;
+        for (auto &i : c->slab_lvl.info) slab_l += i.stream_bytes;
+        for (auto &i : c->slab_spin.info) slab_s += i.stream_bytes;
+        stats[0] = c->nnzb_A;
+        stats[1] = c->nnzb_dd;
+        stats[2] = c->n_sub;
+        stats[3] = c->sub_last - c->sub_first;
+        stats[4] = c->max_lev_L;
+        stats[5] = c->max_lev_U;
+        stats[6] = c->max_P;
+        stats[7] = slab_l;
+        stats[8] = slab_s;
+        stats[9] = c->spmv_bytes;
+        // canonical bytes: 72(nL+nU+n) + 4(nL+nU) + 4*2(n+1) + 48 n
+        stats[10] = 72 * (nL + nU + nl) + 4 * (nL + nU) + 8 * (nl + 1) + 48 * nl;
+        const int64_t nnzA_loc = c->Arp.empty() ? 0 : c->Arp.back();
+        stats[11] = 76 * nnzA_loc + 4 * (nl + 1) + 48 * nl;
+        stats[12] = nl;
+        stats[13] = (int64_t)c->ghost_rows.size();
+        stats[14] = 0;
+        stats[15] = 0;
+    }
+    if (setup_ms)
+        for (int q = 0; q < 6; ++q) setup_ms[q] = c->setup_ms[q];
+    return DD_OK;
+}
+
+dd_status dd_launch_info(const dd_ctx *c, int32_t variant, int64_t *info) {
+    if (!c || !info) return DD_E_INVALID_ARG;
+    const LaunchCfg *l = variant == DD_SPINLOOP ? &c->cfg_spin : variant == DD_DIRECT ? &c->cfg_direct : &c->cfg_lvl;
+    info[0] = l->grid;
+    info[1] = l->threads;
+    info[2] = l->smem;
+    info[3] = l->ring;
+    return DD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,457 @@
+// apply.cu -- fused per-subdomain ILDU0 apply z = U_unit^-1 D^-1 L^-1 r.
+//
+// One CTA owns one subdomain at a time; the subdomain vector (24*P bytes)
+// lives in shared memory for the whole L -> D -> U sequence (sec. 4.4
+// P:715-725; Alg. 6 P:582-615 with unit L per sec. 4.3). The
+// factor slab is level-ordered and read exactly once.
+//
+// Kernels
+//   k_apply_ring<RING,CH,SPIN>  persistent, warp-specialised: one producer
+//       warp streams each subdomain's r slice and factor slab through a
+//       shared-memory ring with 1-D bulk async copies (cp.async.bulk, UBLKCP)
+//       and full/empty mbarriers; TC consumer threads run the sweeps.
+//       SPIN=false: level sets, a CTA barrier between levels (Alg. 6).
+//       SPIN=true : rows in ascending (L) / descending (U) windows, each row
+//                   waits on per-row ready flags in shared memory (Alg. 4
+//                   P:410-441 with per-row flags, R17).
+//   k_apply_direct<SPIN>        ablation: same record processor, factors read
+//       straight from HBM with no staging (the paper's "vector in LDS,
+//       factors from global" design).
+//
+// Arithmetic: lower row i, component c:
+//   acc = r_ic; for blocks (j,B) ascending: for d: acc = fma(-B[c][d], z_jd, acc)
+// D+U row i: y_c = D[c][0]*z_i0; y_c = fma(D[c][1], z_i1, y_c); y_c = fma(D[c][2], z_i2, y_c);
+//   acc = y_c; for U blocks ascending: acc = fma(-B[c][d], x_jd, acc).
+// Compiled with -fmad=false; every fma is explicit (__fma_rn).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "dd_internal.h"
+#include "ptx.cuh"
+
+namespace ddk {
+
+using ddi::RecHdr;
+using ddi::SubInfo;
+constexpr int TC = 128;  // consumer threads = rows per record (Slab::rows_per_rec)
+
+__host__ __device__ constexpr uint32_t al8(uint32_t x) { return (x + 7u) & ~7u; }
+
+// ---- readers: map a byte offset inside the current record to data
+struct GlobalRd {
+    const uint8_t *p;
+    template <class T>
+    __device__ __forceinline__ T ld(uint32_t off) const {
+        return __ldg(reinterpret_cast<const T *>(p + off));
+    }
+};
+
+template <uint32_t RING>
+struct RingRd {
+    const uint8_t *ring;
+    uint32_t base;  // absolute stream position of the record start
+    template <class T>
+    __device__ __forceinline__ T ld(uint32_t off) const {
+        return *reinterpret_cast<const T *>(ring + ((base + off) & (RING - 1u)));
+    }
+};
+
+__device__ __forceinline__ uint16_t ld_volatile_u16(const uint16_t *p) {
+    return *reinterpret_cast<const volatile uint16_t *>(p);
+}
+
+// Process one record: thread t owns row rows[t] (t < w).
+template <bool SPIN, class Rd>
+__device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, int t, double *__restrict__ vec,
+                                               uint16_t *flags, uint16_t ep) {
+    const uint32_t w = h.w, K = h.K;
+    if (t >= (int)w) return;
+    const bool upper = (h.flags & ddi::REC_UPPER) != 0;
+    const uint32_t off_rows = 16u + 2u * K;
+    const uint32_t off_dinv = al8(off_rows + 2u * w);
+    const uint32_t off_cols = off_dinv + (upper ? 72u * w : 0u);
+    const uint32_t off_val = h.off_val;
+    const uint32_t i = rd.template ld<uint16_t>(off_rows + 2u * t);
+    double a0, a1, a2;
+    if (upper) {
+        const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
+        double D[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+        a0 = D[0] * z0;
+        a0 = __fma_rn(D[1], z1, a0);
+        a0 = __fma_rn(D[2], z2, a0);
+        a1 = D[3] * z0;
+        a1 = __fma_rn(D[4], z1, a1);
+        a1 = __fma_rn(D[5], z2, a1);
+        a2 = D[6] * z0;
+        a2 = __fma_rn(D[7], z1, a2);
+        a2 = __fma_rn(D[8], z2, a2);
+    } else {
+        a0 = vec[3 * i];
+        a1 = vec[3 * i + 1];
+        a2 = vec[3 * i + 2];
+    }
+    uint32_t pre = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
+        if ((uint32_t)t >= ck) break;
+        const uint32_t j = rd.template ld<uint16_t>(off_cols + 2u * (pre + t));
+        const uint32_t vb = off_val + 72u * pre + 8u * t;
+        double b[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + 8u * ck * v);
+        if (SPIN) {
+            while (ld_volatile_u16(flags + j) != ep) {
+            }
+            __threadfence_block();
+        }
+        const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+        a0 = __fma_rn(-b[0], x0, a0);
+        a0 = __fma_rn(-b[1], x1, a0);
+        a0 = __fma_rn(-b[2], x2, a0);
+        a1 = __fma_rn(-b[3], x0, a1);
+        a1 = __fma_rn(-b[4], x1, a1);
+        a1 = __fma_rn(-b[5], x2, a1);
+        a2 = __fma_rn(-b[6], x0, a2);
+        a2 = __fma_rn(-b[7], x1, a2);
+        a2 = __fma_rn(-b[8], x2, a2);
+        pre += ck;
+    }
+    vec[3 * i] = a0;
+    vec[3 * i + 1] = a1;
+    vec[3 * i + 2] = a2;
+    if (SPIN) {
+        __threadfence_block();
+        *reinterpret_cast<volatile uint16_t *>(flags + i) = ep;
+    }
+}
+
+__device__ __forceinline__ RecHdr hdr_from(uint4 q) {
+    RecHdr h;
+    h.w = (uint16_t)(q.x & 0xffffu);
+    h.K = (uint16_t)(q.x >> 16);
+    h.flags = (uint16_t)(q.y & 0xffffu);
+    h.nnz = (uint16_t)(q.y >> 16);
+    h.bytes = q.z;
+    h.off_val = q.w;
+    return h;
+}
+
+// ------------------------------------------------------------------ direct
+template <bool SPIN>
+__global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__ slab,
+                                                     const SubInfo *__restrict__ info, int n_sub,
+                                                     const double *__restrict__ r, double *__restrict__ z,
+                                                     int vec_bytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    double *vec = reinterpret_cast<double *>(smem);
+    uint16_t *flags = reinterpret_cast<uint16_t *>(smem + vec_bytes);
+    const int t = threadIdx.x;
+    if (SPIN) {
+        for (int q = t; q < vec_bytes / 24; q += TC) flags[q] = 0;
+    }
+    uint16_t ep = 0;
+    for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
+        const SubInfo si = info[s];
+        const int nd = 3 * si.nrows;
+        const double *rs = r + 3 * (int64_t)si.row0;
+        for (int q = t; q < nd; q += TC) vec[q] = __ldg(rs + q);
+        __syncthreads();
+        const uint8_t *p = slab + si.stream_off;
+        ++ep;
+        bool upper_seen = false;
+        while (true) {
+            const RecHdr h = hdr_from(__ldg(reinterpret_cast<const uint4 *>(p)));
+            if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
+                upper_seen = true;
+                ++ep;
+            }
+            process_record<SPIN>(GlobalRd{p}, h, t, vec, flags, ep);
+            __syncthreads();
+            p += h.bytes;
+            if (h.flags & ddi::REC_LAST) break;
+        }
+        if (SPIN && !upper_seen) ++ep;
+        double *zs = z + 3 * (int64_t)si.row0;
+        for (int q = t; q < nd; q += TC) zs[q] = vec[q];
+    }
+}
+
+// -------------------------------------------------------------------- ring
+template <uint32_t RING, uint32_t CH, bool SPIN>
+__global__ void __launch_bounds__(TC + 32, 1)
+    k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
+                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes) {
+    constexpr uint32_t NST = RING / CH;
+    static_assert((RING & (RING - 1)) == 0 && (CH & (CH - 1)) == 0 && NST >= 4, "ring shape");
+    extern __shared__ __align__(128) uint8_t smem[];
+    double *vec = reinterpret_cast<double *>(smem);
+    uint8_t *ring = smem + vec_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + RING);
+    uint64_t *empty = full + NST;
+    uint16_t *flags = reinterpret_cast<uint16_t *>(empty + NST);
+    const int tid = threadIdx.x;
+
+    if (tid == TC) {
+        for (uint32_t q = 0; q < NST; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], 1);
+        }
+        fence_mbar_init();
+    }
+    if (SPIN) {
+        for (int q = tid; q < vec_bytes / 24; q += TC + 32) flags[q] = 0;
+    }
+    __syncthreads();
+
+    if (tid >= TC) {
+        // ================= producer: one elected lane streams the CTA's work
+        if (tid == TC) {
+            const uint64_t pol = policy_evict_first();
+            uint32_t g = 0;
+            for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
+                const SubInfo si = info[s];
+                const int64_t rlo = (24 * (int64_t)si.row0) & ~(int64_t)15;
+                const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
+                const uint32_t rb = (uint32_t)(rhi - rlo);
+                const uint32_t total = rb + (uint32_t)si.stream_bytes;
+                const uint32_t nch = (total + CH - 1) / CH;
+                const uint8_t *rsrc = reinterpret_cast<const uint8_t *>(r) + rlo;
+                const uint8_t *fsrc = slab + si.stream_off;
+                for (uint32_t c = 0; c < nch; ++c, ++g) {
+                    const uint32_t st = g % NST;
+                    if (g >= NST) mbar_wait(&empty[st], ((g / NST) - 1u) & 1u);
+                    const uint32_t lo = c * CH, hi = min(total, lo + CH);
+                    mbar_arrive_expect_tx(&full[st], hi - lo);
+                    uint8_t *dst = ring + st * CH;
+                    if (lo < rb) bulk_g2s(dst, rsrc + lo, min(hi, rb) - lo, &full[st], pol);
+                    if (hi > rb) {
+                        const uint32_t b = max(lo, rb);
+                        bulk_g2s(dst + (b - lo), fsrc + (b - rb), hi - b, &full[st], pol);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ===================== consumers (TC threads, named barrier 1)
+    const int t = tid;
+    uint32_t gbase = 0;     // chunk index at which the current subdomain starts
+    uint32_t ready = 0;     // chunks this thread has seen full
+    uint32_t released = 0;  // (t == 0) chunks handed back to the producer
+    uint16_t ep = 0;
+    auto ensure = [&](uint32_t chunk) {
+        while (ready <= chunk) {
+            mbar_wait(&full[ready % NST], (ready / NST) & 1u);
+            ++ready;
+        }
+    };
+    auto release_to = [&](uint32_t upto) {
+        if (t == 0) {
+            while (released < upto) {
+                mbar_arrive(&empty[released % NST]);
+                ++released;
+            }
+        }
+    };
+    for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
+        const SubInfo si = info[s];
+        const int64_t rlo = (24 * (int64_t)si.row0) & ~(int64_t)15;
+        const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
+        const uint32_t rb = (uint32_t)(rhi - rlo);
+        const uint32_t shift = (uint32_t)(24 * (int64_t)si.row0 - rlo);
+        const uint32_t total = rb + (uint32_t)si.stream_bytes;
+        const uint32_t nch = (total + CH - 1) / CH;
+        const uint32_t nd = 3u * si.nrows;
+        const uint32_t abs0 = gbase * CH;
+        // ---- r slice: ring -> vec, chunk by chunk
+        const uint32_t nrc = (rb + CH - 1) / CH;
+        for (uint32_t c = 0; c < nrc; ++c) {
+            ensure(gbase + c);
+            const uint32_t qlo = c == 0 ? 0u : (c * CH - shift) / 8u;
+            const uint32_t qhi = min(nd, ((c + 1) * CH - shift) / 8u);
+            for (uint32_t q = qlo + t; q < qhi; q += TC)
+                vec[q] = *reinterpret_cast<const double *>(ring + ((abs0 + shift + 8u * q) & (RING - 1u)));
+            if ((c + 1) % (NST / 2) == 0 && c + 1 < nrc) {
+                named_bar_sync(1, TC);
+                release_to(gbase + c + 1);
+            }
+        }
+        named_bar_sync(1, TC);
+        release_to(gbase + rb / CH);
+        // ---- records
+        uint32_t ro = rb;
+        ++ep;
+        bool upper_seen = false;
+        while (true) {
+            ensure(gbase + ro / CH);
+            const RecHdr h = hdr_from(*reinterpret_cast<const uint4 *>(ring + ((abs0 + ro) & (RING - 1u))));
+            ensure(gbase + (ro + h.bytes - 1) / CH);
+            if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
+                upper_seen = true;
+                ++ep;
+            }
+            process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, t, vec, flags, ep);
+            ro += h.bytes;
+            named_bar_sync(1, TC);
+            if (h.flags & ddi::REC_LAST) {
+                release_to(gbase + nch);
+                break;
+            }
+            release_to(gbase + ro / CH);
+        }
+        if (SPIN && !upper_seen) ++ep;
+        double *zs = z + 3 * (int64_t)si.row0;
+        for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[q];
+        gbase += nch;
+    }
+}
+
+// ------------------------------------------------------------ host side
+using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int);
+
+template <uint32_t RING, uint32_t CH, bool SPIN>
+static RingFn ring_fn() {
+    return k_apply_ring<RING, CH, SPIN>;
+}
+
+static RingFn pick_ring(int ring, bool spin) {
+    if (!spin) {
+        switch (ring) {
+            case 131072: return ring_fn<131072, 8192, false>();
+            case 65536: return ring_fn<65536, 8192, false>();
+            case 32768: return ring_fn<32768, 4096, false>();
+            case 16384: return ring_fn<16384, 2048, false>();
+        }
+    } else {
+        switch (ring) {
+            case 131072: return ring_fn<131072, 8192, true>();
+            case 65536: return ring_fn<65536, 8192, true>();
+            case 32768: return ring_fn<32768, 4096, true>();
+            case 16384: return ring_fn<16384, 2048, true>();
+        }
+    }
+    return nullptr;
+}
+
+static int ring_chunk(int ring) { return ring >= 65536 ? 8192 : (ring >= 32768 ? 4096 : 2048); }
+
+}  // namespace ddk
+
+namespace ddi {
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+dd_status apply_prepare(dd_ctx *ctx) {
+    using namespace ddk;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) {
+        set_error("cudaGetDeviceProperties failed");
+        return DD_E_CUDA;
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    const int smem_max = (int)prop.sharedMemPerBlockOptin;       // 232448 on B200
+    const int smem_sm = (int)prop.sharedMemPerMultiprocessor;    // 233472 on B200
+    const int nsl = ctx->sub_last - ctx->sub_first;
+    const int vec_bytes = ((24 * ctx->max_P + 127) / 128) * 128;
+    // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
+    {
+        LaunchCfg &c = ctx->cfg_direct;
+        const bool spin = false;
+        c.smem = vec_bytes + (spin ? 2 * ctx->max_P : 0);
+        c.threads = TC;
+        c.grid = nsl;
+        c.consumers = TC;
+        c.ring = 0;
+        if (c.smem > smem_max) {
+            set_error("subdomain vector exceeds shared memory");
+            return DD_E_SUBDOMAIN_TOO_LARGE;
+        }
+        cudaFuncSetAttribute(k_apply_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
+        cudaFuncSetAttribute(k_apply_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             vec_bytes + 2 * ctx->max_P + 16);
+    }
+    // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
+    auto choose = [&](LaunchCfg &c, bool spin, int64_t max_rec) -> dd_status {
+        const int want = env_int("DD_RING_KB", 0) * 1024;
+        const int cands[4] = {131072, 65536, 32768, 16384};
+        int ring = 0;
+        for (int rc : cands) {
+            if (want && rc != want) continue;
+            const int nst = rc / ring_chunk(rc);
+            const int sm = vec_bytes + rc + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
+            if (sm <= smem_max && max_rec + ring_chunk(rc) <= rc) {
+                ring = rc;
+                break;
+            }
+        }
+        if (!ring) {
+            set_error("no ring size fits the subdomain vector and the largest record");
+            return DD_E_SUBDOMAIN_TOO_LARGE;
+        }
+        const int nst = ring / ring_chunk(ring);
+        c.ring = ring;
+        c.smem = vec_bytes + ring + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
+        c.threads = TC + 32;
+        c.consumers = TC;
+        const int per_sm = std::max(1, smem_sm / (c.smem + 1024));
+        c.grid = std::min(nsl, ctx->num_sms * per_sm);
+        if (env_int("DD_APPLY_GRID", 0) > 0) c.grid = std::min(nsl, env_int("DD_APPLY_GRID", 0));
+        cudaFuncSetAttribute(pick_ring(ring, spin), cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
+        return DD_OK;
+    };
+    if (ctx->variants & DD_LEVELSET) {
+        dd_status st = choose(ctx->cfg_lvl, false, ctx->slab_lvl.max_rec_bytes);
+        if (st != DD_OK) return st;
+    }
+    if (ctx->variants & DD_SPINLOOP) {
+        dd_status st = choose(ctx->cfg_spin, true, ctx->slab_spin.max_rec_bytes);
+        if (st != DD_OK) return st;
+    }
+    return cudaGetLastError() == cudaSuccess ? DD_OK : DD_E_CUDA;
+}
+
+dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream) {
+    using namespace ddk;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int nsl = ctx->sub_last - ctx->sub_first;
+    if (nsl == 0) return DD_OK;
+    const int vec_bytes = ((24 * ctx->max_P + 127) / 128) * 128;
+    if (variant == 0) variant = DD_LEVELSET;
+    if (variant == DD_DIRECT) {
+        if (!(ctx->variants & (DD_DIRECT | DD_LEVELSET))) return DD_E_INVALID_ARG;
+        const LaunchCfg &c = ctx->cfg_direct;
+        k_apply_direct<false><<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+                                                                 nsl, r, z, vec_bytes);
+    } else if (variant == DD_LEVELSET) {
+        if (!(ctx->variants & DD_LEVELSET)) return DD_E_INVALID_ARG;
+        const LaunchCfg &c = ctx->cfg_lvl;
+        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+                                                                   nsl, r, z, vec_bytes);
+    } else if (variant == DD_SPINLOOP) {
+        if (!(ctx->variants & DD_SPINLOOP)) return DD_E_INVALID_ARG;
+        const LaunchCfg &c = ctx->cfg_spin;
+        pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_spin.d_bytes, ctx->slab_spin.d_info,
+                                                                  nsl, r, z, vec_bytes);
+    } else {
+        set_error("dd_apply: unknown variant");
+        return DD_E_INVALID_ARG;
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("dd_apply launch: ") + cudaGetErrorString(e));
+        return DD_E_CUDA;
+    }
+    return DD_OK;
+}
+
+}  // namespace ddi

@@ -1,0 +1,134 @@
+// dd_internal.h -- product-internal declarations shared by the host setup
+// (setup.cpp), the C ABI (api.cpp) and the CUDA kernels (*.cu).
+// Never included by the oracle; the oracle never included here.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "dd.h"
+
+namespace ddi {
+
+// ---------------------------------------------------------------------------
+// Factor-slab record format. One byte stream per
+// subdomain, records in consumption order, every record 16-byte aligned:
+//   RecHdr (16 B)
+//   uint16 cnt[K]            rows having more than k blocks (jagged diagonal)
+//   uint16 rows[w]           local row ids, sorted by block count descending
+//   (pad to 8 B)
+//   [U records] double dinv[9][w]          structure of arrays
+//   uint16 col[nnz_rec]      k-major: k = 0 block of every row, then k = 1 ...
+//   (pad to 8 B)
+//   double val[nnz_rec][9] as 9 planes per k: val_k[v][cnt_k]
+// ---------------------------------------------------------------------------
+struct RecHdr {
+    uint16_t w;       // rows in this record
+    uint16_t K;       // max blocks per row (L: strictly lower, U: strictly upper)
+    uint16_t flags;   // REC_BARRIER | REC_UPPER | REC_LAST
+    uint16_t nnz;     // blocks in this record (sum of cnt)
+    uint32_t bytes;   // total record bytes (multiple of 16)
+    uint32_t off_val; // byte offset of val[] from the record start
+};
+static_assert(sizeof(RecHdr) == 16, "RecHdr must be 16 bytes");
+
+enum : uint16_t { REC_BARRIER = 1, REC_UPPER = 2, REC_LAST = 4 };
+
+// Per-subdomain descriptor (device array, one per local subdomain).
+struct SubInfo {
+    int64_t stream_off;   // byte offset of the subdomain's record stream
+    int32_t stream_bytes; // multiple of 16
+    int32_t row0;         // first local block row
+    int32_t nrows;        // P_s
+    int32_t n_rec;        // number of records
+};
+static_assert(sizeof(SubInfo) == 24, "SubInfo layout");
+
+// Sliced-ELL SpMV operand: slices of 32 consecutive rows, slot (k, lane) of
+// slice s at slot_ptr[s] + 32*k + lane; values as 9 planes of 32 per k.
+struct SpmvDev {
+    int64_t n_slices = 0;
+    int64_t n_slots = 0;
+    int64_t *slot_ptr = nullptr;  // [n_slices + 1]
+    int32_t *cols = nullptr;      // [n_slots], -1 = padding
+    double *vals = nullptr;       // [9 * n_slots]
+};
+
+struct Slab {
+    std::vector<uint8_t> bytes;   // host copy (all local subdomains)
+    std::vector<SubInfo> info;
+    int32_t rows_per_rec = 128;
+    int64_t max_rec_bytes = 0;
+    uint8_t *d_bytes = nullptr;
+    SubInfo *d_info = nullptr;
+};
+
+struct LaunchCfg {
+    int grid = 0, threads = 0, smem = 0, ring = 0, consumers = 0;
+};
+
+}  // namespace ddi
+
+struct dd_ctx {
+    // --- topology
+    int device = 0, rank = 0, world = 1;
+    bool host_only = false;
+    // --- global partition
+    int64_t N = 0;                 // global block rows
+    int64_t nnzb_A = 0;            // nnzb of A (= A_r)
+    int64_t nnzb_dd = 0;           // nnzb after the drop (global)
+    int32_t n_sub = 0;             // global subdomains
+    std::vector<int32_t> labels;   // [N] original order
+    std::vector<int32_t> new_to_old, old_to_new;
+    std::vector<int64_t> sub_ptr;  // [n_sub + 1] reordered rows
+    // --- this rank
+    int32_t sub_first = 0, sub_last = 0;  // local subdomains [first, last)
+    int64_t row_first = 0, n_local = 0;   // reordered global rows
+    int32_t max_P = 0;
+    // factors of the local rows (local numbering)
+    std::vector<int64_t> Lrp, Urp;
+    std::vector<int32_t> Lci, Uci;
+    std::vector<double> Lv, Uv, Dinv;
+    std::vector<int32_t> hmapL, hmapU;
+    int32_t max_lev_L = 0, max_lev_U = 0;
+    // local rows of A_r, columns in local+ghost numbering
+    std::vector<int64_t> Arp;
+    std::vector<int32_t> Aci;
+    std::vector<double> Av;
+    std::vector<int64_t> ghost_rows;   // reordered global ids, ascending
+    std::vector<int32_t> ghost_owner;
+    // halo send lists per peer (local row ids) and recv counts per peer
+    std::vector<std::vector<int32_t>> send_rows;  // [world]
+    std::vector<int64_t> recv_off;                // [world + 1] into ghost block
+    // slabs
+    ddi::Slab slab_lvl, slab_spin;
+    int32_t variants = 0;
+    ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct;
+    // spmv
+    ddi::SpmvDev spmv;
+    int64_t spmv_bytes = 0;
+    // timings
+    double setup_ms[6] = {0, 0, 0, 0, 0, 0};
+    // --- device state
+    void *d_new_to_old_local = nullptr;  // int32 [n_local]: global orig row of local row
+    double *d_stage = nullptr;           // staging for permute (3N doubles)
+    double *d_xghost = nullptr;          // spmv input with ghost space (world>1)
+    double *d_sendbuf = nullptr;
+    void *dev_ws = nullptr;              // BiCGSTAB workspace (api.cpp)
+    void *nccl = nullptr;                // ncclComm_t
+    double *h_pinned = nullptr;          // small pinned scalars
+    int num_sms = 148;
+};
+
+namespace ddi {
+// setup.cpp
+dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o);
+void set_error(const std::string &msg);
+double now_ms();
+
+// kernels (apply.cu / spmv.cu / blas1.cu)
+dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream);
+dd_status apply_prepare(dd_ctx *ctx);  // choose launch cfgs, set smem attributes
+void spmv_launch(const dd_ctx *ctx, const double *x, double *y, void *stream);
+}  // namespace ddi

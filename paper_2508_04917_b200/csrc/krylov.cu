@@ -1,0 +1,379 @@
+// krylov.cu -- BSR3 SpMV (sliced ELL, fused double-double dot epilogues),
+// BLAS-1 updates with fused dots, deterministic last-block reductions and
+// permutation gather/scatter for the right-preconditioned BiCGSTAB
+// (Alg. 1 P:135-165 with K1 = I, K2 = M; DESIGN.md sec. 4 arithmetic order).
+//
+// Reductions: every thread accumulates Dot2 pairs (s, c) over its elements in
+// a fixed order; blocks combine with a fixed shuffle tree; the last block to
+// finish combines the block partials in block order. For a fixed grid the
+// result is deterministic; it equals the oracle's sequential Dot2 after the
+// final rounding except in rare straddling cases.
+#include <cuda_runtime.h>
+
+#include "dd_internal.h"
+#include "krylov.cuh"
+
+namespace ddk {
+
+struct DD {
+    double s, c;
+};
+
+__device__ __forceinline__ void dot2_acc(double &s, double &c, double a, double b) {
+    const double p = a * b;
+    const double q = __fma_rn(a, b, -p);
+    const double t = s + p;
+    const double bb = t - s;
+    const double r = (s - (t - bb)) + (p - bb);
+    s = t;
+    c = c + (q + r);
+}
+
+__device__ __forceinline__ DD dd_plus(DD x, DD y) {
+    const double t = x.s + y.s;
+    const double bb = t - x.s;
+    const double e = (x.s - (t - bb)) + (y.s - bb);
+    return DD{t, (x.c + y.c) + e};
+}
+
+__device__ __forceinline__ DD shfl_xor_dd(DD v, int m) {
+    return DD{__shfl_xor_sync(0xffffffffu, v.s, m), __shfl_xor_sync(0xffffffffu, v.c, m)};
+}
+
+__device__ __forceinline__ DD warp_reduce_dd(DD v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v = dd_plus(v, shfl_xor_dd(v, m));
+    return v;
+}
+
+// ---------------------------------------------------------------- finalize
+__device__ __forceinline__ void finalize(double *sc, int op, const double *val) {
+    switch (op) {
+        case FIN_INIT:  // ||r0||^2 and rho_1 = rh.r = r.r
+            sc[S_RR] = val[0];
+            sc[S_N0SQ] = val[0];
+            sc[S_RHO] = val[0];
+            break;
+        case FIN_ALPHA:
+            sc[S_SIGMA] = val[0];
+            sc[S_ALPHA] = sc[S_RHO] / val[0];
+            break;
+        case FIN_SS:
+            sc[S_SS] = val[0];
+            break;
+        case FIN_OMEGA:
+            sc[S_TS] = val[0];
+            sc[S_TT] = val[1];
+            sc[S_OMEGA] = val[0] / val[1];
+            break;
+        case FIN_RHO:
+            sc[S_RR] = val[0];
+            sc[S_RHO_PREV] = sc[S_RHO];
+            sc[S_RHO] = val[1];
+            break;
+        case FIN_RESID:
+            sc[S_RES_TT] = val[0];
+            sc[S_RES_BB] = val[1];
+            break;
+        default:
+            break;
+    }
+}
+
+// Block-reduce NV DD values, write this block's partials, and let the last
+// block combine all partials in block order; returns true in thread 0 of the
+// last block, which then holds the combined (s, c) pairs in out[].
+template <int NV>
+__device__ __forceinline__ bool grid_reduce(DD (&v)[NV], DD *partials, unsigned int *counter, DD (&out)[NV]) {
+    __shared__ DD sh[NV][32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        DD w = warp_reduce_dd(v[q]);
+        if (lane == 0) sh[q][wid] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            DD acc = sh[q][0];
+            for (int w = 1; w < nw; ++w) acc = dd_plus(acc, sh[q][w]);
+            partials[blockIdx.x * NV + q] = acc;
+        }
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            DD acc{0.0, 0.0};
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                const double2 pv = __ldcg(reinterpret_cast<const double2 *>(&partials[b * NV + q]));
+                acc = dd_plus(acc, DD{pv.x, pv.y});
+            }
+            out[q] = warp_reduce_dd(acc);
+        }
+        if (lane == 0) *counter = 0u;
+    }
+    return threadIdx.x == 0;
+}
+
+// Deliver reduced values: finalize now (world == 1) or publish the rank-local
+// (s, c) pairs for the NCCL all-gather (world > 1).
+template <int NV>
+__device__ __forceinline__ void deliver(const RedArgs &ra, int op, const DD (&out)[NV]) {
+    if (ra.finalize) {
+        double vals[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) vals[q] = out[q].s + out[q].c;
+        finalize(ra.sc, op, vals);
+    } else {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            ra.loc[2 * q] = out[q].s;
+            ra.loc[2 * q + 1] = out[q].c;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- SpMV
+// One warp per 32-row slice; thread = block row; 3 FMA chains per thread.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_spmv(int64_t n_rows, int64_t n_slices, const int64_t *__restrict__ slot_ptr,
+                                              const int32_t *__restrict__ cols, const double *__restrict__ vals,
+                                              const double *__restrict__ x, const double *__restrict__ xg,
+                                              double *__restrict__ y, const double *__restrict__ aux, RedArgs ra) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    DD d0{0.0, 0.0}, d1{0.0, 0.0};
+    for (int64_t sl = warp0; sl < n_slices; sl += nwarps) {
+        const int64_t base = slot_ptr[sl];
+        const int K = (int)((slot_ptr[sl + 1] - base) >> 5);
+        const int64_t row = 32 * sl + lane;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const int64_t slot = base + 32 * k + lane;
+            const int32_t j = __ldg(cols + slot);
+            if (j < 0) continue;
+            const double *vb = vals + 9 * (base + 32 * k) + lane;
+            double b[9];
+#pragma unroll
+            for (int v = 0; v < 9; ++v) b[v] = __ldg(vb + 32 * v);
+            // local columns < n_rows, ghost (halo) columns after them (sec. 8e)
+            const double *xp = j < n_rows ? x + 3 * (int64_t)j : xg + 3 * ((int64_t)j - n_rows);
+            const double x0 = __ldg(xp), x1 = __ldg(xp + 1), x2 = __ldg(xp + 2);
+            a0 = __fma_rn(b[0], x0, a0);
+            a0 = __fma_rn(b[1], x1, a0);
+            a0 = __fma_rn(b[2], x2, a0);
+            a1 = __fma_rn(b[3], x0, a1);
+            a1 = __fma_rn(b[4], x1, a1);
+            a1 = __fma_rn(b[5], x2, a1);
+            a2 = __fma_rn(b[6], x0, a2);
+            a2 = __fma_rn(b[7], x1, a2);
+            a2 = __fma_rn(b[8], x2, a2);
+        }
+        if (row < n_rows) {
+            y[3 * row] = a0;
+            y[3 * row + 1] = a1;
+            y[3 * row + 2] = a2;
+            if (MODE == SPMV_SIGMA) {  // aux = rh : rh . y
+                dot2_acc(d0.s, d0.c, aux[3 * row], a0);
+                dot2_acc(d0.s, d0.c, aux[3 * row + 1], a1);
+                dot2_acc(d0.s, d0.c, aux[3 * row + 2], a2);
+            } else if (MODE == SPMV_TS_TT) {  // aux = s : t.s and t.t
+                dot2_acc(d0.s, d0.c, a0, aux[3 * row]);
+                dot2_acc(d0.s, d0.c, a1, aux[3 * row + 1]);
+                dot2_acc(d0.s, d0.c, a2, aux[3 * row + 2]);
+                dot2_acc(d1.s, d1.c, a0, a0);
+                dot2_acc(d1.s, d1.c, a1, a1);
+                dot2_acc(d1.s, d1.c, a2, a2);
+            }
+        }
+    }
+    if (MODE == SPMV_SIGMA) {
+        DD v[1] = {d0}, out[1];
+        if (grid_reduce<1>(v, ra.partials, ra.counter, out)) deliver<1>(ra, FIN_ALPHA, out);
+    } else if (MODE == SPMV_TS_TT) {
+        DD v[2] = {d0, d1}, out[2];
+        if (grid_reduce<2>(v, ra.partials, ra.counter, out)) deliver<2>(ra, FIN_OMEGA, out);
+    }
+}
+
+// ------------------------------------------------------------------ BLAS-1
+// r = b - t; rh = r; partial r.r
+__global__ void __launch_bounds__(256) k_init_r(int64_t m, const double *__restrict__ b, const double *__restrict__ t,
+                                                double *__restrict__ r, double *__restrict__ rh, RedArgs ra) {
+    DD d{0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = b[i] - t[i];
+        r[i] = v;
+        rh[i] = v;
+        dot2_acc(d.s, d.c, v, v);
+    }
+    DD v[1] = {d}, out[1];
+    if (grid_reduce<1>(v, ra.partials, ra.counter, out)) deliver<1>(ra, FIN_INIT, out);
+}
+
+// p = r (first) or p = fma(beta, fma(-omega, v, p), r), beta = (rho/rho_prev)*(alpha/omega)
+__global__ void __launch_bounds__(256) k_update_p(int64_t m, int first, const double *__restrict__ r,
+                                                  const double *__restrict__ v, double *__restrict__ p,
+                                                  const double *__restrict__ sc) {
+    const double omega = sc[S_OMEGA];
+    const double beta = (sc[S_RHO] / sc[S_RHO_PREV]) * (sc[S_ALPHA] / omega);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (first) p[i] = r[i];
+        else p[i] = __fma_rn(beta, __fma_rn(-omega, v[i], p[i]), r[i]);
+    }
+}
+
+// s = fma(-alpha, v, r); partial s.s
+__global__ void __launch_bounds__(256) k_update_s(int64_t m, const double *__restrict__ r, const double *__restrict__ v,
+                                                  double *__restrict__ s, RedArgs ra) {
+    const double alpha = ra.sc[S_ALPHA];
+    DD d{0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double sv = __fma_rn(-alpha, v[i], r[i]);
+        s[i] = sv;
+        dot2_acc(d.s, d.c, sv, sv);
+    }
+    DD vv[1] = {d}, out[1];
+    if (grid_reduce<1>(vv, ra.partials, ra.counter, out)) deliver<1>(ra, FIN_SS, out);
+}
+
+// x = fma(alpha, ph, x)   (half-step exit)
+__global__ void __launch_bounds__(256) k_update_x_half(int64_t m, const double *__restrict__ ph, double *__restrict__ x,
+                                                       const double *__restrict__ sc) {
+    const double alpha = sc[S_ALPHA];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __fma_rn(alpha, ph[i], x[i]);
+}
+
+// x = fma(omega, sh, fma(alpha, ph, x)); r = fma(-omega, t, s); partials r.r, rh.r
+// Skipped entirely when tau = t.t < 1e-30 (breakdown, R25): x keeps the last iterate.
+__global__ void __launch_bounds__(256) k_update_xr(int64_t m, const double *__restrict__ ph,
+                                                   const double *__restrict__ sh, const double *__restrict__ s,
+                                                   const double *__restrict__ t, const double *__restrict__ rh,
+                                                   double *__restrict__ x, double *__restrict__ r, RedArgs ra) {
+    const double tt = ra.sc[S_TT];
+    const bool skip = !(tt >= 1e-30);
+    const double alpha = ra.sc[S_ALPHA], omega = ra.sc[S_OMEGA];
+    DD d0{0.0, 0.0}, d1{0.0, 0.0};
+    if (!skip) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            x[i] = __fma_rn(omega, sh[i], __fma_rn(alpha, ph[i], x[i]));
+            const double rv = __fma_rn(-omega, t[i], s[i]);
+            r[i] = rv;
+            dot2_acc(d0.s, d0.c, rv, rv);
+            dot2_acc(d1.s, d1.c, rh[i], rv);
+        }
+    }
+    DD v[2] = {d0, d1}, out[2];
+    if (grid_reduce<2>(v, ra.partials, ra.counter, out) && !skip) deliver<2>(ra, FIN_RHO, out);
+}
+
+// t = b - t; partials t.t, b.b (true residual)
+__global__ void __launch_bounds__(256) k_resid(int64_t m, const double *__restrict__ b, double *__restrict__ t,
+                                               RedArgs ra) {
+    DD d0{0.0, 0.0}, d1{0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = b[i] - t[i];
+        t[i] = v;
+        dot2_acc(d0.s, d0.c, v, v);
+        dot2_acc(d1.s, d1.c, b[i], b[i]);
+    }
+    DD v[2] = {d0, d1}, out[2];
+    if (grid_reduce<2>(v, ra.partials, ra.counter, out)) deliver<2>(ra, FIN_RESID, out);
+}
+
+// multi-rank: combine the gathered per-rank values (in rank order) and finalize
+__global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, double *sc, int op) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double out[2] = {0.0, 0.0};
+    for (int q = 0; q < nv; ++q) {
+        DD acc{0.0, 0.0};
+        for (int rr = 0; rr < world; ++rr) acc = dd_plus(acc, DD{gathered[rr * 2 * nv + 2 * q], gathered[rr * 2 * nv + 2 * q + 1]});
+        out[q] = acc.s + acc.c;
+    }
+    finalize(sc, op, out);
+}
+
+// permutation helpers: out[3 li + c] = in[3 idx[li] + c] and the reverse
+__global__ void k_gather3(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
+                          double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[3 * (int64_t)idx[i / 3] + i % 3];
+}
+
+__global__ void k_scatter3(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
+                           double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[3 * (int64_t)idx[i / 3] + i % 3] = in[i];
+}
+
+}  // namespace ddk
+
+// ---------------------------------------------------------------- launchers
+namespace ddk {
+
+void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
+                 const RedArgs &ra, cudaStream_t st) {
+    const auto &S = ctx->spmv;
+    const int grid = ctx->num_sms * 8;  // fixed: determinism of the fused dots
+    switch (mode) {
+        case SPMV_PLAIN:
+            k_spmv<SPMV_PLAIN><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
+            break;
+        case SPMV_SIGMA:
+            k_spmv<SPMV_SIGMA><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
+            break;
+        case SPMV_TS_TT:
+            k_spmv<SPMV_TS_TT><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
+            break;
+    }
+}
+
+int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 4; }
+
+void launch_init_r(const dd_ctx *ctx, int64_t m, const double *b, const double *t, double *r, double *rh,
+                   const RedArgs &ra, cudaStream_t st) {
+    k_init_r<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, r, rh, ra);
+}
+void launch_update_p(const dd_ctx *ctx, int64_t m, int first, const double *r, const double *v, double *p,
+                     const double *sc, cudaStream_t st) {
+    k_update_p<<<blas_grid(ctx), 256, 0, st>>>(m, first, r, v, p, sc);
+}
+void launch_update_s(const dd_ctx *ctx, int64_t m, const double *r, const double *v, double *s, const RedArgs &ra,
+                     cudaStream_t st) {
+    k_update_s<<<blas_grid(ctx), 256, 0, st>>>(m, r, v, s, ra);
+}
+void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc,
+                          cudaStream_t st) {
+    k_update_x_half<<<blas_grid(ctx), 256, 0, st>>>(m, ph, x, sc);
+}
+void launch_update_xr(const dd_ctx *ctx, int64_t m, const double *ph, const double *sh, const double *s,
+                      const double *t, const double *rh, double *x, double *r, const RedArgs &ra, cudaStream_t st) {
+    k_update_xr<<<blas_grid(ctx), 256, 0, st>>>(m, ph, sh, s, t, rh, x, r, ra);
+}
+void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, const RedArgs &ra, cudaStream_t st) {
+    k_resid<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, ra);
+}
+void launch_finalize_gathered(int world, int nv, const double *gathered, double *sc, int op, cudaStream_t st) {
+    k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, sc, op);
+}
+void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st) {
+    k_gather3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+}
+void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out,
+                     cudaStream_t st) {
+    k_scatter3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+}
+size_t partials_bytes(const dd_ctx *ctx) { return sizeof(DD) * 2 * (size_t)(ctx->num_sms * 8); }
+
+}  // namespace ddk

@@ -1,0 +1,633 @@
+// setup.cpp -- host-side setup of the decomposed ILDU0 preconditioner
+// (product code; independent of oracle/). Steps, in the paper's order:
+//   Alg. 2 geometric cuts or contiguous chunks (R26)
+//   stable grouping permutation (R6, R7)
+//   Alg. 3 block reorder of this rank's rows (R8)
+//   drop of inter-subdomain blocks (R9)
+//   block ILU0 + ILDU0 per subdomain (Alg. 7, R11-R15)
+//   longest-path level sets per subdomain (Alg. 5 semantics P:448-508, R16)
+//   packing of the level-ordered factor slabs (B200 design)
+//   sliced-ELL SpMV operand of A_r with halo numbering (sec. 8e)
+// Floating point follows DESIGN.md sec. 4 (explicit std::fma, compiled with
+// -ffp-contract=off) so the factors equal the oracle's bit for bit.
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "dd_internal.h"
+
+namespace ddi {
+
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+const char *last_error_c() { return g_err.c_str(); }
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------ 3x3 algebra
+// C = A*B, C_rc = fma(a_r2, b_2c, fma(a_r1, b_1c, a_r0*b_0c)). C may alias A.
+static inline void blk_mul(const double *A, const double *B, double *C) {
+    double t[9];
+    for (int r = 0; r < 3; ++r) {
+        const double a0 = A[3 * r], a1 = A[3 * r + 1], a2 = A[3 * r + 2];
+        for (int c = 0; c < 3; ++c) t[3 * r + c] = std::fma(a2, B[6 + c], std::fma(a1, B[3 + c], a0 * B[c]));
+    }
+    std::memcpy(C, t, sizeof t);
+}
+
+// W -= L*U entrywise as three chained fmas in d = 0, 1, 2 order.
+static inline void blk_sub_mul(double *W, const double *L, const double *U) {
+    for (int r = 0; r < 3; ++r) {
+        const double l0 = L[3 * r], l1 = L[3 * r + 1], l2 = L[3 * r + 2];
+        for (int c = 0; c < 3; ++c) {
+            double w = W[3 * r + c];
+            w = std::fma(-l0, U[c], w);
+            w = std::fma(-l1, U[3 + c], w);
+            w = std::fma(-l2, U[6 + c], w);
+            W[3 * r + c] = w;
+        }
+    }
+}
+
+// adjugate / determinant; false if |det| < floor (or NaN).
+static inline bool blk_inv(const double *m, double floor_, double *out) {
+    const double c00 = std::fma(m[4], m[8], -(m[5] * m[7]));
+    const double c01 = std::fma(m[5], m[6], -(m[3] * m[8]));
+    const double c02 = std::fma(m[3], m[7], -(m[4] * m[6]));
+    const double c10 = std::fma(m[2], m[7], -(m[1] * m[8]));
+    const double c11 = std::fma(m[0], m[8], -(m[2] * m[6]));
+    const double c12 = std::fma(m[1], m[6], -(m[0] * m[7]));
+    const double c20 = std::fma(m[1], m[5], -(m[2] * m[4]));
+    const double c21 = std::fma(m[2], m[3], -(m[0] * m[5]));
+    const double c22 = std::fma(m[0], m[4], -(m[1] * m[3]));
+    const double det = std::fma(m[0], c00, std::fma(m[1], c01, m[2] * c02));
+    if (!(std::fabs(det) >= floor_)) return false;
+    const double rd = 1.0 / det;
+    out[0] = c00 * rd; out[1] = c10 * rd; out[2] = c20 * rd;
+    out[3] = c01 * rd; out[4] = c11 * rd; out[5] = c21 * rd;
+    out[6] = c02 * rd; out[7] = c12 * rd; out[8] = c22 * rd;
+    return true;
+}
+
+// ---------------------------------------------------------- slab packing
+namespace {
+
+struct RowRef {
+    int32_t row;          // subdomain-local row id
+    int32_t nblk;         // blocks in this triangle
+    const int32_t *cols;  // rank-local column ids (ascending)
+    const double *vals;   // 9 per block
+    const double *dinv;   // U records only
+};
+
+inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Append one record for `rows` (already sorted by nblk descending, stable).
+void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool upper,
+                uint16_t flags, int32_t col_base, int64_t &max_rec) {
+    const int w = (int)rows.size();
+    int K = 0;
+    int nnz = 0;
+    for (auto &r : rows) {
+        K = std::max(K, r.nblk);
+        nnz += r.nblk;
+    }
+    const size_t off_rows = 16 + 2 * (size_t)K;
+    const size_t off_dinv = al(off_rows + 2 * (size_t)w, 8);
+    const size_t off_cols = off_dinv + (upper ? 72 * (size_t)w : 0);
+    const size_t off_val = al(off_cols + 2 * (size_t)nnz, 8);
+    const size_t bytes = al(off_val + 72 * (size_t)nnz, 16);
+    const size_t base = out.size();
+    out.resize(base + bytes, 0);
+    uint8_t *p = out.data() + base;
+    RecHdr h;
+    h.w = (uint16_t)w;
+    h.K = (uint16_t)K;
+    h.flags = (uint16_t)(flags | (upper ? REC_UPPER : 0));
+    h.nnz = (uint16_t)nnz;
+    h.bytes = (uint32_t)bytes;
+    h.off_val = (uint32_t)off_val;
+    std::memcpy(p, &h, sizeof h);
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(p + 16);
+    for (int k = 0; k < K; ++k) {
+        int c = 0;
+        for (auto &r : rows) c += (r.nblk > k);
+        cnt[k] = (uint16_t)c;
+    }
+    uint16_t *rid = reinterpret_cast<uint16_t *>(p + off_rows);
+    for (int t = 0; t < w; ++t) rid[t] = (uint16_t)rows[t].row;
+    if (upper) {
+        double *dv = reinterpret_cast<double *>(p + off_dinv);
+        for (int v = 0; v < 9; ++v)
+            for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
+    }
+    uint16_t *cc = reinterpret_cast<uint16_t *>(p + off_cols);
+    double *vv = reinterpret_cast<double *>(p + off_val);
+    size_t pos = 0;
+    for (int k = 0; k < K; ++k) {
+        const int ck = cnt[k];
+        for (int t = 0; t < ck; ++t) cc[pos + t] = (uint16_t)(rows[t].cols[k] - col_base);
+        for (int v = 0; v < 9; ++v)
+            for (int t = 0; t < ck; ++t) vv[9 * pos + (size_t)v * ck + t] = rows[t].vals[9 * (size_t)k + v];
+        pos += ck;
+    }
+    max_rec = std::max<int64_t>(max_rec, (int64_t)bytes);
+}
+
+// groups: sequences of rows; barrier after each group with barrier flag.
+void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &groups,
+                 const std::vector<bool> &barrier, bool upper, int rmax, int32_t col_base,
+                 int32_t &n_rec, int64_t &max_rec, bool last_section) {
+    for (size_t g = 0; g < groups.size(); ++g) {
+        auto &rows = groups[g];
+        std::stable_sort(rows.begin(), rows.end(),
+                         [](const RowRef &a, const RowRef &b) { return a.nblk > b.nblk; });
+        const int w = (int)rows.size();
+        for (int s = 0; s < w; s += rmax) {
+            const int e = std::min(w, s + rmax);
+            std::vector<RowRef> part(rows.begin() + s, rows.begin() + e);
+            uint16_t fl = 0;
+            if (e == w && barrier[g]) fl |= REC_BARRIER;
+            if (last_section && g + 1 == groups.size() && e == w) fl |= REC_LAST;
+            put_record(out, part, upper, fl, col_base, max_rec);
+            ++n_rec;
+        }
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host setup
+dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
+    const double t0 = now_ms();
+    const int64_t N = A->n_block_rows;
+    if (N <= 0 || !A->row_ptr || !A->col_idx || !A->vals || A->nnzb < 0) {
+        set_error("dd_setup: empty or NULL matrix");
+        return DD_E_INVALID_ARG;
+    }
+    if (N > INT32_MAX - 1) {
+        set_error("dd_setup: more than 2^31-1 block rows");
+        return DD_E_INVALID_ARG;
+    }
+    const int64_t *rp = A->row_ptr;
+    const int32_t *ci = A->col_idx;
+    const double *av = A->vals;
+    if (rp[0] != 0 || rp[N] != A->nnzb) {
+        set_error("dd_setup: row_ptr[0] != 0 or row_ptr[n] != nnzb");
+        return DD_E_INVALID_ARG;
+    }
+    if (o->n_threads > 0) omp_set_num_threads(o->n_threads);
+    ctx->N = N;
+    ctx->nnzb_A = A->nnzb;
+
+    // ---- validate: monotone row_ptr, in-range, strictly ascending, diagonal
+    int64_t bad_unsorted = INT64_MAX, bad_diag = INT64_MAX, bad_range = INT64_MAX;
+#pragma omp parallel for schedule(static) reduction(min : bad_unsorted, bad_diag, bad_range)
+    for (int64_t i = 0; i < N; ++i) {
+        if (rp[i + 1] < rp[i]) {
+            bad_range = std::min(bad_range, i);
+            continue;
+        }
+        bool diag = false;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            if (ci[p] < 0 || ci[p] >= N) bad_range = std::min(bad_range, i);
+            if (p > rp[i] && ci[p] <= ci[p - 1]) bad_unsorted = std::min(bad_unsorted, i);
+            diag |= (ci[p] == i);
+        }
+        if (!diag) bad_diag = std::min(bad_diag, i);
+    }
+    if (bad_range != INT64_MAX) {
+        set_error("dd_setup: bad row_ptr or column out of range at row " + std::to_string(bad_range));
+        return DD_E_INVALID_ARG;
+    }
+    if (bad_unsorted != INT64_MAX) {
+        set_error("dd_setup: columns not strictly ascending in row " + std::to_string(bad_unsorted));
+        return DD_E_UNSORTED_OR_DUP;
+    }
+    if (bad_diag != INT64_MAX) {
+        set_error("dd_setup: missing diagonal block in row " + std::to_string(bad_diag));
+        return DD_E_MISSING_DIAG;
+    }
+
+    // ---- labels: Alg. 2 or contiguous chunks
+    ctx->labels.assign(N, 0);
+    if (o->grid) {
+        const dd_grid g = *o->grid;
+        if (g.nx <= 0 || g.ny <= 0 || g.nz <= 0 || g.tx <= 0 || g.ty <= 0 || g.tz <= 0 ||
+            (int64_t)g.nx * g.ny * g.nz != N) {
+            set_error("dd_setup: grid does not match the matrix");
+            return DD_E_INVALID_ARG;
+        }
+        if (g.nx % g.tx || g.ny % g.ty || g.nz % g.tz) {
+            set_error("dd_setup: grid not divisible by tile dims");
+            return DD_E_GRID_NOT_DIVISIBLE;
+        }
+        const int64_t bx = g.nx / g.tx, by = g.ny / g.ty;
+#pragma omp parallel for schedule(static)
+        for (int64_t gidx = 0; gidx < N; ++gidx) {
+            const int64_t i = gidx % g.nx, j = (gidx / g.nx) % g.ny, k = gidx / ((int64_t)g.nx * g.ny);
+            ctx->labels[gidx] = (int32_t)(i / g.tx + bx * (j / g.ty + by * (k / g.tz)));
+        }
+    } else {
+        if (o->subdomain_rows <= 0) {
+            set_error("dd_setup: subdomain_rows must be > 0 without a grid");
+            return DD_E_INVALID_ARG;
+        }
+        const int64_t P = o->subdomain_rows;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < N; ++i) ctx->labels[i] = (int32_t)(i / P);
+    }
+    int32_t maxl = 0;
+    for (int64_t i = 0; i < N; ++i) maxl = std::max(maxl, ctx->labels[i]);
+    const int32_t n_sub = maxl + 1;
+    ctx->n_sub = n_sub;
+
+    // ---- stable grouping permutation (counting sort)
+    ctx->sub_ptr.assign((size_t)n_sub + 1, 0);
+    for (int64_t i = 0; i < N; ++i) ctx->sub_ptr[ctx->labels[i] + 1]++;
+    for (int32_t s = 0; s < n_sub; ++s) ctx->sub_ptr[s + 1] += ctx->sub_ptr[s];
+    ctx->new_to_old.assign(N, 0);
+    ctx->old_to_new.assign(N, 0);
+    {
+        std::vector<int64_t> fill(ctx->sub_ptr.begin(), ctx->sub_ptr.end() - 1);
+        for (int64_t i = 0; i < N; ++i) ctx->new_to_old[fill[ctx->labels[i]]++] = (int32_t)i;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < N; ++j) ctx->old_to_new[ctx->new_to_old[j]] = (int32_t)j;
+    int64_t maxP = 0;
+    for (int32_t s = 0; s < n_sub; ++s) maxP = std::max(maxP, ctx->sub_ptr[s + 1] - ctx->sub_ptr[s]);
+    if (maxP > 65535) {
+        set_error("dd_setup: subdomain larger than 65535 block rows");
+        return DD_E_SUBDOMAIN_TOO_LARGE;
+    }
+    ctx->max_P = (int32_t)maxP;
+
+    // ---- this rank's subdomains (count-balanced contiguous range, R32)
+    const int world = std::max(1, ctx->world), rank = ctx->rank;
+    ctx->sub_first = (int32_t)((int64_t)n_sub * rank / world);
+    ctx->sub_last = (int32_t)((int64_t)n_sub * (rank + 1) / world);
+    ctx->row_first = ctx->sub_ptr[ctx->sub_first];
+    const int64_t nl = ctx->sub_ptr[ctx->sub_last] - ctx->row_first;
+    ctx->n_local = nl;
+    const int64_t r0 = ctx->row_first;
+    const double t1 = now_ms();
+    ctx->setup_ms[0] = t1 - t0;
+
+    // ---- Alg. 3 reorder of the local rows (global reordered column ids)
+    std::vector<int64_t> &Arp = ctx->Arp;
+    Arp.assign(nl + 1, 0);
+    for (int64_t li = 0; li < nl; ++li) {
+        const int64_t m = ctx->new_to_old[r0 + li];
+        Arp[li + 1] = Arp[li] + (rp[m + 1] - rp[m]);
+    }
+    const int64_t nnz_loc = Arp[nl];
+    std::vector<int32_t> gcol(nnz_loc);
+    ctx->Av.assign(9 * nnz_loc, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t li = 0; li < nl; ++li) {
+        const int64_t m = ctx->new_to_old[r0 + li];
+        const int64_t nb = rp[m + 1] - rp[m];
+        int32_t idx[64];
+        int32_t nc[64];
+        std::vector<int32_t> big_idx, big_nc;
+        int32_t *ix = idx, *cc = nc;
+        if (nb > 64) {
+            big_idx.resize(nb);
+            big_nc.resize(nb);
+            ix = big_idx.data();
+            cc = big_nc.data();
+        }
+        for (int64_t t = 0; t < nb; ++t) {
+            ix[t] = (int32_t)t;
+            cc[t] = ctx->old_to_new[ci[rp[m] + t]];
+        }
+        std::sort(ix, ix + nb, [&](int32_t a, int32_t b) { return cc[a] < cc[b]; });
+        for (int64_t t = 0; t < nb; ++t) {
+            gcol[Arp[li] + t] = cc[ix[t]];
+            std::memcpy(&ctx->Av[9 * (Arp[li] + t)], &av[9 * (rp[m] + ix[t])], 9 * sizeof(double));
+        }
+    }
+    // global drop statistics (count of same-label blocks over all rows)
+    {
+        int64_t kept = 0;
+#pragma omp parallel for schedule(static) reduction(+ : kept)
+        for (int64_t i = 0; i < N; ++i)
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p) kept += (ctx->labels[i] == ctx->labels[ci[p]]);
+        ctx->nnzb_dd = kept;
+    }
+    // halo numbering: local columns 0..nl-1, ghosts nl.. (ascending global id)
+    {
+        std::vector<int32_t> gh;
+        for (int64_t p = 0; p < nnz_loc; ++p)
+            if (gcol[p] < r0 || gcol[p] >= r0 + nl) gh.push_back(gcol[p]);
+        std::sort(gh.begin(), gh.end());
+        gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
+        ctx->ghost_rows.assign(gh.begin(), gh.end());
+        ctx->ghost_owner.resize(gh.size());
+        for (size_t q = 0; q < gh.size(); ++q) {
+            // owner = rank whose subdomain range contains row gh[q]
+            const int64_t s = std::upper_bound(ctx->sub_ptr.begin(), ctx->sub_ptr.end(), (int64_t)gh[q]) -
+                              ctx->sub_ptr.begin() - 1;
+            int own = 0;
+            for (int rr = 0; rr < world; ++rr)
+                if (s >= (int64_t)n_sub * rr / world && s < (int64_t)n_sub * (rr + 1) / world) own = rr;
+            ctx->ghost_owner[q] = own;
+        }
+        ctx->recv_off.assign(world + 1, 0);
+        for (size_t q = 0; q < gh.size(); ++q) ctx->recv_off[ctx->ghost_owner[q] + 1]++;
+        for (int rr = 0; rr < world; ++rr) ctx->recv_off[rr + 1] += ctx->recv_off[rr];
+        // send lists: my rows that peer q reads (ascending = q's ghost order)
+        ctx->send_rows.assign(world, {});
+        for (int q = 0; q < world && world > 1; ++q) {
+            if (q == rank) continue;
+            const int64_t qa = ctx->sub_ptr[(int64_t)n_sub * q / world];
+            const int64_t qe = ctx->sub_ptr[(int64_t)n_sub * (q + 1) / world];
+            std::vector<int32_t> need;
+#pragma omp parallel
+            {
+                std::vector<int32_t> mine;
+#pragma omp for schedule(static) nowait
+                for (int64_t g = qa; g < qe; ++g) {
+                    const int64_t m = ctx->new_to_old[g];
+                    for (int64_t p = rp[m]; p < rp[m + 1]; ++p) {
+                        const int64_t c = ctx->old_to_new[ci[p]];
+                        if (c >= r0 && c < r0 + nl) mine.push_back((int32_t)(c - r0));
+                    }
+                }
+#pragma omp critical
+                need.insert(need.end(), mine.begin(), mine.end());
+            }
+            std::sort(need.begin(), need.end());
+            need.erase(std::unique(need.begin(), need.end()), need.end());
+            ctx->send_rows[q] = std::move(need);
+        }
+        ctx->Aci.assign(nnz_loc, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < nnz_loc; ++p) {
+            const int32_t g = gcol[p];
+            if (g >= r0 && g < r0 + nl)
+                ctx->Aci[p] = (int32_t)(g - r0);
+            else
+                ctx->Aci[p] = (int32_t)(nl + (std::lower_bound(gh.begin(), gh.end(), g) - gh.begin()));
+        }
+    }
+    const double t2 = now_ms();
+    ctx->setup_ms[1] = t2 - t1;
+
+    // ---- factor pattern sizes (drop: keep same-subdomain blocks)
+    const int32_t s0 = ctx->sub_first, s1 = ctx->sub_last, nsl = s1 - s0;
+    std::vector<int32_t> row_sub(nl);
+    for (int32_t s = s0; s < s1; ++s)
+        for (int64_t g = ctx->sub_ptr[s]; g < ctx->sub_ptr[s + 1]; ++g) row_sub[g - r0] = s;
+    ctx->Lrp.assign(nl + 1, 0);
+    ctx->Urp.assign(nl + 1, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t li = 0; li < nl; ++li) {
+        const int32_t s = row_sub[li];
+        const int64_t a = ctx->sub_ptr[s], e = ctx->sub_ptr[s + 1];
+        int64_t nL = 0, nU = 0;
+        for (int64_t p = Arp[li]; p < Arp[li + 1]; ++p) {
+            const int64_t g = gcol[p];
+            if (g >= a && g < e) {
+                if (g < r0 + li) ++nL;
+                if (g > r0 + li) ++nU;
+            }
+        }
+        ctx->Lrp[li + 1] = nL;
+        ctx->Urp[li + 1] = nU;
+    }
+    for (int64_t li = 0; li < nl; ++li) {
+        ctx->Lrp[li + 1] += ctx->Lrp[li];
+        ctx->Urp[li + 1] += ctx->Urp[li];
+    }
+    ctx->Lci.assign(ctx->Lrp[nl], 0);
+    ctx->Uci.assign(ctx->Urp[nl], 0);
+    ctx->Lv.assign(9 * ctx->Lrp[nl], 0.0);
+    ctx->Uv.assign(9 * ctx->Urp[nl], 0.0);
+    ctx->Dinv.assign(9 * nl, 0.0);
+    ctx->hmapL.assign(nl, 0);
+    ctx->hmapU.assign(nl, 0);
+
+    // ---- per-subdomain block ILU0 -> ILDU0 -> levels
+    const double floor_ = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
+    int64_t bad_pivot = INT64_MAX;
+#pragma omp parallel reduction(min : bad_pivot)
+    {
+        std::vector<int64_t> lrp;
+        std::vector<int32_t> lci;
+        std::vector<double> W;
+        std::vector<int64_t> ldg, pos;
+#pragma omp for schedule(dynamic, 1)
+        for (int32_t s = s0; s < s1; ++s) {
+            const int64_t a = ctx->sub_ptr[s], e = ctx->sub_ptr[s + 1], P = e - a;
+            const int64_t la = a - r0;  // local row of the first subdomain row
+            // subdomain-local CSR of A_dd
+            lrp.assign(P + 1, 0);
+            lci.clear();
+            W.clear();
+            for (int64_t i = 0; i < P; ++i) {
+                const int64_t li = la + i;
+                for (int64_t p = Arp[li]; p < Arp[li + 1]; ++p) {
+                    const int64_t g = gcol[p];
+                    if (g >= a && g < e) {
+                        lci.push_back((int32_t)(g - a));
+                        W.insert(W.end(), &ctx->Av[9 * p], &ctx->Av[9 * p] + 9);
+                    }
+                }
+                lrp[i + 1] = (int64_t)lci.size();
+            }
+            ldg.assign(P, -1);
+            for (int64_t i = 0; i < P; ++i)
+                for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p)
+                    if (lci[p] == i) ldg[i] = p;
+            pos.assign(P, -1);
+            bool failed = false;
+            for (int64_t i = 0; i < P && !failed; ++i) {
+                for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) pos[lci[p]] = p;
+                for (int64_t p = lrp[i]; p < ldg[i]; ++p) {
+                    const int64_t k = lci[p];
+                    // L_ik = W_ik * U_kk^-1 (right multiplication, R12)
+                    blk_mul(&W[9 * p], &ctx->Dinv[9 * (la + k)], &W[9 * p]);
+                    // W_ij -= L_ik U_kj for j in pattern(i) and (k,j) in U
+                    for (int64_t q = ldg[k] + 1; q < lrp[k + 1]; ++q) {
+                        const int64_t tgt = pos[lci[q]];
+                        if (tgt >= 0) blk_sub_mul(&W[9 * tgt], &W[9 * p], &W[9 * q]);
+                    }
+                }
+                if (!blk_inv(&W[9 * ldg[i]], floor_, &ctx->Dinv[9 * (la + i)])) {
+                    bad_pivot = std::min(bad_pivot, a + i);
+                    failed = true;
+                }
+                for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) pos[lci[p]] = -1;
+            }
+            if (failed) continue;
+            // scatter: L (strictly lower) and U_unit = Dinv_i * U_ij (j > i)
+            for (int64_t i = 0; i < P; ++i) {
+                const int64_t li = la + i;
+                int64_t qL = ctx->Lrp[li], qU = ctx->Urp[li];
+                for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) {
+                    if (lci[p] < i) {
+                        ctx->Lci[qL] = (int32_t)(la + lci[p]);
+                        std::memcpy(&ctx->Lv[9 * qL], &W[9 * p], 9 * sizeof(double));
+                        ++qL;
+                    } else if (lci[p] > i) {
+                        ctx->Uci[qU] = (int32_t)(la + lci[p]);
+                        blk_mul(&ctx->Dinv[9 * li], &W[9 * p], &ctx->Uv[9 * qU]);
+                        ++qU;
+                    }
+                }
+            }
+            // longest-path levels (Alg. 5 fixpoint == longest path, R16)
+            for (int64_t i = 0; i < P; ++i) {
+                const int64_t li = la + i;
+                int32_t h = 0;
+                for (int64_t q = ctx->Lrp[li]; q < ctx->Lrp[li + 1]; ++q) h = std::max(h, ctx->hmapL[ctx->Lci[q]] + 1);
+                ctx->hmapL[li] = h;
+            }
+            for (int64_t i = P - 1; i >= 0; --i) {
+                const int64_t li = la + i;
+                int32_t h = 0;
+                for (int64_t q = ctx->Urp[li]; q < ctx->Urp[li + 1]; ++q) h = std::max(h, ctx->hmapU[ctx->Uci[q]] + 1);
+                ctx->hmapU[li] = h;
+            }
+        }
+    }
+    const double t3 = now_ms();
+    ctx->setup_ms[2] = t3 - t2;
+    // global pivot status must agree across ranks; the API layer reduces it.
+    if (bad_pivot != INT64_MAX) {
+        set_error("dd_setup: singular pivot block (|det| < pivot_floor) at reordered row " +
+                  std::to_string(bad_pivot));
+        return DD_E_SINGULAR_PIVOT;
+    }
+    int32_t mL = 0, mU = 0;
+    for (int64_t li = 0; li < nl; ++li) {
+        mL = std::max(mL, ctx->hmapL[li]);
+        mU = std::max(mU, ctx->hmapU[li]);
+    }
+    ctx->max_lev_L = mL + 1;
+    ctx->max_lev_U = mU + 1;
+    const double t4 = now_ms();
+    ctx->setup_ms[3] = t4 - t3;
+
+    // ---- slab packing (level-set and/or spin-loop orders)
+    ctx->variants = o->variants ? o->variants : DD_LEVELSET;
+    // rows per record: the largest of 128/64/32/16 whose worst-case record
+    // (K blocks per row, U records carry Dinv) fits the staging ring that is
+    // left next to the subdomain vector (B200: 232448 B opt-in per CTA).
+    int32_t Kmax = 0;
+    for (int64_t li = 0; li < nl; ++li)
+        Kmax = std::max<int32_t>(Kmax, (int32_t)std::max(ctx->Lrp[li + 1] - ctx->Lrp[li], ctx->Urp[li + 1] - ctx->Urp[li]));
+    {
+        const int64_t vec = (24 * (int64_t)ctx->max_P + 127) / 128 * 128;
+        const int64_t avail = 232448 - vec - 2 * (int64_t)ctx->max_P - 1024;
+        int64_t ring = 131072;
+        while (ring > 16384 && ring > avail) ring /= 2;
+        const int64_t ch = ring >= 65536 ? 8192 : (ring >= 32768 ? 4096 : 2048);
+        int32_t rmax = 128;
+        auto est = [&](int64_t R) { return 16 + 2 * Kmax + 2 * R + 8 + 72 * R + R * Kmax * 74 + 32; };
+        while (rmax > 16 && est(rmax) + ch > ring) rmax /= 2;
+        ctx->slab_lvl.rows_per_rec = rmax;
+        ctx->slab_spin.rows_per_rec = rmax;
+    }
+    auto build_slab = [&](ddi::Slab &slab, bool spin) {
+        const int rmax = slab.rows_per_rec;
+        std::vector<std::vector<uint8_t>> per(nsl);
+        slab.info.assign(nsl, SubInfo{});
+        int64_t max_rec = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : max_rec)
+        for (int32_t q = 0; q < nsl; ++q) {
+            const int32_t s = s0 + q;
+            const int64_t a = ctx->sub_ptr[s], e = ctx->sub_ptr[s + 1], P = e - a;
+            const int64_t la = a - r0;
+            auto rowL = [&](int64_t i) {
+                const int64_t li = la + i;
+                return RowRef{(int32_t)i, (int32_t)(ctx->Lrp[li + 1] - ctx->Lrp[li]), &ctx->Lci[ctx->Lrp[li]],
+                              &ctx->Lv[9 * ctx->Lrp[li]], nullptr};
+            };
+            auto rowU = [&](int64_t i) {
+                const int64_t li = la + i;
+                return RowRef{(int32_t)i, (int32_t)(ctx->Urp[li + 1] - ctx->Urp[li]), &ctx->Uci[ctx->Urp[li]],
+                              &ctx->Uv[9 * ctx->Urp[li]], &ctx->Dinv[9 * li]};
+            };
+            std::vector<std::vector<RowRef>> gL, gU;
+            std::vector<bool> bL, bU;
+            if (!spin) {
+                int32_t hl = 0, hu = 0;
+                for (int64_t i = 0; i < P; ++i) {
+                    hl = std::max(hl, ctx->hmapL[la + i]);
+                    hu = std::max(hu, ctx->hmapU[la + i]);
+                }
+                gL.assign(hl + 1, {});
+                gU.assign(hu + 1, {});
+                for (int64_t i = 0; i < P; ++i) {
+                    if (ctx->hmapL[la + i] > 0) gL[ctx->hmapL[la + i]].push_back(rowL(i));
+                    gU[ctx->hmapU[la + i]].push_back(rowU(i));
+                }
+                // level 0 of L needs no work: z_i = r_i is already in shared memory
+                gL.erase(gL.begin());
+                bL.assign(gL.size(), true);
+                bU.assign(gU.size(), true);
+            } else {
+                for (int64_t i = 0; i < P; i += rmax) {
+                    gL.emplace_back();
+                    for (int64_t t = i; t < std::min(P, i + rmax); ++t) gL.back().push_back(rowL(t));
+                }
+                for (int64_t i = P - 1; i >= 0; i -= rmax) {
+                    gU.emplace_back();
+                    for (int64_t t = i; t > std::max<int64_t>(-1, i - rmax); --t) gU.back().push_back(rowU(t));
+                }
+                bL.assign(gL.size(), true);
+                bU.assign(gU.size(), true);
+            }
+            int32_t nrec = 0;
+            int64_t mr = 0;
+            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false);
+            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true);
+            slab.info[q].stream_bytes = (int32_t)per[q].size();
+            slab.info[q].row0 = (int32_t)la;
+            slab.info[q].nrows = (int32_t)P;
+            slab.info[q].n_rec = nrec;
+            max_rec = std::max(max_rec, mr);
+        }
+        int64_t off = 0;
+        for (int32_t q = 0; q < nsl; ++q) {
+            slab.info[q].stream_off = off;
+            off += slab.info[q].stream_bytes;
+        }
+        slab.bytes.resize(off);
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int32_t q = 0; q < nsl; ++q) {
+            std::memcpy(slab.bytes.data() + slab.info[q].stream_off, per[q].data(), per[q].size());
+            std::vector<uint8_t>().swap(per[q]);
+        }
+        slab.max_rec_bytes = max_rec;
+    };
+    if (ctx->variants & (DD_LEVELSET | DD_DIRECT)) build_slab(ctx->slab_lvl, false);
+    if (ctx->variants & DD_SPINLOOP) build_slab(ctx->slab_spin, true);
+
+    // ---- sliced-ELL SpMV operand
+    {
+        auto &S = ctx->spmv;
+        S.n_slices = (nl + 31) / 32;
+        std::vector<int64_t> sp(S.n_slices + 1, 0);
+        for (int64_t s = 0; s < S.n_slices; ++s) {
+            int64_t K = 0;
+            for (int64_t li = 32 * s; li < std::min(nl, 32 * s + 32); ++li) K = std::max(K, Arp[li + 1] - Arp[li]);
+            sp[s + 1] = sp[s] + 32 * K;
+        }
+        S.n_slots = sp[S.n_slices];
+        ctx->spmv_bytes = S.n_slots * (4 + 72) + 8 * (S.n_slices + 1);
+    }
+    ctx->setup_ms[4] = now_ms() - t4;
+    return DD_OK;
+}
+
+}  // namespace ddi

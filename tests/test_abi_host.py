@@ -1,0 +1,113 @@
+"""CPU tests of the product library: it loads, exports every symbol include/dd.h
+declares, and its host-side setup (run with host_only = 1, no device work)
+equals the oracle's setup bit for bit. No compute calls are made here."""
+import re
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2508_04917_b200 as dd
+from inputs.gen import laplacian_bsr3, random_block_grid, spe10_style_bsr3
+from tests.helpers import kron_blocks
+from tests.parity import assert_setup_bitwise
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built():
+    from paper_2508_04917_b200 import build
+    build.build()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "dd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dd_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = dd.lib()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), f"libdd.so does not export {s}"
+    assert sorted(dd.EXPORTS) == syms
+
+
+def test_no_device_is_an_error_not_a_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    rp, ci, v = laplacian_bsr3(4, 4, 4)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, v, P=8)
+    assert e.value.name == "DD_E_NO_DEVICE"
+
+
+CASES = {
+    "cfg1_16^3": (lambda: laplacian_bsr3(16, 16, 16), dict(grid=(16, 16, 16), tiles=(8, 8, 8))),
+    "cfg2a_64^3": (lambda: laplacian_bsr3(64, 64, 64), dict(grid=(64, 64, 64), tiles=(16, 16, 8))),
+    "random_blocks": (lambda: random_block_grid(12, 10, 8, seed=3), dict(grid=(12, 10, 8), tiles=(6, 5, 4))),
+    "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),
+    "P1": (lambda: random_block_grid(6, 5, 4, seed=6), dict(P=1)),
+    "one_subdomain": (lambda: random_block_grid(9, 8, 7, seed=7), dict(grid=(9, 8, 7), tiles=(9, 8, 7))),
+    "spe10_small": (lambda: spe10_style_bsr3(20, 40, 20, upper_ness_from=10)[:3],
+                    dict(grid=(20, 40, 20), tiles=(10, 20, 10))),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_host_setup_bitwise_vs_oracle(name):
+    gen, kw = CASES[name]
+    rp, ci, v = gen()
+    S = oracle.setup(rp, ci, v, **kw)
+    ctx = dd.dd_setup(rp, ci, v, host_only=True, variants=7, **kw)
+    assert_setup_bitwise(ctx, S)
+    st = ctx.stats()
+    # canonical apply bytes: 72(nL+nU+n) + 4(nL+nU) + 8(n+1) + 48n
+    n = S["n"]
+    rows = np.repeat(np.arange(n), np.diff(S["rp_d"]))
+    nLU = int(np.sum(S["ci_d"] != rows))
+    assert st["apply_canonical_bytes"] == 72 * (nLU + n) + 4 * nLU + 8 * (n + 1) + 48 * n
+
+
+def test_config_table_D1_counts():
+    """SURVEY Table D1 rows 2a and 4: nnzb, drop and level counts."""
+    rp, ci, v = laplacian_bsr3(64, 64, 64)
+    ctx = dd.dd_setup(rp, ci, v, grid=(64, 64, 64), tiles=(16, 16, 8), host_only=True)
+    st = ctx.stats()
+    assert (st["nnzb_before"], st["nnzb_after"], st["n_sub"], st["max_levels_L"]) == (1810432, 1703936, 128, 38)
+    rp, ci, v, _ = spe10_style_bsr3()
+    ctx = dd.dd_setup(rp, ci, v, grid=(60, 220, 85), tiles=(10, 20, 17), host_only=True)
+    st = ctx.stats()
+    assert (st["nnzb_before"], st["nnzb_after"], st["n_sub"], st["max_levels_L"]) == (7780000, 7385400, 330, 45)
+
+
+def test_errors_match_oracle():
+    # missing diagonal
+    rp = np.array([0, 1, 2], np.int64)
+    ci = np.array([1, 0], np.int32)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, np.ones(18), P=2, host_only=True)
+    assert e.value.name == "DD_E_MISSING_DIAG"
+    # unsorted columns
+    rp = np.array([0, 2, 4], np.int64)
+    ci = np.array([1, 0, 0, 1], np.int32)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, np.ones(36), P=2, host_only=True)
+    assert e.value.name == "DD_E_UNSORTED_OR_DUP"
+    # grid not divisible
+    rp, ci, v = laplacian_bsr3(5, 4, 4)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, v, grid=(5, 4, 4), tiles=(2, 2, 2), host_only=True)
+    assert e.value.name == "DD_E_GRID_NOT_DIVISIBLE"
+    # singular pivot at the same row as the oracle
+    rp, ci, a = kron_blocks([[1.0, 1.0], [1.0, 1.0]])
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.ilu0(rp, ci, a)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, a, P=2, host_only=True)
+    assert e.value.name == "DD_E_SINGULAR_PIVOT" and f"row {eo.value.row}" in str(e.value)

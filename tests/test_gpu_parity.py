@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs. Bars (BASELINE.json north_star): setup bit-exact; dd_apply max
+relative error <= 1e-10 (design expectation: 0 ulps);
+SpMV bitwise; BiCGSTAB converged to 1e-8 with iterations within +-2."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2508_04917_b200 as dd
+from inputs.gen import (apply_input, laplacian_bsr3, manufactured_rhs, random_block_grid,
+                        spe10_style_bsr3)
+from tests.parity import assert_setup_bitwise
+
+pytestmark = pytest.mark.gpu
+ALL = dd.DD_LEVELSET | dd.DD_SPINLOOP | dd.DD_DIRECT
+VARIANTS = [dd.DD_LEVELSET, dd.DD_SPINLOOP, dd.DD_DIRECT]
+
+CASES = {
+    # name: (generator, setup kwargs)
+    "cfg1_16^3": (lambda: laplacian_bsr3(16, 16, 16), dict(grid=(16, 16, 16), tiles=(8, 8, 8))),
+    "cfg2a_64^3": (lambda: laplacian_bsr3(64, 64, 64), dict(grid=(64, 64, 64), tiles=(16, 16, 8))),
+    "cfg2b_64^3_P8192": (lambda: laplacian_bsr3(64, 64, 64), dict(grid=(64, 64, 64), tiles=(32, 16, 16))),
+    "random_blocks": (lambda: random_block_grid(24, 20, 16, seed=3), dict(grid=(24, 20, 16), tiles=(6, 5, 4))),
+    "random_P4000_split_levels": (lambda: random_block_grid(40, 20, 20, seed=8),
+                                  dict(grid=(40, 20, 20), tiles=(20, 20, 10))),
+    "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),
+    "P1": (lambda: random_block_grid(6, 5, 4, seed=6), dict(P=1)),
+    "one_subdomain": (lambda: random_block_grid(12, 12, 12, seed=7), dict(grid=(12, 12, 12), tiles=(12, 12, 12))),
+    "spe10_style_cfg4": (lambda: spe10_style_bsr3()[:3], dict(grid=(60, 220, 85), tiles=(10, 20, 17))),
+}
+
+_cache = {}
+
+
+def get_case(name):
+    if name not in _cache:
+        gen, kw = CASES[name]
+        rp, ci, v = gen()
+        oracle.set_threads(0)
+        S = oracle.setup(rp, ci, v, **kw)
+        ctx = dd.dd_setup(rp, ci, v, variants=ALL, **kw)
+        _cache[name] = (rp, ci, v, S, ctx)
+    return _cache[name]
+
+
+def torch_vec(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_setup_bitwise(name):
+    _, _, _, S, ctx = get_case(name)
+    assert_setup_bitwise(ctx, S)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=["levelset", "spin", "direct"])
+@pytest.mark.parametrize("name", list(CASES))
+def test_apply_parity(name, variant):
+    import torch
+    _, _, _, S, ctx = get_case(name)
+    r = apply_input(S["n"], seed=2)
+    z_ref = oracle.apply(S, r)
+    z = torch.full((3 * S["n"],), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.apply(torch_vec(r), z, variant)
+    torch.cuda.synchronize()
+    zz = z.cpu().numpy()
+    rel = np.abs(zz - z_ref).max() / np.abs(z_ref).max()
+    assert rel <= 1e-10, f"max rel err {rel}"
+    # design expectation (fixed per-row FMA order): bitwise equal
+    assert np.array_equal(zz, z_ref), f"not bitwise: {np.count_nonzero(zz != z_ref)} entries differ"
+
+
+@pytest.mark.parametrize("name", ["cfg1_16^3", "cfg2a_64^3", "random_blocks", "chunks_ragged_oddP"])
+def test_apply_deterministic_and_stream(name):
+    import torch
+    _, _, _, S, ctx = get_case(name)
+    r = torch_vec(apply_input(S["n"], seed=4))
+    s = torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        z = torch.empty_like(r)
+        with torch.cuda.stream(s):
+            ctx.apply(r, z, dd.DD_LEVELSET, stream=s)
+        s.synchronize()
+        outs.append(z.cpu().numpy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_spmv_bitwise(name):
+    import torch
+    _, _, _, S, ctx = get_case(name)
+    x = apply_input(S["n"], seed=3)
+    y_ref = oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], x)
+    y = torch.empty(3 * S["n"], dtype=torch.float64, device="cuda")
+    ctx.spmv(torch_vec(x), y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_ref)
+
+
+@pytest.mark.parametrize("name,tol", [("cfg1_16^3", 1e-8), ("cfg2a_64^3", 1e-8), ("random_blocks", 1e-8),
+                                      ("spe10_style_cfg4", 1e-8), ("spe10_style_cfg4", 1e-6),
+                                      ("chunks_ragged_oddP", 1e-8)])
+def test_bicgstab_iterations(name, tol):
+    import torch
+    rp, ci, v, S, ctx = get_case(name)
+    _, b = manufactured_rhs(rp, ci, v, seed=1)
+    br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
+    oracle.set_threads(0)
+    xo, ro = oracle.bicgstab(S, br, tol=tol, max_iter=5000)
+    x = torch.zeros(3 * S["n"], dtype=torch.float64, device="cuda")
+    rg = ctx.bicgstab(torch_vec(br), x, tol=tol, max_iter=5000, hist=True)
+    assert ro["status"] == 0 and rg["converged"] == 1
+    assert abs(rg["iterations"] - ro["iterations"]) <= 2, (rg["iterations"], ro["iterations"])
+    assert rg["true_rel_resid"] <= 10 * tol
+    k = min(len(rg["resid_hist"]), len(ro["resid_hist"]), 10)
+    assert np.allclose(rg["resid_hist"][:k], ro["resid_hist"][:k], rtol=1e-9, atol=0)
+
+
+def test_solve_host_e2e_original_order():
+    """dd_solve_host: original-order host b in, original-order host x out."""
+    rp, ci, v, S, ctx = get_case("cfg1_16^3")
+    xs, b = manufactured_rhs(rp, ci, v, seed=1)
+    x = np.zeros_like(b)
+    rep = ctx.solve_host(b, x, tol=1e-10)
+    assert rep["converged"] == 1
+    assert np.abs(x - xs).max() <= 1e-7
+
+
+def test_permute_roundtrip():
+    import torch
+    _, _, _, S, ctx = get_case("chunks_ragged_oddP")
+    v = np.random.default_rng(0).uniform(-1, 1, 3 * S["n"])
+    d = torch.empty(3 * S["n"], dtype=torch.float64, device="cuda")
+    ctx.permute(v, d)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), v.reshape(-1, 3)[S["new_to_old"]].ravel())
+    back = np.zeros_like(v)
+    ctx.unpermute(d, back)
+    assert np.array_equal(back, v)
+
+
+# ------------------------------------------------------- full size (config 3)
+@pytest.fixture(scope="module")
+def cfg3():
+    rp, ci, v = laplacian_bsr3(160, 160, 160)
+    kw = dict(grid=(160, 160, 160), tiles=(16, 16, 8))
+    oracle.set_threads(0)
+    S = oracle.setup(rp, ci, v, **kw)
+    ctx = dd.dd_setup(rp, ci, v, variants=ALL, **kw)
+    return rp, ci, v, S, ctx
+
+
+def test_cfg3_full_size_apply_spmv(cfg3):
+    """BASELINE config 3 (160^3, P=2048), bench launch configuration: every
+    output element compared (the oracle finishes the full apply in seconds)."""
+    import torch
+    rp, ci, v, S, ctx = cfg3
+    assert_setup_bitwise(ctx, S)
+    r = apply_input(S["n"], seed=2)
+    z_ref = oracle.apply(S, r)
+    rd = torch_vec(r)
+    for var in VARIANTS:
+        z = torch.empty_like(rd)
+        ctx.apply(rd, z, var)
+        torch.cuda.synchronize()
+        assert np.array_equal(z.cpu().numpy(), z_ref), var
+    y = torch.empty_like(rd)
+    ctx.spmv(rd, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], r))
+
+
+@pytest.mark.skipif(os.environ.get("DD_SKIP_CFG3_SOLVE") == "1", reason="DD_SKIP_CFG3_SOLVE=1")
+def test_cfg3_bicgstab_iterations(cfg3):
+    import torch
+    rp, ci, v, S, ctx = cfg3
+    _, b = manufactured_rhs(rp, ci, v, seed=1)
+    br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
+    x = torch.zeros(3 * S["n"], dtype=torch.float64, device="cuda")
+    rg = ctx.bicgstab(torch_vec(br), x, tol=1e-8, max_iter=2000)
+    oracle.set_threads(0)
+    _, ro = oracle.bicgstab(S, br, tol=1e-8, max_iter=2000, hist=False)
+    assert rg["converged"] == 1 and ro["status"] == 0
+    assert abs(rg["iterations"] - ro["iterations"]) <= 2, (rg["iterations"], ro["iterations"])
+    assert rg["true_rel_resid"] <= 1e-7
