@@ -186,10 +186,16 @@ dd_status dd_get_halo(const dd_ctx *ctx, int64_t *n_ghost, int64_t *ghost_rows,
 dd_status dd_get_send_rows(const dd_ctx *ctx, int32_t peer, int64_t *n, int32_t *rows);
 /* stats[16]: {nnzb_before, nnzb_after, n_sub_global, n_sub_local, max_levels_L,
  *   max_levels_U, max_P, slab_bytes_levelset, slab_bytes_spin, spmv_bytes,
- *   apply_canonical_bytes, spmv_canonical_bytes, n_local, n_ghost, 0, 0};
+ *   apply_canonical_bytes, spmv_canonical_bytes, n_local, n_ghost,
+ *   kernels launched so far, 0};
  * setup_ms[6]: {partition+permute, reorder+drop, ilu0+ildu0, levels,
  *   pack, device upload}. Either may be NULL. */
 dd_status dd_stats(const dd_ctx *ctx, int64_t *stats, double *setup_ms);
+/* Per-kernel timing inside dd_bicgstab (CUDA events on the solver stream,
+ * harvested at its own sync points). mode 1: enable + reset, 0: disable,
+ * -1: query. out[8] (nullable) = {n_apply, apply_ms, n_spmv, spmv_ms,
+ * n_blas1, blas1_ms, kernels launched by this context so far, 0}. */
+dd_status dd_profile(dd_ctx *ctx, int32_t mode, double *out);
 /* Apply-kernel launch shape chosen at setup: {grid, threads, smem_bytes,
  * ring_bytes} for the given variant. */
 dd_status dd_launch_info(const dd_ctx *ctx, int32_t variant, int64_t *info);

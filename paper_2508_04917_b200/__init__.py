@@ -27,7 +27,7 @@ STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP"
 EXPORTS = ["dd_setup", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
            "dd_get_levels", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
-           "dd_nccl_unique_id", "dd_last_error"]
+           "dd_profile", "dd_nccl_unique_id", "dd_last_error"]
 
 
 class DDError(RuntimeError):
@@ -79,7 +79,7 @@ def lib():
             "dd_bicgstab": [P, P, P, d, i32, P, P, P], "dd_solve_host": [P, P, P, d, i32, P, P],
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
             "dd_get_levels": [P, i32, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
-            "dd_stats": [P, P, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
+            "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
             "dd_last_error": [],
         }
         for name, args in sig.items():
@@ -141,9 +141,10 @@ class Context:
         self.destroy()
 
     def destroy(self):
-        if getattr(self, "h", None):
-            lib().dd_destroy(self.h)
-            self.h = None
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.dd_destroy(h)
+        self.h = None
 
     # --- compute
     def apply(self, r, z, variant=DD_LEVELSET, stream=None):
@@ -225,7 +226,7 @@ class Context:
 
     STAT_KEYS = ["nnzb_before", "nnzb_after", "n_sub", "n_sub_local", "max_levels_L", "max_levels_U", "max_P",
                  "slab_bytes_levelset", "slab_bytes_spin", "spmv_bytes", "apply_canonical_bytes",
-                 "spmv_canonical_bytes", "n_local", "n_ghost"]
+                 "spmv_canonical_bytes", "n_local", "n_ghost", "launches"]
     SETUP_KEYS = ["partition_ms", "reorder_drop_ms", "ilu0_ms", "levels_ms", "pack_ms", "upload_ms"]
 
     def stats(self):
@@ -235,6 +236,13 @@ class Context:
         out = {k: int(s[i]) for i, k in enumerate(self.STAT_KEYS)}
         out.update({k: float(t[i]) for i, k in enumerate(self.SETUP_KEYS)})
         return out
+
+    def profile(self, mode=-1):
+        """mode 1: enable+reset, 0: disable, -1: query. Returns the counters."""
+        out = np.zeros(8)
+        _check(lib().dd_profile(self.h, mode, _ptr(out)))
+        return dict(n_apply=int(out[0]), apply_ms=float(out[1]), n_spmv=int(out[2]), spmv_ms=float(out[3]),
+                    n_blas=int(out[4]), blas_ms=float(out[5]), launches=int(out[6]))
 
     def launch_info(self, variant=DD_LEVELSET):
         info = np.zeros(4, np.int64)
@@ -326,6 +334,10 @@ def dd_get_send_rows(ctx, peer):
 
 def dd_stats(ctx):
     return ctx.stats()
+
+
+def dd_profile(ctx, mode=-1):
+    return ctx.profile(mode)
 
 
 def dd_launch_info(ctx, variant=DD_LEVELSET):

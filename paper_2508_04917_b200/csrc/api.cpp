@@ -71,6 +71,63 @@ dd_status dmalloc(T **p, size_t count) {
 
 Workspace *ws_of(dd_ctx *c) { return reinterpret_cast<Workspace *>(c->dev_ws); }
 
+// Optional per-kernel timing inside dd_bicgstab (dd_profile): CUDA events on
+// the solver's stream around every apply / SpMV / BLAS-1 launch, harvested at
+// the solver's own synchronisation points (no extra host syncs).
+enum { PK_APPLY = 0, PK_SPMV = 1, PK_BLAS = 2 };
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Pend {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pend> pend;
+    double ms[3] = {0, 0, 0};
+    int64_t n[3] = {0, 0, 0};
+};
+
+Prof *prof_of(dd_ctx *c) {
+    if (!c->prof) c->prof = new Prof();
+    return reinterpret_cast<Prof *>(c->prof);
+}
+
+cudaEvent_t prof_ev(Prof *p) {
+    if (p->used == p->pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        p->pool.push_back(e);
+    }
+    return p->pool[p->used++];
+}
+
+template <class F>
+dd_status timed(dd_ctx *c, int kind, cudaStream_t st, F &&launch) {
+    Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
+    if (!p || !p->on) return launch();
+    cudaEvent_t a = prof_ev(p), b = prof_ev(p);
+    cudaEventRecord(a, st);
+    dd_status r = launch();
+    cudaEventRecord(b, st);
+    p->pend.push_back({kind, a, b});
+    return r;
+}
+
+void prof_collect(dd_ctx *c) {
+    Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
+    if (!p) return;
+    for (auto &q : p->pend) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
+            p->ms[q.kind] += ms;
+            p->n[q.kind] += 1;
+        }
+    }
+    p->pend.clear();
+    p->used = 0;
+}
+
 dd_status upload_slab(Slab &sl) {
     TRY(dmalloc(&sl.d_bytes, sl.bytes.size() + 16));
     TRY(dmalloc(&sl.d_info, sl.info.size() + 1));
@@ -183,6 +240,7 @@ dd_status reduce_across(dd_ctx *c, int nv, int op, cudaStream_t st) {
     Workspace *ws = ws_of(c);
     NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
     ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ws->sc, op, st);
+    ++c->n_launches;
     return DD_OK;
 }
 
@@ -215,6 +273,7 @@ dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
     Workspace *ws = ws_of(c);
     CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    prof_collect(c);
     return DD_OK;
 }
 
@@ -310,6 +369,10 @@ void dd_destroy(dd_ctx *c) {
             delete ws;
         }
         if (c->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->nccl));
+        if (c->prof) {
+            for (auto e : reinterpret_cast<Prof *>(c->prof)->pool) cudaEventDestroy(e);
+            delete reinterpret_cast<Prof *>(c->prof);
+        }
     }
     delete c;
 }
@@ -380,12 +443,18 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
                 iters = k - 1;
                 break;
             }
-            ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, st);
-            TRY(apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream));
+            TRY(timed(c, PK_BLAS, st, [&] {
+                ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, st);
+                return DD_OK;
+            }));
+            TRY(timed(c, PK_APPLY, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream); }));
             ++napp;
-            TRY(spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, st));
+            TRY(timed(c, PK_SPMV, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, st); }));
             TRY(reduce_across(c, 1, ddk::FIN_ALPHA, st));
-            ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
+            TRY(timed(c, PK_BLAS, st, [&] {
+                ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
+                return DD_OK;
+            }));
             TRY(reduce_across(c, 1, ddk::FIN_SS, st));
             TRY(read_scalars(c, st));
             if (std::fabs(sc[ddk::S_SIGMA]) < 1e-30) {
@@ -404,11 +473,14 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
                 rel = ns / n0;
                 break;
             }
-            TRY(apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream));
+            TRY(timed(c, PK_APPLY, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream); }));
             ++napp;
-            TRY(spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, st));
+            TRY(timed(c, PK_SPMV, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, st); }));
             TRY(reduce_across(c, 2, ddk::FIN_OMEGA, st));
-            ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
+            TRY(timed(c, PK_BLAS, st, [&] {
+                ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
+                return DD_OK;
+            }));
             TRY(read_scalars(c, st));  // tau check before the all-gather keeps ranks in step
             if (!(sc[ddk::S_TT] >= 1e-30)) {
                 status = DD_E_BREAKDOWN;
@@ -560,11 +632,34 @@ dd_status dd_stats(const dd_ctx *c, int64_t *stats, double *setup_ms) {
         stats[11] = 76 * nnzA_loc + 4 * (nl + 1) + 48 * nl;
         stats[12] = nl;
         stats[13] = (int64_t)c->ghost_rows.size();
-        stats[14] = 0;
+        stats[14] = c->n_launches;
         stats[15] = 0;
     }
     if (setup_ms)
         for (int q = 0; q < 6; ++q) setup_ms[q] = c->setup_ms[q];
+    return DD_OK;
+}
+
+dd_status dd_profile(dd_ctx *c, int32_t mode, double *out) {
+    if (!c) return DD_E_INVALID_ARG;
+    Prof *p = prof_of(c);
+    if (mode == 1) {
+        p->on = true;
+        for (int q = 0; q < 3; ++q) {
+            p->ms[q] = 0;
+            p->n[q] = 0;
+        }
+    } else if (mode == 0) {
+        p->on = false;
+    }
+    if (out) {
+        for (int q = 0; q < 3; ++q) {
+            out[2 * q] = (double)p->n[q];
+            out[2 * q + 1] = p->ms[q];
+        }
+        out[6] = (double)c->n_launches;
+        out[7] = 0;
+    }
     return DD_OK;
 }
 

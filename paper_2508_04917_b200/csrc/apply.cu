@@ -42,7 +42,7 @@ constexpr int TC = 128;  // consumer threads = rows per record (Slab::rows_per_r
 __host__ __device__ constexpr uint32_t al8(uint32_t x) { return (x + 7u) & ~7u; }
 
 // ---- readers: map a byte offset inside the current record to data
-struct GlobalRd {
+struct GlobalRd {  // direct variant: the record in HBM
     const uint8_t *p;
     template <class T>
     __device__ __forceinline__ T ld(uint32_t off) const {
@@ -50,8 +50,16 @@ struct GlobalRd {
     }
 };
 
+struct LinRd {  // ring variant, record does not wrap: plain shared pointer
+    const uint8_t *p;
+    template <class T>
+    __device__ __forceinline__ T ld(uint32_t off) const {
+        return *reinterpret_cast<const T *>(p + off);
+    }
+};
+
 template <uint32_t RING>
-struct RingRd {
+struct RingRd {  // ring variant, record wraps the ring end
     const uint8_t *ring;
     uint32_t base;  // absolute stream position of the record start
     template <class T>
@@ -64,24 +72,96 @@ __device__ __forceinline__ uint16_t ld_volatile_u16(const uint16_t *p) {
     return *reinterpret_cast<const volatile uint16_t *>(p);
 }
 
-// Process one record: thread t owns row rows[t] (t < w).
+__device__ __forceinline__ void spin_until(const uint16_t *flags, uint32_t j, uint16_t ep) {
+    while (ld_volatile_u16(flags + j) != ep) {
+    }
+    __threadfence_block();
+}
+
+// Process one record: thread t owns the t-th row of the record (t < w).
+// Every load (descriptor, values, Dinv) is addressed from (t, cnt) alone, so
+// all are in flight before the first FMA; the only dependent step is the
+// gather of vec[3j..3j+2] through the descriptor's column ids.
 template <bool SPIN, class Rd>
-__device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, int t, double *__restrict__ vec,
-                                               uint16_t *flags, uint16_t ep) {
+__device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
+                                               double *__restrict__ vec, uint16_t *flags, uint16_t ep) {
     const uint32_t w = h.w, K = h.K;
     if (t >= (int)w) return;
     const bool upper = (h.flags & ddi::REC_UPPER) != 0;
-    const uint32_t off_rows = 16u + 2u * K;
-    const uint32_t off_dinv = al8(off_rows + 2u * w);
-    const uint32_t off_cols = off_dinv + (upper ? 72u * w : 0u);
+    const uint32_t off_desc = ddi::rec_off_desc(K);
+    const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
-    const uint32_t i = rd.template ld<uint16_t>(off_rows + 2u * t);
+    if (K <= 3) {
+        const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
+        const uint32_t i = d.x & 0xffffu;
+        const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
+        const uint32_t cnt[3] = {K > 0 ? (c8.x & 0xffffu) : 0u, K > 1 ? (c8.x >> 16) : 0u, K > 2 ? (c8.y & 0xffffu) : 0u};
+        double b[3][9];
+        uint32_t pre = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if ((uint32_t)t < cnt[k]) {
+                const uint32_t vb = off_val + 72u * pre + 8u * t, st = 8u * cnt[k];
+#pragma unroll
+                for (int v = 0; v < 9; ++v) b[k][v] = rd.template ld<double>(vb + st * v);
+            }
+            pre += cnt[k];
+        }
+        double a0, a1, a2;
+        if (upper) {
+            double D[9];
+#pragma unroll
+            for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+            const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
+            a0 = D[0] * z0;
+            a0 = __fma_rn(D[1], z1, a0);
+            a0 = __fma_rn(D[2], z2, a0);
+            a1 = D[3] * z0;
+            a1 = __fma_rn(D[4], z1, a1);
+            a1 = __fma_rn(D[5], z2, a1);
+            a2 = D[6] * z0;
+            a2 = __fma_rn(D[7], z1, a2);
+            a2 = __fma_rn(D[8], z2, a2);
+        } else {
+            a0 = vec[3 * i];
+            a1 = vec[3 * i + 1];
+            a2 = vec[3 * i + 2];
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if ((uint32_t)t < cnt[k]) {
+                const uint32_t j = col[k];
+                if (SPIN) spin_until(flags, j, ep);
+                const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+                a0 = __fma_rn(-b[k][0], x0, a0);
+                a0 = __fma_rn(-b[k][1], x1, a0);
+                a0 = __fma_rn(-b[k][2], x2, a0);
+                a1 = __fma_rn(-b[k][3], x0, a1);
+                a1 = __fma_rn(-b[k][4], x1, a1);
+                a1 = __fma_rn(-b[k][5], x2, a1);
+                a2 = __fma_rn(-b[k][6], x0, a2);
+                a2 = __fma_rn(-b[k][7], x1, a2);
+                a2 = __fma_rn(-b[k][8], x2, a2);
+            }
+        }
+        vec[3 * i] = a0;
+        vec[3 * i + 1] = a1;
+        vec[3 * i + 2] = a2;
+        if (SPIN) {
+            __threadfence_block();
+            *reinterpret_cast<volatile uint16_t *>(flags + i) = ep;
+        }
+        return;
+    }
+    // ---- general K (> 3): descriptor of rec_dw(K) bytes, loop over k
+    const uint32_t dw = ddi::rec_dw(K);
+    const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * t);
     double a0, a1, a2;
     if (upper) {
-        const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
         double D[9];
 #pragma unroll
         for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+        const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
         a0 = D[0] * z0;
         a0 = __fma_rn(D[1], z1, a0);
         a0 = __fma_rn(D[2], z2, a0);
@@ -100,16 +180,12 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, in
     for (uint32_t k = 0; k < K; ++k) {
         const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
         if ((uint32_t)t >= ck) break;
-        const uint32_t j = rd.template ld<uint16_t>(off_cols + 2u * (pre + t));
+        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k));
         const uint32_t vb = off_val + 72u * pre + 8u * t;
         double b[9];
 #pragma unroll
         for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + 8u * ck * v);
-        if (SPIN) {
-            while (ld_volatile_u16(flags + j) != ep) {
-            }
-            __threadfence_block();
-        }
+        if (SPIN) spin_until(flags, j, ep);
         const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
         a0 = __fma_rn(-b[0], x0, a0);
         a0 = __fma_rn(-b[1], x1, a0);
@@ -167,11 +243,12 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
         bool upper_seen = false;
         while (true) {
             const RecHdr h = hdr_from(__ldg(reinterpret_cast<const uint4 *>(p)));
+            const uint4 c8 = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
             if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
                 upper_seen = true;
                 ++ep;
             }
-            process_record<SPIN>(GlobalRd{p}, h, t, vec, flags, ep);
+            process_record<SPIN>(GlobalRd{p}, h, c8, t, vec, flags, ep);
             __syncthreads();
             p += h.bytes;
             if (h.flags & ddi::REC_LAST) break;
@@ -291,13 +368,20 @@ __global__ void __launch_bounds__(TC + 32, 1)
         bool upper_seen = false;
         while (true) {
             ensure(gbase + ro / CH);
-            const RecHdr h = hdr_from(*reinterpret_cast<const uint4 *>(ring + ((abs0 + ro) & (RING - 1u))));
+            const uint32_t pos = (abs0 + ro) & (RING - 1u);
+            const RecHdr h = hdr_from(*reinterpret_cast<const uint4 *>(ring + pos));
             ensure(gbase + (ro + h.bytes - 1) / CH);
+            // the 16 B after the header (cnt[0..7]) never straddle the ring end:
+            // records and the ring are 16-byte aligned
+            const uint4 c8 = *reinterpret_cast<const uint4 *>(ring + ((pos + 16u) & (RING - 1u)));
             if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
                 upper_seen = true;
                 ++ep;
             }
-            process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, t, vec, flags, ep);
+            if (pos + h.bytes <= RING)
+                process_record<SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep);
+            else
+                process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep);
             ro += h.bytes;
             named_bar_sync(1, TC);
             if (h.flags & ddi::REC_LAST) {
@@ -324,14 +408,14 @@ static RingFn ring_fn() {
 static RingFn pick_ring(int ring, bool spin) {
     if (!spin) {
         switch (ring) {
-            case 131072: return ring_fn<131072, 8192, false>();
+            case 131072: return ring_fn<131072, 16384, false>();
             case 65536: return ring_fn<65536, 8192, false>();
             case 32768: return ring_fn<32768, 4096, false>();
             case 16384: return ring_fn<16384, 2048, false>();
         }
     } else {
         switch (ring) {
-            case 131072: return ring_fn<131072, 8192, true>();
+            case 131072: return ring_fn<131072, 16384, true>();
             case 65536: return ring_fn<65536, 8192, true>();
             case 32768: return ring_fn<32768, 4096, true>();
             case 16384: return ring_fn<16384, 2048, true>();
@@ -340,7 +424,7 @@ static RingFn pick_ring(int ring, bool spin) {
     return nullptr;
 }
 
-static int ring_chunk(int ring) { return ring >= 65536 ? 8192 : (ring >= 32768 ? 4096 : 2048); }
+static int ring_chunk(int ring) { return ring / 8; }
 
 }  // namespace ddk
 
@@ -376,37 +460,42 @@ dd_status apply_prepare(dd_ctx *ctx) {
             set_error("subdomain vector exceeds shared memory");
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
-        cudaFuncSetAttribute(k_apply_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
-        cudaFuncSetAttribute(k_apply_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             vec_bytes + 2 * ctx->max_P + 16);
+        // the attribute is per function and shared by every context: set the maximum
+        cudaFuncSetAttribute(k_apply_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        cudaFuncSetAttribute(k_apply_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     }
     // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
+    // Ring choice: the consumer sweep is latency-bound, so maximise resident
+    // CTAs per SM first (cudaOccupancy: shared memory and registers), then
+    // take the largest ring that holds the biggest record plus one chunk.
     auto choose = [&](LaunchCfg &c, bool spin, int64_t max_rec) -> dd_status {
         const int want = env_int("DD_RING_KB", 0) * 1024;
         const int cands[4] = {131072, 65536, 32768, 16384};
-        int ring = 0;
+        int best_ring = 0, best_occ = 0;
         for (int rc : cands) {
             if (want && rc != want) continue;
             const int nst = rc / ring_chunk(rc);
             const int sm = vec_bytes + rc + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
-            if (sm <= smem_max && max_rec + ring_chunk(rc) <= rc) {
-                ring = rc;
-                break;
+            if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
+            cudaFuncSetAttribute(pick_ring(rc, spin), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(rc, spin), TC + 32, sm);
+            if (occ > best_occ) {
+                best_occ = occ;
+                best_ring = rc;
             }
         }
-        if (!ring) {
+        if (!best_ring) {
             set_error("no ring size fits the subdomain vector and the largest record");
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
-        const int nst = ring / ring_chunk(ring);
-        c.ring = ring;
-        c.smem = vec_bytes + ring + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
+        const int nst = best_ring / ring_chunk(best_ring);
+        c.ring = best_ring;
+        c.smem = vec_bytes + best_ring + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
         c.threads = TC + 32;
         c.consumers = TC;
-        const int per_sm = std::max(1, smem_sm / (c.smem + 1024));
-        c.grid = std::min(nsl, ctx->num_sms * per_sm);
+        c.grid = std::min(nsl, ctx->num_sms * std::max(1, best_occ));
         if (env_int("DD_APPLY_GRID", 0) > 0) c.grid = std::min(nsl, env_int("DD_APPLY_GRID", 0));
-        cudaFuncSetAttribute(pick_ring(ring, spin), cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
         return DD_OK;
     };
     if (ctx->variants & DD_LEVELSET) {
@@ -446,6 +535,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
         set_error("dd_apply: unknown variant");
         return DD_E_INVALID_ARG;
     }
+    ++ctx->n_launches;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("dd_apply launch: ") + cudaGetErrorString(e));

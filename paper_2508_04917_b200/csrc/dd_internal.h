@@ -9,20 +9,29 @@
 
 #include "dd.h"
 
+#if !defined(__CUDACC__) && !defined(__host__)
+#define __host__
+#endif
+#if !defined(__CUDACC__) && !defined(__device__)
+#define __device__
+#endif
+
 namespace ddi {
 
 // ---------------------------------------------------------------------------
-// Factor-slab record format (DESIGN.md section 6). One byte stream per
+// Factor-slab record format (DESIGN.md sec. 6). One byte stream per
 // subdomain, records in consumption order, every record 16-byte aligned:
 //   RecHdr (16 B)
-//   uint16 cnt[K]            rows having more than k blocks (jagged diagonal)
-//   uint16 rows[w]           local row ids, sorted by block count descending
-//   (pad to 8 B)
-//   [U records] double dinv[9][w]          structure of arrays
-//   uint16 col[nnz_rec]      k-major: k = 0 block of every row, then k = 1 ...
-//   (pad to 8 B)
-//   double val[nnz_rec][9] as 9 planes per k: val_k[v][cnt_k]
-// ---------------------------------------------------------------------------
+//   uint16 cnt[K], padded to 16 B  rows having more than k blocks (jagged
+//                                  diagonal; rows sorted by block count desc.)
+//   desc[w]: per row DW bytes = {row, col_0 .. col_{K-1}, 0xFFFF pad}
+//            DW = 8 for K <= 3, else 2*(1+K) rounded up to 16; padded to 16 B
+//   [U records] double dinv[9][w]  (structure of arrays)
+//   double val: for k = 0..K-1, 9 planes val_k[v][cnt_k]
+//   padded to 16 B.
+// One 8-byte descriptor load gives a thread its row and all its columns; the
+// value addresses depend only on (t, cnt), so every load of a record can be
+// issued before the first FMA.
 struct RecHdr {
     uint16_t w;       // rows in this record
     uint16_t K;       // max blocks per row (L: strictly lower, U: strictly upper)
@@ -31,6 +40,12 @@ struct RecHdr {
     uint32_t bytes;   // total record bytes (multiple of 16)
     uint32_t off_val; // byte offset of val[] from the record start
 };
+// descriptor width and offsets (shared by the packer and the kernels)
+inline __host__ __device__ uint32_t rec_dw(uint32_t K) { return K <= 3 ? 8u : ((2u * (1u + K) + 15u) & ~15u); }
+inline __host__ __device__ uint32_t rec_off_desc(uint32_t K) { return 16u + ((2u * K + 15u) & ~15u); }
+inline __host__ __device__ uint32_t rec_off_dinv(uint32_t K, uint32_t w) {
+    return (rec_off_desc(K) + rec_dw(K) * w + 15u) & ~15u;
+}
 static_assert(sizeof(RecHdr) == 16, "RecHdr must be 16 bytes");
 
 enum : uint16_t { REC_BARRIER = 1, REC_UPPER = 2, REC_LAST = 4 };
@@ -119,6 +134,8 @@ struct dd_ctx {
     void *nccl = nullptr;                // ncclComm_t
     double *h_pinned = nullptr;          // small pinned scalars
     int num_sms = 148;
+    mutable int64_t n_launches = 0;      // kernels launched by this context
+    void *prof = nullptr;                // api.cpp profiling state
 };
 
 namespace ddi {

@@ -324,6 +324,7 @@ namespace ddk {
 
 void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
                  const RedArgs &ra, cudaStream_t st) {
+    ++ctx->n_launches;
     const auto &S = ctx->spmv;
     const int grid = ctx->num_sms * 8;  // fixed: determinism of the fused dots
     switch (mode) {
@@ -343,35 +344,43 @@ int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 4; }
 
 void launch_init_r(const dd_ctx *ctx, int64_t m, const double *b, const double *t, double *r, double *rh,
                    const RedArgs &ra, cudaStream_t st) {
+    ++ctx->n_launches;
     k_init_r<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, r, rh, ra);
 }
 void launch_update_p(const dd_ctx *ctx, int64_t m, int first, const double *r, const double *v, double *p,
                      const double *sc, cudaStream_t st) {
+    ++ctx->n_launches;
     k_update_p<<<blas_grid(ctx), 256, 0, st>>>(m, first, r, v, p, sc);
 }
 void launch_update_s(const dd_ctx *ctx, int64_t m, const double *r, const double *v, double *s, const RedArgs &ra,
                      cudaStream_t st) {
+    ++ctx->n_launches;
     k_update_s<<<blas_grid(ctx), 256, 0, st>>>(m, r, v, s, ra);
 }
 void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc,
                           cudaStream_t st) {
+    ++ctx->n_launches;
     k_update_x_half<<<blas_grid(ctx), 256, 0, st>>>(m, ph, x, sc);
 }
 void launch_update_xr(const dd_ctx *ctx, int64_t m, const double *ph, const double *sh, const double *s,
                       const double *t, const double *rh, double *x, double *r, const RedArgs &ra, cudaStream_t st) {
+    ++ctx->n_launches;
     k_update_xr<<<blas_grid(ctx), 256, 0, st>>>(m, ph, sh, s, t, rh, x, r, ra);
 }
 void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, const RedArgs &ra, cudaStream_t st) {
+    ++ctx->n_launches;
     k_resid<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, ra);
 }
 void launch_finalize_gathered(int world, int nv, const double *gathered, double *sc, int op, cudaStream_t st) {
     k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, sc, op);
 }
 void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st) {
+    ++ctx->n_launches;
     k_gather3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
 }
 void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out,
                      cudaStream_t st) {
+    ++ctx->n_launches;
     k_scatter3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
 }
 size_t partials_bytes(const dd_ctx *ctx) { return sizeof(DD) * 2 * (size_t)(ctx->num_sms * 8); }

@@ -99,10 +99,9 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
         K = std::max(K, r.nblk);
         nnz += r.nblk;
     }
-    const size_t off_rows = 16 + 2 * (size_t)K;
-    const size_t off_dinv = al(off_rows + 2 * (size_t)w, 8);
-    const size_t off_cols = off_dinv + (upper ? 72 * (size_t)w : 0);
-    const size_t off_val = al(off_cols + 2 * (size_t)nnz, 8);
+    const size_t off_desc = rec_off_desc(K), dw = rec_dw(K);
+    const size_t off_dinv = rec_off_dinv(K, w);
+    const size_t off_val = off_dinv + (upper ? 72 * (size_t)w : 0);
     const size_t bytes = al(off_val + 72 * (size_t)nnz, 16);
     const size_t base = out.size();
     out.resize(base + bytes, 0);
@@ -121,19 +120,21 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
         for (auto &r : rows) c += (r.nblk > k);
         cnt[k] = (uint16_t)c;
     }
-    uint16_t *rid = reinterpret_cast<uint16_t *>(p + off_rows);
-    for (int t = 0; t < w; ++t) rid[t] = (uint16_t)rows[t].row;
+    for (int t = 0; t < w; ++t) {
+        uint16_t *d = reinterpret_cast<uint16_t *>(p + off_desc + dw * t);
+        for (size_t q = 0; q < dw / 2; ++q) d[q] = 0xFFFF;
+        d[0] = (uint16_t)rows[t].row;
+        for (int k = 0; k < rows[t].nblk; ++k) d[1 + k] = (uint16_t)(rows[t].cols[k] - col_base);
+    }
     if (upper) {
         double *dv = reinterpret_cast<double *>(p + off_dinv);
         for (int v = 0; v < 9; ++v)
             for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
     }
-    uint16_t *cc = reinterpret_cast<uint16_t *>(p + off_cols);
     double *vv = reinterpret_cast<double *>(p + off_val);
     size_t pos = 0;
     for (int k = 0; k < K; ++k) {
         const int ck = cnt[k];
-        for (int t = 0; t < ck; ++t) cc[pos + t] = (uint16_t)(rows[t].cols[k] - col_base);
         for (int v = 0; v < 9; ++v)
             for (int t = 0; t < ck; ++t) vv[9 * pos + (size_t)v * ck + t] = rows[t].vals[9 * (size_t)k + v];
         pos += ck;
@@ -530,9 +531,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         const int64_t avail = 232448 - vec - 2 * (int64_t)ctx->max_P - 1024;
         int64_t ring = 131072;
         while (ring > 16384 && ring > avail) ring /= 2;
-        const int64_t ch = ring >= 65536 ? 8192 : (ring >= 32768 ? 4096 : 2048);
+        const int64_t ch = ring / 8;
         int32_t rmax = 128;
-        auto est = [&](int64_t R) { return 16 + 2 * Kmax + 2 * R + 8 + 72 * R + R * Kmax * 74 + 32; };
+        auto est = [&](int64_t R) { return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 72 * R + 72 * R * Kmax + 16; };
         while (rmax > 16 && est(rmax) + ch > ring) rmax /= 2;
         ctx->slab_lvl.rows_per_rec = rmax;
         ctx->slab_spin.rows_per_rec = rmax;
