@@ -151,8 +151,7 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     TRY(apply_prepare(ctx));
     const int64_t nl = ctx->n_local;
     // slabs
-    if (ctx->variants & (DD_LEVELSET | DD_DIRECT)) TRY(upload_slab(ctx->slab_lvl));
-    if (ctx->variants & DD_SPINLOOP) TRY(upload_slab(ctx->slab_spin));
+    TRY(upload_slab(ctx->slab_lvl));
     // sliced-ELL SpMV operand
     {
         auto &S = ctx->spmv;

@@ -11,12 +11,13 @@
 //       shared-memory ring with 1-D bulk async copies (cp.async.bulk, UBLKCP)
 //       and full/empty mbarriers; TC consumer threads run the sweeps.
 //       SPIN=false: level sets, a CTA barrier between levels (Alg. 6).
-//       SPIN=true : rows in ascending (L) / descending (U) windows, each row
-//                   waits on per-row ready flags in shared memory (Alg. 4
-//                   P:410-441 with per-row flags, R17).
-//   k_apply_direct<SPIN>        ablation: same record processor, factors read
-//       straight from HBM with no staging (the paper's "vector in LDS,
-//       factors from global" design).
+//       SPIN=true : sync-free (Alg. 4 P:410-441 with per-row ready flags in
+//                   shared memory, R17): each warp walks the same level-ordered
+//                   records on its own and waits only on the flags of the rows
+//                   it depends on -- no CTA barrier per level.
+//   k_apply_direct              ablation: same records read straight from
+//       global memory (the paper's "vector in LDS, factors from global"
+//       design) with a bulk L2 prefetch running ahead.
 //
 // Arithmetic: lower row i, component c:
 //   acc = r_ic; for blocks (j,B) ascending: for d: acc = fma(-B[c][d], z_jd, acc)
@@ -68,12 +69,10 @@ struct RingRd {  // ring variant, record wraps the ring end
     }
 };
 
-__device__ __forceinline__ uint16_t ld_volatile_u16(const uint16_t *p) {
-    return *reinterpret_cast<const volatile uint16_t *>(p);
-}
-
-__device__ __forceinline__ void spin_until(const uint16_t *flags, uint32_t j, uint16_t ep) {
-    while (ld_volatile_u16(flags + j) != ep) {
+// Sync-free variant: flags[i] holds the epoch of the last sweep that finished
+// row i (L sweeps publish ep - 1, U sweeps ep; epochs only grow).
+__device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, uint32_t ep) {
+    while (*reinterpret_cast<const volatile uint32_t *>(flags + j) < ep) {
     }
     __threadfence_block();
 }
@@ -84,7 +83,7 @@ __device__ __forceinline__ void spin_until(const uint16_t *flags, uint32_t j, ui
 // gather of vec[3j..3j+2] through the descriptor's column ids.
 template <bool SPIN, class Rd>
 __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
-                                               double *__restrict__ vec, uint16_t *flags, uint16_t ep) {
+                                               double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
     if (t >= (int)w) return;
     const bool upper = (h.flags & ddi::REC_UPPER) != 0;
@@ -112,6 +111,7 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
             double D[9];
 #pragma unroll
             for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+            if (SPIN) spin_until(flags, i, ep - 1);  // own L result
             const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
             a0 = D[0] * z0;
             a0 = __fma_rn(D[1], z1, a0);
@@ -149,7 +149,7 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
         vec[3 * i + 2] = a2;
         if (SPIN) {
             __threadfence_block();
-            *reinterpret_cast<volatile uint16_t *>(flags + i) = ep;
+            *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
         }
         return;
     }
@@ -161,6 +161,7 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
         double D[9];
 #pragma unroll
         for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+        if (SPIN) spin_until(flags, i, ep - 1);  // own L result
         const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
         a0 = D[0] * z0;
         a0 = __fma_rn(D[1], z1, a0);
@@ -203,7 +204,7 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
     vec[3 * i + 2] = a2;
     if (SPIN) {
         __threadfence_block();
-        *reinterpret_cast<volatile uint16_t *>(flags + i) = ep;
+        *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
     }
 }
 
@@ -219,65 +220,87 @@ __device__ __forceinline__ RecHdr hdr_from(uint4 q) {
 }
 
 // ------------------------------------------------------------------ direct
-template <bool SPIN>
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Ablation: level-set sweep reading the records straight from global memory;
+// only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
+// keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
 __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
-                                                     int vec_bytes) {
+                                                     uint32_t pf_bytes) {
     extern __shared__ __align__(128) uint8_t smem[];
     double *vec = reinterpret_cast<double *>(smem);
-    uint16_t *flags = reinterpret_cast<uint16_t *>(smem + vec_bytes);
     const int t = threadIdx.x;
-    if (SPIN) {
-        for (int q = t; q < vec_bytes / 24; q += TC) flags[q] = 0;
-    }
-    uint16_t ep = 0;
     for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
         const SubInfo si = info[s];
+        const uint8_t *base = slab + si.stream_off;
+        const uint32_t sz = (uint32_t)si.stream_bytes;
+        uint32_t pf = 0;
+        if (t == 0 && pf_bytes) {
+            pf = min(sz, pf_bytes);
+            prefetch_l2(base, pf);
+        }
         const int nd = 3 * si.nrows;
         const double *rs = r + 3 * (int64_t)si.row0;
         for (int q = t; q < nd; q += TC) vec[q] = __ldg(rs + q);
         __syncthreads();
-        const uint8_t *p = slab + si.stream_off;
-        ++ep;
-        bool upper_seen = false;
+        uint32_t ro = 0;
         while (true) {
+            const uint8_t *p = base + ro;
             const RecHdr h = hdr_from(__ldg(reinterpret_cast<const uint4 *>(p)));
             const uint4 c8 = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
-            if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
-                upper_seen = true;
-                ++ep;
+            if (t == 0 && pf_bytes && pf < sz && pf < ro + pf_bytes) {
+                const uint32_t e = min(sz, ro + h.bytes + pf_bytes);
+                prefetch_l2(base + pf, e - pf);
+                pf = e;
             }
-            process_record<SPIN>(GlobalRd{p}, h, c8, t, vec, flags, ep);
-            __syncthreads();
-            p += h.bytes;
-            if (h.flags & ddi::REC_LAST) break;
+            const bool last = (h.flags & ddi::REC_LAST) != 0;
+            // L level 0 carries no blocks (z_i = r_i in place): no work, no barrier
+            const bool skip = !(h.flags & ddi::REC_UPPER) && h.K == 0 && !last;
+            if (!skip) {
+                process_record<false>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
+                __syncthreads();
+            }
+            ro += h.bytes;
+            if (last) break;
         }
-        if (SPIN && !upper_seen) ++ep;
         double *zs = z + 3 * (int64_t)si.row0;
         for (int q = t; q < nd; q += TC) zs[q] = vec[q];
     }
 }
 
 // -------------------------------------------------------------------- ring
+// SPIN = false (level set, Alg. 6): every consumer thread takes one row of
+//   each record; a named barrier separates records (levels).
+// SPIN = true  (sync-free, Alg. 4 with per-row ready flags): each warp walks
+//   the records on its own (rows 32w..32w+31 of each), waiting only on the
+//   ready flags of its dependencies; records are in level (topological) order
+//   so the warps pipeline levels. Ring chunks are released per warp (empty
+//   barriers count NW arrivals).
+// mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
+//   the streaming ceiling of the ring.
 template <uint32_t RING, uint32_t CH, bool SPIN>
 __global__ void __launch_bounds__(TC + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
-                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes) {
+                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode) {
     constexpr uint32_t NST = RING / CH;
+    constexpr uint32_t NW = TC / 32;
     static_assert((RING & (RING - 1)) == 0 && (CH & (CH - 1)) == 0 && NST >= 4, "ring shape");
     extern __shared__ __align__(128) uint8_t smem[];
     double *vec = reinterpret_cast<double *>(smem);
     uint8_t *ring = smem + vec_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + RING);
     uint64_t *empty = full + NST;
-    uint16_t *flags = reinterpret_cast<uint16_t *>(empty + NST);
+    uint32_t *flags = reinterpret_cast<uint32_t *>(empty + NST);
     const int tid = threadIdx.x;
 
     if (tid == TC) {
         for (uint32_t q = 0; q < NST; ++q) {
             mbar_init(&full[q], 1);
-            mbar_init(&empty[q], 1);
+            mbar_init(&empty[q], SPIN ? NW : 1);
         }
         fence_mbar_init();
     }
@@ -319,10 +342,11 @@ __global__ void __launch_bounds__(TC + 32, 1)
 
     // ===================== consumers (TC threads, named barrier 1)
     const int t = tid;
+    const uint32_t lane = t & 31u;
     uint32_t gbase = 0;     // chunk index at which the current subdomain starts
     uint32_t ready = 0;     // chunks this thread has seen full
-    uint32_t released = 0;  // (t == 0) chunks handed back to the producer
-    uint16_t ep = 0;
+    uint32_t released = 0;  // chunks handed back (SPIN: each warp's lane 0; else t == 0)
+    uint32_t ep = 0;
     auto ensure = [&](uint32_t chunk) {
         while (ready <= chunk) {
             mbar_wait(&full[ready % NST], (ready / NST) & 1u);
@@ -330,7 +354,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
         }
     };
     auto release_to = [&](uint32_t upto) {
-        if (t == 0) {
+        if (SPIN ? lane == 0 : t == 0) {
             while (released < upto) {
                 mbar_arrive(&empty[released % NST]);
                 ++released;
@@ -362,10 +386,9 @@ __global__ void __launch_bounds__(TC + 32, 1)
         }
         named_bar_sync(1, TC);
         release_to(gbase + rb / CH);
+        ep += 2;  // sync-free: L rows publish ep - 1, U rows ep
         // ---- records
         uint32_t ro = rb;
-        ++ep;
-        bool upper_seen = false;
         while (true) {
             ensure(gbase + ro / CH);
             const uint32_t pos = (abs0 + ro) & (RING - 1u);
@@ -374,23 +397,34 @@ __global__ void __launch_bounds__(TC + 32, 1)
             // the 16 B after the header (cnt[0..7]) never straddle the ring end:
             // records and the ring are 16-byte aligned
             const uint4 c8 = *reinterpret_cast<const uint4 *>(ring + ((pos + 16u) & (RING - 1u)));
-            if (SPIN && (h.flags & ddi::REC_UPPER) && !upper_seen) {
-                upper_seen = true;
-                ++ep;
+            const bool upper = (h.flags & ddi::REC_UPPER) != 0;
+            const bool last = (h.flags & ddi::REC_LAST) != 0;
+            // L level 0 carries no blocks (z_i = r_i in place): the level set
+            // skips it (no work, no barrier); the sync-free sweep publishes flags
+            const bool skip = !SPIN && !upper && h.K == 0 && !last;
+            const uint32_t ep_set = upper ? ep : ep - 1;
+            if (mode == 1 || skip) {
+            } else if (pos + h.bytes <= RING) {
+                process_record<SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
+            } else {
+                process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
             }
-            if (pos + h.bytes <= RING)
-                process_record<SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep);
-            else
-                process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep);
             ro += h.bytes;
-            named_bar_sync(1, TC);
-            if (h.flags & ddi::REC_LAST) {
+            if (SPIN) {
+                // lanes diverge in the flag waits: reconverge before lane 0 hands
+                // chunks back (rows of one record never depend on each other, so
+                // this cannot deadlock)
+                __syncwarp();
+            } else if (!skip) {
+                named_bar_sync(1, TC);
+            }
+            if (last) {
+                if (SPIN) named_bar_sync(1, TC);  // every row final before z is stored
                 release_to(gbase + nch);
                 break;
             }
             release_to(gbase + ro / CH);
         }
-        if (SPIN && !upper_seen) ++ep;
         double *zs = z + 3 * (int64_t)si.row0;
         for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[q];
         gbase += nch;
@@ -398,7 +432,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
 }
 
 // ------------------------------------------------------------ host side
-using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int);
+using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int);
 
 template <uint32_t RING, uint32_t CH, bool SPIN>
 static RingFn ring_fn() {
@@ -450,8 +484,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
     {
         LaunchCfg &c = ctx->cfg_direct;
-        const bool spin = false;
-        c.smem = vec_bytes + (spin ? 2 * ctx->max_P : 0);
+        c.smem = vec_bytes;
         c.threads = TC;
         c.grid = nsl;
         c.consumers = TC;
@@ -461,8 +494,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         // the attribute is per function and shared by every context: set the maximum
-        cudaFuncSetAttribute(k_apply_direct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-        cudaFuncSetAttribute(k_apply_direct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        cudaFuncSetAttribute(k_apply_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     }
     // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
     // Ring choice: the consumer sweep is latency-bound, so maximise resident
@@ -475,7 +507,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
         for (int rc : cands) {
             if (want && rc != want) continue;
             const int nst = rc / ring_chunk(rc);
-            const int sm = vec_bytes + rc + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
+            const int sm = vec_bytes + rc + 16 * nst + (spin ? vec_bytes / 6 : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
             cudaFuncSetAttribute(pick_ring(rc, spin), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
             int occ = 0;
@@ -491,20 +523,24 @@ dd_status apply_prepare(dd_ctx *ctx) {
         }
         const int nst = best_ring / ring_chunk(best_ring);
         c.ring = best_ring;
-        c.smem = vec_bytes + best_ring + 16 * nst + (spin ? 2 * ctx->max_P + 16 : 0);
+        c.smem = vec_bytes + best_ring + 16 * nst + (spin ? vec_bytes / 6 : 0);
         c.threads = TC + 32;
         c.consumers = TC;
         c.grid = std::min(nsl, ctx->num_sms * std::max(1, best_occ));
         if (env_int("DD_APPLY_GRID", 0) > 0) c.grid = std::min(nsl, env_int("DD_APPLY_GRID", 0));
         return DD_OK;
     };
-    if (ctx->variants & DD_LEVELSET) {
+    // every variant walks the same level-ordered slab: prepare all of them
+    ctx->variants = DD_LEVELSET | DD_SPINLOOP | DD_DIRECT;
+    {
         dd_status st = choose(ctx->cfg_lvl, false, ctx->slab_lvl.max_rec_bytes);
         if (st != DD_OK) return st;
     }
-    if (ctx->variants & DD_SPINLOOP) {
-        dd_status st = choose(ctx->cfg_spin, true, ctx->slab_spin.max_rec_bytes);
-        if (st != DD_OK) return st;
+    // the sync-free variant also needs 4 B of ready flags per row; when it
+    // does not fit it is dropped (dd_apply_variant then reports the error)
+    if (choose(ctx->cfg_spin, true, ctx->slab_lvl.max_rec_bytes) != DD_OK) {
+        ctx->variants &= ~DD_SPINLOOP;
+        ctx->cfg_spin = LaunchCfg{};
     }
     return cudaGetLastError() == cudaSuccess ? DD_OK : DD_E_CUDA;
 }
@@ -516,21 +552,23 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     if (nsl == 0) return DD_OK;
     const int vec_bytes = ((24 * ctx->max_P + 127) / 128) * 128;
     if (variant == 0) variant = DD_LEVELSET;
+    static const int mode = env_int("DD_APPLY_MODE", 0);  // 1: streaming ceiling (measurement only)
     if (variant == DD_DIRECT) {
-        if (!(ctx->variants & (DD_DIRECT | DD_LEVELSET))) return DD_E_INVALID_ARG;
+        static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
         const LaunchCfg &c = ctx->cfg_direct;
-        k_apply_direct<false><<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                 nsl, r, z, vec_bytes);
+        k_apply_direct<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf);
     } else if (variant == DD_LEVELSET) {
-        if (!(ctx->variants & DD_LEVELSET)) return DD_E_INVALID_ARG;
         const LaunchCfg &c = ctx->cfg_lvl;
         pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes);
+                                                                   nsl, r, z, vec_bytes, mode);
     } else if (variant == DD_SPINLOOP) {
-        if (!(ctx->variants & DD_SPINLOOP)) return DD_E_INVALID_ARG;
+        if (!(ctx->variants & DD_SPINLOOP)) {
+            set_error("dd_apply: sync-free variant unavailable (its ready flags do not fit shared memory)");
+            return DD_E_SUBDOMAIN_TOO_LARGE;
+        }
         const LaunchCfg &c = ctx->cfg_spin;
-        pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_spin.d_bytes, ctx->slab_spin.d_info,
-                                                                  nsl, r, z, vec_bytes);
+        pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+                                                                  nsl, r, z, vec_bytes, mode);
     } else {
         set_error("dd_apply: unknown variant");
         return DD_E_INVALID_ARG;

@@ -569,11 +569,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 gL.assign(hl + 1, {});
                 gU.assign(hu + 1, {});
                 for (int64_t i = 0; i < P; ++i) {
-                    if (ctx->hmapL[la + i] > 0) gL[ctx->hmapL[la + i]].push_back(rowL(i));
+                    gL[ctx->hmapL[la + i]].push_back(rowL(i));
                     gU[ctx->hmapU[la + i]].push_back(rowU(i));
                 }
-                // level 0 of L needs no work: z_i = r_i is already in shared memory
-                gL.erase(gL.begin());
+                // L level 0 (no lower blocks: z_i = r_i) stays as a block-free
+                // record: the level-set kernels skip it, the sync-free kernel
+                // publishes its ready flags from it
                 bL.assign(gL.size(), true);
                 bU.assign(gU.size(), true);
             } else {
@@ -611,8 +612,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         }
         slab.max_rec_bytes = max_rec;
     };
-    if (ctx->variants & (DD_LEVELSET | DD_DIRECT)) build_slab(ctx->slab_lvl, false);
-    if (ctx->variants & DD_SPINLOOP) build_slab(ctx->slab_spin, true);
+    // one level-ordered slab serves every variant (level order is a
+    // topological order, which the sync-free variant also walks)
+    build_slab(ctx->slab_lvl, false);
 
     // ---- sliced-ELL SpMV operand
     {
