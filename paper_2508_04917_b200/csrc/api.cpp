@@ -49,6 +49,12 @@ struct Workspace {
     double *loc = nullptr;       // [4] rank-local (s, c) pairs
     double *gathered = nullptr;  // [world * 4]
     double *h_sc = nullptr;      // pinned [S_COUNT]
+    int *ctl = nullptr;          // device solver control [8]
+    int *h_ctl = nullptr;        // pinned [16]: two snapshots
+    double *d_hist = nullptr;    // device residual history
+    int64_t hist_cap = 0;
+    double *h_tol = nullptr;     // pinned scalar (tolerance upload)
+    cudaEvent_t ev[2] = {nullptr, nullptr};
     double *xg = nullptr;        // ghost rows of the SpMV input [3 * n_ghost]
     double *sendbuf = nullptr;   // [3 * total send rows]
     int32_t *d_send_idx = nullptr;
@@ -80,7 +86,7 @@ struct Prof {
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     struct Pend {
-        int kind;
+        int kind, iter;
         cudaEvent_t a, b;
     };
     std::vector<Pend> pend;
@@ -103,23 +109,29 @@ cudaEvent_t prof_ev(Prof *p) {
 }
 
 template <class F>
-dd_status timed(dd_ctx *c, int kind, cudaStream_t st, F &&launch) {
+dd_status timed(dd_ctx *c, int kind, int iter, cudaStream_t st, F &&launch) {
     Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
     if (!p || !p->on) return launch();
     cudaEvent_t a = prof_ev(p), b = prof_ev(p);
     cudaEventRecord(a, st);
     dd_status r = launch();
     cudaEventRecord(b, st);
-    p->pend.push_back({kind, a, b});
+    p->pend.push_back({kind, iter, a, b});
     return r;
 }
 
-void prof_collect(dd_ctx *c) {
+// Harvest after the stream is idle. Launches enqueued past the stopping point
+// return at entry, so only the first n_real[kind] launches of each kind (and,
+// for BLAS-1, those of iterations <= k_last) are counted.
+void prof_collect(dd_ctx *c, const int64_t *n_real, int k_last) {
     Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
     if (!p) return;
+    int64_t seen[3] = {0, 0, 0};
     for (auto &q : p->pend) {
+        const bool real = q.kind == PK_BLAS ? q.iter <= k_last : seen[q.kind] < n_real[q.kind];
+        ++seen[q.kind];
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
+        if (real && cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
             p->ms[q.kind] += ms;
             p->n[q.kind] += 1;
         }
@@ -210,6 +222,12 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     TRY(dmalloc(&ws->loc, 4));
     TRY(dmalloc(&ws->gathered, 4 * (size_t)std::max(1, ctx->world)));
     CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_sc), ddk::S_COUNT * sizeof(double)));
+    TRY(dmalloc(&ws->ctl, 8));
+    CK(cudaMemset(ws->ctl, 0, 8 * sizeof(int)));
+    CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_ctl), 16 * sizeof(int)));
+    CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_tol), sizeof(double)));
+    CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     // halo buffers
     const int64_t ng = (int64_t)ctx->ghost_rows.size();
     TRY(dmalloc(&ws->xg, std::max<int64_t>(1, 3 * ng)));
@@ -230,15 +248,16 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
 
 ddk::RedArgs red_args(dd_ctx *c) {
     Workspace *ws = ws_of(c);
-    return ddk::RedArgs{reinterpret_cast<ddk::DD *>(ws->partials), ws->counter, ws->sc, ws->loc, c->world <= 1 ? 1 : 0};
+    return ddk::RedArgs{reinterpret_cast<ddk::DD *>(ws->partials), ws->counter, ws->sc, ws->loc,
+                        c->world <= 1 ? 1 : 0, nullptr, nullptr, 0};
 }
 
 // world > 1: all-gather the rank-local (s, c) pairs and finalize in rank order.
-dd_status reduce_across(dd_ctx *c, int nv, int op, cudaStream_t st) {
+dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaStream_t st) {
     if (c->world <= 1) return DD_OK;
     Workspace *ws = ws_of(c);
     NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
-    ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ws->sc, op, st);
+    ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ra, op, st);
     ++c->n_launches;
     return DD_OK;
 }
@@ -262,9 +281,10 @@ dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
     return DD_OK;
 }
 
-dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, cudaStream_t st) {
+dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, const ddk::RedArgs &ra,
+                    cudaStream_t st) {
     TRY(halo(c, x, st));
-    ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, red_args(c), st);
+    ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, ra, st);
     return DD_OK;
 }
 
@@ -272,7 +292,6 @@ dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
     Workspace *ws = ws_of(c);
     CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    prof_collect(c);
     return DD_OK;
 }
 
@@ -363,6 +382,12 @@ void dd_destroy(dd_ctx *c) {
                 cudaFree(q);
             cudaFree(ws->partials);
             cudaFree(ws->counter);
+            cudaFree(ws->ctl);
+            cudaFree(ws->d_hist);
+            cudaFreeHost(ws->h_ctl);
+            cudaFreeHost(ws->h_tol);
+            for (auto e : ws->ev)
+                if (e) cudaEventDestroy(e);
             cudaFree(ws->d_send_idx);
             cudaFreeHost(ws->h_sc);
             delete ws;
@@ -399,7 +424,7 @@ dd_status dd_apply(dd_ctx *c, const double *r, double *z, void *stream) {
 dd_status dd_spmv(dd_ctx *c, const double *x, double *y, void *stream) {
     if (!usable(c)) return DD_E_INVALID_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, y, nullptr, st));
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, y, nullptr, red_args(c), st));
     CK(cudaGetLastError());
     return DD_OK;
 }
@@ -415,100 +440,103 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     Workspace *ws = ws_of(c);
     const int64_t m = ws->m;
-    const ddk::RedArgs ra = red_args(c);
-    double *sc = ws->h_sc;
-    int nh = 0;
-    double iters = 0.0, rel = 1.0;
-    int napp = 0, status = DD_E_MAXITER, brk = 0;
+    if (ws->hist_cap < 2 * (int64_t)max_iter + 1) {
+        cudaFree(ws->d_hist);
+        ws->d_hist = nullptr;
+        ws->hist_cap = 0;
+        TRY(dmalloc(&ws->d_hist, 2 * (size_t)max_iter + 1));
+        ws->hist_cap = 2 * (int64_t)max_iter + 1;
+    }
+    CK(cudaMemsetAsync(ws->ctl, 0, 8 * sizeof(int), st));
+    *ws->h_tol = tol;
+    CK(cudaMemcpyAsync(ws->sc + ddk::S_TOL, ws->h_tol, sizeof(double), cudaMemcpyHostToDevice, st));
+    ddk::RedArgs ra = red_args(c);
+    ra.ctl = ws->ctl;
+    ra.hist = ws->d_hist;
+    ra.k = 0;
+    const ddk::RedArgs ra_plain = red_args(c);
 
-    // r = b - A x0; rh = r; rho_1 = ||r0||^2
-    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, st));
+    // r = b - A x0; rh = r; rho_1 = ||r0||^2; thr = tol ||r0|| (FIN_INIT)
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, ra_plain, st));
     ddk::launch_init_r(c, m, b, ws->t, ws->r, ws->rh, ra, st);
-    TRY(reduce_across(c, 1, ddk::FIN_INIT, st));
-    TRY(read_scalars(c, st));
-    const double n0 = std::sqrt(sc[ddk::S_N0SQ]);
-    if (hist) hist[nh] = n0;
-    ++nh;
-    if (n0 == 0.0) {
-        status = DD_OK;
-        rel = 0.0;
-    } else {
-        const double thr = tol * n0;
-        iters = max_iter;
-        for (int k = 1; k <= max_iter; ++k) {
-            if (std::fabs(sc[ddk::S_RHO]) < 1e-30) {
-                status = DD_E_BREAKDOWN;
-                brk = 1;
-                iters = k - 1;
-                break;
-            }
-            TRY(timed(c, PK_BLAS, st, [&] {
-                ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, st);
+    TRY(reduce_across(c, 1, ddk::FIN_INIT, ra, st));
+
+    // Alg. 1 iterations, enqueued in batches; every kernel returns at entry
+    // once the device-side control has stopped. The host looks at the control
+    // word one batch behind, so the GPU never idles on a half-step decision;
+    // every rank waits on the same batch, so all ranks stop together.
+    constexpr int BATCH = 2;
+    int k_enq = 0, j = 0;
+    for (bool stop = false; !stop; ++j) {
+        for (int q = 0; q < BATCH && k_enq < max_iter; ++q) {
+            const int k = ++k_enq;
+            ra.k = k;
+            TRY(timed(c, PK_BLAS, k, st, [&] {
+                ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, ws->ctl, st);
                 return DD_OK;
             }));
-            TRY(timed(c, PK_APPLY, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream); }));
-            ++napp;
-            TRY(timed(c, PK_SPMV, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, st); }));
-            TRY(reduce_across(c, 1, ddk::FIN_ALPHA, st));
-            TRY(timed(c, PK_BLAS, st, [&] {
+            TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream, ws->ctl); }));
+            TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st); }));
+            TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
+            TRY(timed(c, PK_BLAS, k, st, [&] {
                 ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
                 return DD_OK;
             }));
-            TRY(reduce_across(c, 1, ddk::FIN_SS, st));
-            TRY(read_scalars(c, st));
-            if (std::fabs(sc[ddk::S_SIGMA]) < 1e-30) {
-                status = DD_E_BREAKDOWN;
-                brk = 2;
-                iters = k - 1;
-                break;
-            }
-            const double ns = std::sqrt(sc[ddk::S_SS]);
-            if (hist) hist[nh] = ns;
-            ++nh;
-            if (ns < thr) {
-                ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, st);
-                status = DD_OK;
-                iters = k - 0.5;
-                rel = ns / n0;
-                break;
-            }
-            TRY(timed(c, PK_APPLY, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream); }));
-            ++napp;
-            TRY(timed(c, PK_SPMV, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, st); }));
-            TRY(reduce_across(c, 2, ddk::FIN_OMEGA, st));
-            TRY(timed(c, PK_BLAS, st, [&] {
+            TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
+            ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
+            TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream, ws->ctl); }));
+            TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st); }));
+            TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
+            TRY(timed(c, PK_BLAS, k, st, [&] {
                 ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
                 return DD_OK;
             }));
-            TRY(read_scalars(c, st));  // tau check before the all-gather keeps ranks in step
-            if (!(sc[ddk::S_TT] >= 1e-30)) {
-                status = DD_E_BREAKDOWN;
-                brk = 3;
-                iters = k - 0.5;
-                break;
-            }
-            TRY(reduce_across(c, 2, ddk::FIN_RHO, st));
-            if (c->world > 1) TRY(read_scalars(c, st));
-            const double nr = std::sqrt(sc[ddk::S_RR]);
-            if (hist) hist[nh] = nr;
-            ++nh;
-            rel = nr / n0;
-            if (nr < thr) {
-                status = DD_OK;
-                iters = k;
-                break;
-            }
+            TRY(reduce_across(c, 2, ddk::FIN_RHO, ra, st));
         }
+        int *snap = ws->h_ctl + 8 * (j % 2);
+        CK(cudaMemcpyAsync(snap, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ws->ev[j % 2], st));
+        if (j >= 1) {
+            CK(cudaEventSynchronize(ws->ev[(j - 1) % 2]));
+            if (ws->h_ctl[8 * ((j - 1) % 2) + ddk::C_STATE] != ddk::ST_RUN) stop = true;
+        }
+        if (k_enq >= max_iter) stop = true;
+    }
+    CK(cudaMemcpyAsync(ws->h_ctl, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int state = ws->h_ctl[ddk::C_STATE], kf = ws->h_ctl[ddk::C_K], nh = ws->h_ctl[ddk::C_NH];
+    std::vector<double> hv(std::max(1, nh));
+    CK(cudaMemcpy(hv.data(), ws->d_hist, sizeof(double) * std::max(1, nh), cudaMemcpyDeviceToHost));
+    if (hist) std::memcpy(hist, hv.data(), sizeof(double) * nh);
+    double iters = 0.0;
+    int64_t napp = 0;
+    int status = DD_OK, brk = 0;
+    double rel = 1.0;
+    const double n0 = hv[0];
+    auto last_full = [&]() { return n0 > 0 ? hv[std::max(0, (nh - 1) & ~1)] / n0 : 0.0; };
+    switch (state) {
+        case ddk::ST_DONE_HALF: iters = kf - 0.5; napp = 2 * kf - 1; rel = hv[2 * kf - 1] / n0; break;
+        case ddk::ST_DONE_FULL: iters = kf; napp = 2 * kf; rel = hv[2 * kf] / n0; break;
+        case ddk::ST_ZERO: iters = 0; napp = 0; rel = 0.0; break;
+        case ddk::ST_BRK_RHO: status = DD_E_BREAKDOWN; brk = 1; iters = kf; napp = 2 * kf; rel = last_full(); break;
+        case ddk::ST_BRK_SIGMA: status = DD_E_BREAKDOWN; brk = 2; iters = kf - 1; napp = 2 * kf - 1; rel = last_full(); break;
+        case ddk::ST_BRK_TAU: status = DD_E_BREAKDOWN; brk = 3; iters = kf - 0.5; napp = 2 * kf; rel = last_full(); break;
+        default: status = DD_E_MAXITER; iters = max_iter; napp = 2 * (int64_t)max_iter; rel = last_full(); break;
+    }
+    {
+        const int64_t n_real[3] = {napp, napp, 0};
+        prof_collect(c, n_real, (int)std::ceil(iters));
     }
     // true residual ||b - A x|| / ||b||
-    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, st));
-    ddk::launch_resid(c, m, b, ws->t, ra, st);
-    TRY(reduce_across(c, 2, ddk::FIN_RESID, st));
+    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, ra_plain, st));
+    ddk::launch_resid(c, m, b, ws->t, ra_plain, st);
+    TRY(reduce_across(c, 2, ddk::FIN_RESID, ra_plain, st));
     TRY(read_scalars(c, st));
     CK(cudaGetLastError());
+    const double *sc = ws->h_sc;
     if (rep) {
         rep->iterations = iters;
-        rep->n_applies = napp;
+        rep->n_applies = (int32_t)napp;
         rep->converged = status == DD_OK;
         rep->breakdown = brk;
         rep->status = status;

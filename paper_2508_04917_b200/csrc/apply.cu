@@ -230,7 +230,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
-                                                     uint32_t pf_bytes) {
+                                                     uint32_t pf_bytes, const int *skip) {
+    // inside dd_bicgstab: skip (uniformly) once the solver has stopped
+    if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     extern __shared__ __align__(128) uint8_t smem[];
     double *vec = reinterpret_cast<double *>(smem);
     const int t = threadIdx.x;
@@ -285,7 +287,9 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
 template <uint32_t RING, uint32_t CH, bool SPIN>
 __global__ void __launch_bounds__(TC + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
-                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode) {
+                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip) {
+    // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
+    if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
     constexpr uint32_t NW = TC / 32;
     static_assert((RING & (RING - 1)) == 0 && (CH & (CH - 1)) == 0 && NST >= 4, "ring shape");
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
 }
 
 // ------------------------------------------------------------ host side
-using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int);
+using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *);
 
 template <uint32_t RING, uint32_t CH, bool SPIN>
 static RingFn ring_fn() {
@@ -545,7 +549,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     return cudaGetLastError() == cudaSuccess ? DD_OK : DD_E_CUDA;
 }
 
-dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream) {
+dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip) {
     using namespace ddk;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int nsl = ctx->sub_last - ctx->sub_first;
@@ -556,11 +560,11 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     if (variant == DD_DIRECT) {
         static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
         const LaunchCfg &c = ctx->cfg_direct;
-        k_apply_direct<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf);
+        k_apply_direct<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf, skip);
     } else if (variant == DD_LEVELSET) {
         const LaunchCfg &c = ctx->cfg_lvl;
         pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode);
+                                                                   nsl, r, z, vec_bytes, mode, skip);
     } else if (variant == DD_SPINLOOP) {
         if (!(ctx->variants & DD_SPINLOOP)) {
             set_error("dd_apply: sync-free variant unavailable (its ready flags do not fit shared memory)");
@@ -568,7 +572,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
         }
         const LaunchCfg &c = ctx->cfg_spin;
         pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                  nsl, r, z, vec_bytes, mode);
+                                                                  nsl, r, z, vec_bytes, mode, skip);
     } else {
         set_error("dd_apply: unknown variant");
         return DD_E_INVALID_ARG;

@@ -145,7 +145,8 @@ void set_error(const std::string &msg);
 double now_ms();
 
 // kernels (apply.cu / spmv.cu / blas1.cu)
-dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream);
+dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream,
+                       const int *skip = nullptr);
 dd_status apply_prepare(dd_ctx *ctx);  // choose launch cfgs, set smem attributes
 void spmv_launch(const dd_ctx *ctx, const double *x, double *y, void *stream);
 }  // namespace ddi

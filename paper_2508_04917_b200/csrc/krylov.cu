@@ -10,6 +10,8 @@
 // final rounding except in rare straddling cases.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "dd_internal.h"
 #include "krylov.cuh"
 
@@ -47,30 +49,85 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 }
 
 // ---------------------------------------------------------------- finalize
-__device__ __forceinline__ void finalize(double *sc, int op, const double *val) {
+// Runs in one thread after a reduction completes (last block, or the rank-order
+// combine when world > 1). Besides the scalars of Alg. 1 it takes the solver's
+// control decisions in the oracle's order (R21, R25):
+//   FIN_INIT  ||r0||, rho_1 = r.r, thr = tol ||r0||; ||r0|| = 0 -> done
+//   FIN_ALPHA |sigma| < 1e-30 -> breakdown, else alpha = rho / sigma
+//   FIN_SS    ||s|| < thr -> half-step convergence (x += alpha p_hat pending)
+//   FIN_OMEGA tau < 1e-30 -> breakdown, else omega = (t.s) / tau
+//   FIN_RHO   ||r|| < thr -> converged; else |rho_next| < 1e-30 -> breakdown
+__device__ __forceinline__ void finalize(double *sc, int op, const double *val, int *ctl, double *hist, int k) {
     switch (op) {
-        case FIN_INIT:  // ||r0||^2 and rho_1 = rh.r = r.r
+        case FIN_INIT: {  // ||r0||^2 and rho_1 = rh.r = r.r
             sc[S_RR] = val[0];
             sc[S_N0SQ] = val[0];
             sc[S_RHO] = val[0];
+            const double n0 = sqrt(val[0]);
+            sc[S_THR] = sc[S_TOL] * n0;
+            if (ctl) {
+                hist[0] = n0;
+                ctl[C_NH] = 1;
+                if (n0 == 0.0) {
+                    ctl[C_STATE] = ST_ZERO;
+                    ctl[C_K] = 0;
+                } else if (fabs(val[0]) < 1e-30) {
+                    ctl[C_STATE] = ST_BRK_RHO;
+                    ctl[C_K] = 0;
+                }
+            }
             break;
+        }
         case FIN_ALPHA:
             sc[S_SIGMA] = val[0];
+            if (ctl && fabs(val[0]) < 1e-30) {
+                ctl[C_STATE] = ST_BRK_SIGMA;
+                ctl[C_K] = k;
+                break;
+            }
             sc[S_ALPHA] = sc[S_RHO] / val[0];
             break;
-        case FIN_SS:
+        case FIN_SS: {
             sc[S_SS] = val[0];
+            const double ns = sqrt(val[0]);
+            if (ctl) {
+                hist[2 * k - 1] = ns;
+                ctl[C_NH] = 2 * k;
+                if (ns < sc[S_THR]) {
+                    ctl[C_STATE] = ST_HALF;
+                    ctl[C_K] = k;
+                }
+            }
             break;
+        }
         case FIN_OMEGA:
             sc[S_TS] = val[0];
             sc[S_TT] = val[1];
+            if (ctl && !(val[1] >= 1e-30)) {
+                ctl[C_STATE] = ST_BRK_TAU;
+                ctl[C_K] = k;
+                break;
+            }
             sc[S_OMEGA] = val[0] / val[1];
             break;
-        case FIN_RHO:
+        case FIN_RHO: {
             sc[S_RR] = val[0];
             sc[S_RHO_PREV] = sc[S_RHO];
             sc[S_RHO] = val[1];
+            const double nr = sqrt(val[0]);
+            if (ctl) {
+                hist[2 * k] = nr;
+                ctl[C_NH] = 2 * k + 1;
+                if (nr < sc[S_THR]) {
+                    ctl[C_STATE] = ST_DONE_FULL;
+                    ctl[C_K] = k;
+                } else if (fabs(val[1]) < 1e-30) {
+                    ctl[C_STATE] = ST_BRK_RHO;
+                    ctl[C_K] = k;
+                }
+            }
             break;
+        }
         case FIN_RESID:
             sc[S_RES_TT] = val[0];
             sc[S_RES_BB] = val[1];
@@ -78,6 +135,10 @@ __device__ __forceinline__ void finalize(double *sc, int op, const double *val) 
         default:
             break;
     }
+}
+
+__device__ __forceinline__ bool stopped(const int *ctl) {
+    return ctl && *reinterpret_cast<const volatile int *>(ctl + C_STATE) != ST_RUN;
 }
 
 // Block-reduce NV DD values, write this block's partials, and let the last
@@ -131,7 +192,7 @@ __device__ __forceinline__ void deliver(const RedArgs &ra, int op, const DD (&ou
         double vals[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) vals[q] = out[q].s + out[q].c;
-        finalize(ra.sc, op, vals);
+        finalize(ra.sc, op, vals, ra.ctl, ra.hist, ra.k);
     } else {
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
@@ -143,11 +204,12 @@ __device__ __forceinline__ void deliver(const RedArgs &ra, int op, const DD (&ou
 
 // ------------------------------------------------------------------- SpMV
 // One warp per 32-row slice; thread = block row; 3 FMA chains per thread.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_spmv(int64_t n_rows, int64_t n_slices, const int64_t *__restrict__ slot_ptr,
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_spmv(int64_t n_rows, int64_t n_slices, const int64_t *__restrict__ slot_ptr,
                                               const int32_t *__restrict__ cols, const double *__restrict__ vals,
                                               const double *__restrict__ x, const double *__restrict__ xg,
                                               double *__restrict__ y, const double *__restrict__ aux, RedArgs ra) {
+    if (MODE != SPMV_PLAIN && stopped(ra.ctl)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -220,62 +282,125 @@ __global__ void __launch_bounds__(256) k_init_r(int64_t m, const double *__restr
     if (grid_reduce<1>(v, ra.partials, ra.counter, out)) deliver<1>(ra, FIN_INIT, out);
 }
 
+// Elementwise BLAS-1 kernels: VEC = 16-byte (double2) loads/stores when every
+// pointer is 16-byte aligned (the scalar tail element, if 3n is odd, is done
+// by thread 0); the grid is fixed per context, so the fused dots are
+// deterministic for a given context.
+#define GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
 // p = r (first) or p = fma(beta, fma(-omega, v, p), r), beta = (rho/rho_prev)*(alpha/omega)
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_update_p(int64_t m, int first, const double *__restrict__ r,
                                                   const double *__restrict__ v, double *__restrict__ p,
-                                                  const double *__restrict__ sc) {
+                                                  const double *__restrict__ sc, const int *ctl) {
+    if (stopped(ctl)) return;
     const double omega = sc[S_OMEGA];
     const double beta = (sc[S_RHO] / sc[S_RHO_PREV]) * (sc[S_ALPHA] / omega);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        if (first) p[i] = r[i];
-        else p[i] = __fma_rn(beta, __fma_rn(-omega, v[i], p[i]), r[i]);
+    auto one = [&](double rv, double vv, double pv) { return first ? rv : __fma_rn(beta, __fma_rn(-omega, vv, pv), rv); };
+    if (VEC) {
+        const double2 *r2 = reinterpret_cast<const double2 *>(r), *v2 = reinterpret_cast<const double2 *>(v);
+        double2 *p2 = reinterpret_cast<double2 *>(p);
+        GRID_STRIDE(i, m >> 1) {
+            const double2 a = r2[i], b = first ? make_double2(0, 0) : v2[i], c = first ? make_double2(0, 0) : p2[i];
+            p2[i] = make_double2(one(a.x, b.x, c.x), one(a.y, b.y, c.y));
+        }
+        if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[m - 1] = one(r[m - 1], v[m - 1], p[m - 1]);
+    } else {
+        GRID_STRIDE(i, m) p[i] = one(r[i], v[i], p[i]);
     }
 }
 
 // s = fma(-alpha, v, r); partial s.s
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_update_s(int64_t m, const double *__restrict__ r, const double *__restrict__ v,
                                                   double *__restrict__ s, RedArgs ra) {
+    if (stopped(ra.ctl)) return;
     const double alpha = ra.sc[S_ALPHA];
     DD d{0.0, 0.0};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const double sv = __fma_rn(-alpha, v[i], r[i]);
-        s[i] = sv;
+    auto one = [&](double rv, double vv) {
+        const double sv = __fma_rn(-alpha, vv, rv);
         dot2_acc(d.s, d.c, sv, sv);
+        return sv;
+    };
+    if (VEC) {
+        const double2 *r2 = reinterpret_cast<const double2 *>(r), *v2 = reinterpret_cast<const double2 *>(v);
+        double2 *s2 = reinterpret_cast<double2 *>(s);
+        GRID_STRIDE(i, m >> 1) {
+            const double2 a = r2[i], b = v2[i];
+            const double x0 = one(a.x, b.x);
+            const double x1 = one(a.y, b.y);
+            s2[i] = make_double2(x0, x1);
+        }
+        if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) s[m - 1] = one(r[m - 1], v[m - 1]);
+    } else {
+        GRID_STRIDE(i, m) s[i] = one(r[i], v[i]);
     }
     DD vv[1] = {d}, out[1];
     if (grid_reduce<1>(vv, ra.partials, ra.counter, out)) deliver<1>(ra, FIN_SS, out);
 }
 
-// x = fma(alpha, ph, x)   (half-step exit)
+// x = fma(alpha, ph, x)   (half-step exit; runs only when FIN_SS found
+// ||s|| < thr; the last block then marks the solve converged)
 __global__ void __launch_bounds__(256) k_update_x_half(int64_t m, const double *__restrict__ ph, double *__restrict__ x,
-                                                       const double *__restrict__ sc) {
+                                                       const double *__restrict__ sc, int *ctl) {
+    if (*reinterpret_cast<const volatile int *>(ctl + C_STATE) != ST_HALF) return;
     const double alpha = sc[S_ALPHA];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         x[i] = __fma_rn(alpha, ph[i], x[i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned int *cnt = reinterpret_cast<unsigned int *>(ctl + C_CNT);
+        if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+            *cnt = 0u;
+            ctl[C_STATE] = ST_DONE_HALF;
+        }
+    }
 }
 
 // x = fma(omega, sh, fma(alpha, ph, x)); r = fma(-omega, t, s); partials r.r, rh.r
-// Skipped entirely when tau = t.t < 1e-30 (breakdown, R25): x keeps the last iterate.
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_update_xr(int64_t m, const double *__restrict__ ph,
                                                    const double *__restrict__ sh, const double *__restrict__ s,
                                                    const double *__restrict__ t, const double *__restrict__ rh,
                                                    double *__restrict__ x, double *__restrict__ r, RedArgs ra) {
-    const double tt = ra.sc[S_TT];
-    const bool skip = !(tt >= 1e-30);
+    if (stopped(ra.ctl)) return;
     const double alpha = ra.sc[S_ALPHA], omega = ra.sc[S_OMEGA];
     DD d0{0.0, 0.0}, d1{0.0, 0.0};
-    if (!skip) {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            x[i] = __fma_rn(omega, sh[i], __fma_rn(alpha, ph[i], x[i]));
-            const double rv = __fma_rn(-omega, t[i], s[i]);
-            r[i] = rv;
-            dot2_acc(d0.s, d0.c, rv, rv);
-            dot2_acc(d1.s, d1.c, rh[i], rv);
+    auto one = [&](double phv, double shv, double sv, double tv, double rhv, double &xv) {
+        xv = __fma_rn(omega, shv, __fma_rn(alpha, phv, xv));
+        const double rv = __fma_rn(-omega, tv, sv);
+        dot2_acc(d0.s, d0.c, rv, rv);
+        dot2_acc(d1.s, d1.c, rhv, rv);
+        return rv;
+    };
+    if (VEC) {
+        const double2 *ph2 = reinterpret_cast<const double2 *>(ph), *sh2 = reinterpret_cast<const double2 *>(sh),
+                      *s2 = reinterpret_cast<const double2 *>(s), *t2 = reinterpret_cast<const double2 *>(t),
+                      *rh2 = reinterpret_cast<const double2 *>(rh);
+        double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
+        GRID_STRIDE(i, m >> 1) {
+            const double2 a = ph2[i], b = sh2[i], c = s2[i], e = t2[i], f = rh2[i];
+            double2 xv = x2[i];
+            const double r0 = one(a.x, b.x, c.x, e.x, f.x, xv.x);
+            const double r1 = one(a.y, b.y, c.y, e.y, f.y, xv.y);
+            x2[i] = xv;
+            r2[i] = make_double2(r0, r1);
+        }
+        if ((m & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            double xv = x[m - 1];
+            r[m - 1] = one(ph[m - 1], sh[m - 1], s[m - 1], t[m - 1], rh[m - 1], xv);
+            x[m - 1] = xv;
+        }
+    } else {
+        GRID_STRIDE(i, m) {
+            double xv = x[i];
+            r[i] = one(ph[i], sh[i], s[i], t[i], rh[i], xv);
+            x[i] = xv;
         }
     }
     DD v[2] = {d0, d1}, out[2];
-    if (grid_reduce<2>(v, ra.partials, ra.counter, out) && !skip) deliver<2>(ra, FIN_RHO, out);
+    if (grid_reduce<2>(v, ra.partials, ra.counter, out)) deliver<2>(ra, FIN_RHO, out);
 }
 
 // t = b - t; partials t.t, b.b (true residual)
@@ -293,15 +418,16 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, const double *__restri
 }
 
 // multi-rank: combine the gathered per-rank values (in rank order) and finalize
-__global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, double *sc, int op) {
+__global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, RedArgs ra, int op) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (op != FIN_INIT && op != FIN_RESID && stopped(ra.ctl)) return;
     double out[2] = {0.0, 0.0};
     for (int q = 0; q < nv; ++q) {
         DD acc{0.0, 0.0};
         for (int rr = 0; rr < world; ++rr) acc = dd_plus(acc, DD{gathered[rr * 2 * nv + 2 * q], gathered[rr * 2 * nv + 2 * q + 1]});
         out[q] = acc.s + acc.c;
     }
-    finalize(sc, op, out);
+    finalize(ra.sc, op, out, ra.ctl, ra.hist, ra.k);
 }
 
 // permutation helpers: out[3 li + c] = in[3 idx[li] + c] and the reverse
@@ -322,25 +448,41 @@ __global__ void k_scatter3(int64_t n, const int32_t *__restrict__ idx, const dou
 // ---------------------------------------------------------------- launchers
 namespace ddk {
 
+// DD_SPMV_MINB_<mode> (experiment knob): min resident blocks per SM for the
+// launch bounds of each SpMV mode (1 = compiler's choice).
+template <int MODE>
+static void spmv_go(int minb, int grid, cudaStream_t st, int64_t n, const ddi::SpmvDev &S, const double *x, const double *xg,
+                    double *y, const double *aux, const RedArgs &ra) {
+    switch (minb) {
+        case 8: k_spmv<MODE, 8><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        case 6: k_spmv<MODE, 6><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        case 5: k_spmv<MODE, 5><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        default: k_spmv<MODE, 1><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+    }
+}
+
+static int env_i(const char *n, int d) {
+    const char *v = getenv(n);
+    return v ? atoi(v) : d;
+}
+
 void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
                  const RedArgs &ra, cudaStream_t st) {
     ++ctx->n_launches;
     const auto &S = ctx->spmv;
     const int grid = ctx->num_sms * 8;  // fixed: determinism of the fused dots
+    static const int mb0 = env_i("DD_SPMV_MINB_0", 1), mb1 = env_i("DD_SPMV_MINB_1", 5),
+                     mb2 = env_i("DD_SPMV_MINB_2", 5);
     switch (mode) {
-        case SPMV_PLAIN:
-            k_spmv<SPMV_PLAIN><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
-            break;
-        case SPMV_SIGMA:
-            k_spmv<SPMV_SIGMA><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
-            break;
-        case SPMV_TS_TT:
-            k_spmv<SPMV_TS_TT><<<grid, 256, 0, st>>>(ctx->n_local, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
-            break;
+        case SPMV_PLAIN: spmv_go<SPMV_PLAIN>(mb0, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(mb1, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_TS_TT: spmv_go<SPMV_TS_TT>(mb2, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
     }
 }
 
-int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 4; }
+int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 8; }
+
+static inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 void launch_init_r(const dd_ctx *ctx, int64_t m, const double *b, const double *t, double *r, double *rh,
                    const RedArgs &ra, cudaStream_t st) {
@@ -348,31 +490,36 @@ void launch_init_r(const dd_ctx *ctx, int64_t m, const double *b, const double *
     k_init_r<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, r, rh, ra);
 }
 void launch_update_p(const dd_ctx *ctx, int64_t m, int first, const double *r, const double *v, double *p,
-                     const double *sc, cudaStream_t st) {
+                     const double *sc, const int *ctl, cudaStream_t st) {
     ++ctx->n_launches;
-    k_update_p<<<blas_grid(ctx), 256, 0, st>>>(m, first, r, v, p, sc);
+    if (al16(r) && al16(v) && al16(p)) k_update_p<true><<<blas_grid(ctx), 256, 0, st>>>(m, first, r, v, p, sc, ctl);
+    else k_update_p<false><<<blas_grid(ctx), 256, 0, st>>>(m, first, r, v, p, sc, ctl);
 }
 void launch_update_s(const dd_ctx *ctx, int64_t m, const double *r, const double *v, double *s, const RedArgs &ra,
                      cudaStream_t st) {
     ++ctx->n_launches;
-    k_update_s<<<blas_grid(ctx), 256, 0, st>>>(m, r, v, s, ra);
+    if (al16(r) && al16(v) && al16(s)) k_update_s<true><<<blas_grid(ctx), 256, 0, st>>>(m, r, v, s, ra);
+    else k_update_s<false><<<blas_grid(ctx), 256, 0, st>>>(m, r, v, s, ra);
 }
-void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc,
+void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc, int *ctl,
                           cudaStream_t st) {
     ++ctx->n_launches;
-    k_update_x_half<<<blas_grid(ctx), 256, 0, st>>>(m, ph, x, sc);
+    k_update_x_half<<<blas_grid(ctx), 256, 0, st>>>(m, ph, x, sc, ctl);
 }
 void launch_update_xr(const dd_ctx *ctx, int64_t m, const double *ph, const double *sh, const double *s,
                       const double *t, const double *rh, double *x, double *r, const RedArgs &ra, cudaStream_t st) {
     ++ctx->n_launches;
-    k_update_xr<<<blas_grid(ctx), 256, 0, st>>>(m, ph, sh, s, t, rh, x, r, ra);
+    if (al16(ph) && al16(sh) && al16(s) && al16(t) && al16(rh) && al16(x) && al16(r))
+        k_update_xr<true><<<blas_grid(ctx), 256, 0, st>>>(m, ph, sh, s, t, rh, x, r, ra);
+    else
+        k_update_xr<false><<<blas_grid(ctx), 256, 0, st>>>(m, ph, sh, s, t, rh, x, r, ra);
 }
 void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, const RedArgs &ra, cudaStream_t st) {
     ++ctx->n_launches;
     k_resid<<<blas_grid(ctx), 256, 0, st>>>(m, b, t, ra);
 }
-void launch_finalize_gathered(int world, int nv, const double *gathered, double *sc, int op, cudaStream_t st) {
-    k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, sc, op);
+void launch_finalize_gathered(int world, int nv, const double *gathered, const RedArgs &ra, int op, cudaStream_t st) {
+    k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, ra, op);
 }
 void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st) {
     ++ctx->n_launches;

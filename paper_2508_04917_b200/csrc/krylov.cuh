@@ -23,10 +23,28 @@ enum : int {
     S_N0SQ,
     S_RES_TT,
     S_RES_BB,
+    S_TOL,   // host-written before a solve
+    S_THR,   // tol * ||r0||
     S_COUNT = 16
 };
 
 enum : int { FIN_INIT = 1, FIN_ALPHA, FIN_SS, FIN_OMEGA, FIN_RHO, FIN_RESID };
+
+// Device-side solver control (int ctl[8]): the finalizing last blocks decide
+// convergence / breakdown (R21, R25) and every iteration kernel returns at
+// entry unless ctl[C_STATE] == ST_RUN, so the host can enqueue iterations
+// ahead without synchronising at each half step.
+enum : int { C_STATE = 0, C_K = 1, C_NH = 2, C_CNT = 3 };
+enum : int {
+    ST_RUN = 0,
+    ST_HALF = 1,       // ||s|| < tol ||r0||: x += alpha p_hat pending
+    ST_DONE_HALF = 2,  // converged at a half step
+    ST_DONE_FULL = 3,  // converged at a full step
+    ST_ZERO = 4,       // ||r0|| == 0
+    ST_BRK_RHO = 5,
+    ST_BRK_SIGMA = 6,
+    ST_BRK_TAU = 7
+};
 enum : int { SPMV_PLAIN = 0, SPMV_SIGMA = 1, SPMV_TS_TT = 2 };
 
 struct DD;
@@ -37,6 +55,9 @@ struct RedArgs {
     double *sc;             // device scalars
     double *loc;            // rank-local results (world > 1)
     int finalize;           // 1: last block finalizes (world == 1)
+    int *ctl;               // solver control (nullptr: no control, e.g. plain SpMV)
+    double *hist;           // residual history [2*max_iter+1] (device)
+    int k;                  // iteration the launch belongs to
 };
 
 void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
@@ -44,15 +65,15 @@ void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg,
 void launch_init_r(const dd_ctx *ctx, int64_t m, const double *b, const double *t, double *r, double *rh,
                    const RedArgs &ra, cudaStream_t st);
 void launch_update_p(const dd_ctx *ctx, int64_t m, int first, const double *r, const double *v, double *p,
-                     const double *sc, cudaStream_t st);
+                     const double *sc, const int *ctl, cudaStream_t st);
 void launch_update_s(const dd_ctx *ctx, int64_t m, const double *r, const double *v, double *s, const RedArgs &ra,
                      cudaStream_t st);
-void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc,
+void launch_update_x_half(const dd_ctx *ctx, int64_t m, const double *ph, double *x, const double *sc, int *ctl,
                           cudaStream_t st);
 void launch_update_xr(const dd_ctx *ctx, int64_t m, const double *ph, const double *sh, const double *s,
                       const double *t, const double *rh, double *x, double *r, const RedArgs &ra, cudaStream_t st);
 void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, const RedArgs &ra, cudaStream_t st);
-void launch_finalize_gathered(int world, int nv, const double *gathered, double *sc, int op, cudaStream_t st);
+void launch_finalize_gathered(int world, int nv, const double *gathered, const RedArgs &ra, int op, cudaStream_t st);
 void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st);
 void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out,
                      cudaStream_t st);
