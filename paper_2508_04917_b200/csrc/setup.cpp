@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -535,6 +536,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         int32_t rmax = 128;
         auto est = [&](int64_t R) { return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 72 * R + 72 * R * Kmax + 16; };
         while (rmax > 16 && est(rmax) + ch > ring) rmax /= 2;
+        if (const char *e = getenv("DD_ROWS_PER_REC")) rmax = std::max(16, std::min(rmax, atoi(e)));
         ctx->slab_lvl.rows_per_rec = rmax;
         ctx->slab_spin.rows_per_rec = rmax;
     }
