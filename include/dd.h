@@ -113,6 +113,7 @@ typedef struct {
                                  introspection calls work, compute calls
                                  return DD_E_INVALID_ARG)                       */
     int32_t n_threads;        /* host setup threads, 0 = all                   */
+    int32_t enable_refactor;  /* 1: keep the symbolic maps dd_refactor needs    */
 } dd_opts;
 
 typedef struct dd_ctx dd_ctx;
@@ -131,6 +132,19 @@ typedef struct {
 /* Setup (collective). Returns DD_OK and *out, or an error and *out = NULL. */
 dd_status dd_setup(const dd_bsr3 *A, const dd_opts *opts, dd_ctx **out);
 void dd_destroy(dd_ctx *ctx);
+
+/* Numeric re-factorisation with the SAME sparsity pattern (nonlinear solvers
+ * re-factor one pattern many times): new block values
+ * vals[9*nnzb] in A's ORIGINAL block order (host or device memory per
+ * vals_on_device). Runs on the GPU: values are gathered into the reordered /
+ * dropped layout, every subdomain is factored (block ILU0 -> ILDU0, Alg. 7
+ * P:680-711, same arithmetic order as dd_setup, so identical bits) level by
+ * level, and L, Dinv and U_unit are written straight into the apply slab; the
+ * SpMV operand is refreshed too. Requires dd_opts.enable_refactor = 1.
+ * Returns DD_E_SINGULAR_PIVOT (context unusable until a successful refactor)
+ * if a pivot block has |det| < pivot_floor. Ordered on `stream`; returns after
+ * the pivot check (one synchronisation). */
+dd_status dd_refactor(dd_ctx *ctx, const double *vals, int32_t vals_on_device, void *stream);
 
 /* This rank's rows in the reordered global numbering. */
 dd_status dd_local_range(const dd_ctx *ctx, int64_t *first_block_row, int64_t *n_block_rows);
@@ -164,7 +178,8 @@ dd_status dd_permute(dd_ctx *ctx, const double *v_orig_host, double *v_reord_dev
 dd_status dd_unpermute(dd_ctx *ctx, const double *v_reord_dev, double *v_orig_host,
                        void *stream);
 
-/* Introspection for parity (caller-allocated host arrays). */
+/* Introspection for parity (caller-allocated host arrays). It reports what
+ * dd_setup computed on the host (dd_refactor updates only device state). */
 dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original order*/,
                            int32_t *new_to_old /*[N]*/);
 /* which: 0 = L (hmapL), 1 = U (hmapU); local rows, reordered order. */

@@ -27,7 +27,7 @@ STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP"
 EXPORTS = ["dd_setup", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
            "dd_get_levels", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
-           "dd_profile", "dd_nccl_unique_id", "dd_last_error"]
+           "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_last_error"]
 
 
 class DDError(RuntimeError):
@@ -50,7 +50,7 @@ class Opts(C.Structure):
     _fields_ = [("subdomain_rows", C.c_int32), ("grid", C.c_void_p), ("variants", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("pivot_floor", C.c_double), ("host_only", C.c_int32),
-                ("n_threads", C.c_int32)]
+                ("n_threads", C.c_int32), ("enable_refactor", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -79,7 +79,7 @@ def lib():
             "dd_bicgstab": [P, P, P, d, i32, P, P, P], "dd_solve_host": [P, P, P, d, i32, P, P],
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
             "dd_get_levels": [P, i32, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
-            "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
+            "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_refactor": [P, P, i32, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
             "dd_last_error": [],
         }
         for name, args in sig.items():
@@ -186,6 +186,15 @@ class Context:
         _check(lib().dd_unpermute(self.h, _dev_vec(v_reord_dev, 3 * self.n_local, "v"), _ptr(v_orig_host),
                                   _stream(stream)))
 
+    def refactor(self, vals, stream=None):
+        """New block values (original block order, same pattern): host numpy or
+        CUDA float64 tensor."""
+        if isinstance(vals, np.ndarray):
+            vals = np.ascontiguousarray(vals, np.float64)
+            _check(lib().dd_refactor(self.h, _ptr(vals), 0, _stream(stream)))
+        else:
+            _check(lib().dd_refactor(self.h, _dev_vec(vals, 0, "vals"), 1, _stream(stream)))
+
     # --- introspection
     def partition(self):
         lab = np.empty(self.N, np.int32)
@@ -251,7 +260,8 @@ class Context:
 
 
 def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=DD_LEVELSET, device=0, rank=0,
-             world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0) -> Context:
+             world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0,
+             enable_refactor=False) -> Context:
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
@@ -270,6 +280,7 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     o.pivot_floor = pivot_floor
     o.host_only = int(bool(host_only))
     o.n_threads = n_threads
+    o.enable_refactor = int(bool(enable_refactor))
     h = C.c_void_p()
     _check(lib().dd_setup(C.byref(A), C.byref(o), C.byref(h)))
     return Context(h, n, keep=(g, idbuf))
@@ -334,6 +345,10 @@ def dd_get_send_rows(ctx, peer):
 
 def dd_stats(ctx):
     return ctx.stats()
+
+
+def dd_refactor(ctx, vals, stream=None):
+    ctx.refactor(vals, stream)
 
 
 def dd_profile(ctx, mode=-1):

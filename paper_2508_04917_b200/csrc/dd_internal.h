@@ -134,6 +134,19 @@ struct dd_ctx {
     void *nccl = nullptr;                // ncclComm_t
     double *h_pinned = nullptr;          // small pinned scalars
     int num_sms = 148;
+    // --- refactor (dd_refactor) symbolic maps, built when opts.enable_refactor
+    bool refactor = false;
+    double pivot_floor = 1e-300;
+    std::vector<int64_t> Asrc;           // reordered local A_r block -> original block index
+    std::vector<int64_t> Wrp, Wsrc;      // A_dd working layout (rank-local rows)
+    std::vector<int32_t> Wcol;
+    std::vector<int64_t> Wdiag;
+    std::vector<int64_t> Uptr;           // per W position: update range
+    std::vector<int32_t> UpdQ, UpdT;     // (U_kj position, target position)
+    std::vector<int32_t> LevRows, LevPtr, SubLev;
+    std::vector<int64_t> SlabLoff, SlabUoff, SlabDoff;  // byte offsets into the slab
+    std::vector<int32_t> SlabLst, SlabUst, SlabDst;     // plane strides (bytes)
+    void *rf = nullptr;                  // device-side refactor state (api.cpp)
     mutable int64_t n_launches = 0;      // kernels launched by this context
     void *prof = nullptr;                // api.cpp profiling state
 };

@@ -1,0 +1,26 @@
+// refactor.cuh -- declarations shared by refactor.cu and api.cpp (product-internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ddk {
+
+struct RfArgs {
+    const int32_t *SubLev, *LevPtr, *LevRows;
+    const int64_t *Wrp, *Wdiag, *Uptr, *Lrp, *Urp;
+    const int32_t *Wcol, *UpdQ, *UpdT;
+    double *W, *Dinv;
+    uint8_t *slab;
+    const int64_t *Loff, *Uoff, *Doff;
+    const int32_t *Lst, *Ust, *Dst;
+    double floor_;
+    unsigned long long *bad;  // min failing (reordered global) row
+    int64_t row_first;
+};
+
+void launch_gather_blocks(int64_t n, const int64_t *src, const double *from, double *to, int ell, int grid,
+                          cudaStream_t st);
+void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st);
+
+}  // namespace ddk

@@ -86,13 +86,23 @@ struct RowRef {
     const int32_t *cols;  // rank-local column ids (ascending)
     const double *vals;   // 9 per block
     const double *dinv;   // U records only
+    int64_t src0;         // Lv / Uv index of the row's first block (refactor maps)
+    int64_t li;           // rank-local row (Dinv map)
+};
+
+// Slab scatter maps for dd_refactor (null when not requested): byte offset of
+// element 0 of every L / U_unit / Dinv block inside its subdomain stream, and
+// the plane stride (element v at off + v * stride).
+struct SlabMaps {
+    int64_t *Loff = nullptr, *Uoff = nullptr, *Doff = nullptr;
+    int32_t *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
 };
 
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Append one record for `rows` (already sorted by nblk descending, stable).
 void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool upper,
-                uint16_t flags, int32_t col_base, int64_t &max_rec) {
+                uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp) {
     const int w = (int)rows.size();
     int K = 0;
     int nnz = 0;
@@ -131,6 +141,11 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
         double *dv = reinterpret_cast<double *>(p + off_dinv);
         for (int v = 0; v < 9; ++v)
             for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
+        if (mp.Doff)
+            for (int t = 0; t < w; ++t) {
+                mp.Doff[rows[t].li] = (int64_t)(base + off_dinv + 8 * (size_t)t);
+                mp.Dst[rows[t].li] = 8 * w;
+            }
     }
     double *vv = reinterpret_cast<double *>(p + off_val);
     size_t pos = 0;
@@ -138,6 +153,13 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
         const int ck = cnt[k];
         for (int v = 0; v < 9; ++v)
             for (int t = 0; t < ck; ++t) vv[9 * pos + (size_t)v * ck + t] = rows[t].vals[9 * (size_t)k + v];
+        int64_t *mo = upper ? mp.Uoff : mp.Loff;
+        int32_t *ms = upper ? mp.Ust : mp.Lst;
+        if (mo)
+            for (int t = 0; t < ck; ++t) {
+                mo[rows[t].src0 + k] = (int64_t)(base + off_val + 8 * (9 * pos + (size_t)t));
+                ms[rows[t].src0 + k] = 8 * ck;
+            }
         pos += ck;
     }
     max_rec = std::max<int64_t>(max_rec, (int64_t)bytes);
@@ -146,7 +168,7 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
 // groups: sequences of rows; barrier after each group with barrier flag.
 void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &groups,
                  const std::vector<bool> &barrier, bool upper, int rmax, int32_t col_base,
-                 int32_t &n_rec, int64_t &max_rec, bool last_section) {
+                 int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp) {
     for (size_t g = 0; g < groups.size(); ++g) {
         auto &rows = groups[g];
         std::stable_sort(rows.begin(), rows.end(),
@@ -158,7 +180,7 @@ void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &gr
             uint16_t fl = 0;
             if (e == w && barrier[g]) fl |= REC_BARRIER;
             if (last_section && g + 1 == groups.size() && e == w) fl |= REC_LAST;
-            put_record(out, part, upper, fl, col_base, max_rec);
+            put_record(out, part, upper, fl, col_base, max_rec, mp);
             ++n_rec;
         }
     }
@@ -292,6 +314,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     const int64_t nnz_loc = Arp[nl];
     std::vector<int32_t> gcol(nnz_loc);
     ctx->Av.assign(9 * nnz_loc, 0.0);
+    ctx->refactor = o->enable_refactor != 0;
+    ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
+    if (ctx->refactor) ctx->Asrc.assign(nnz_loc, -1);
 #pragma omp parallel for schedule(static)
     for (int64_t li = 0; li < nl; ++li) {
         const int64_t m = ctx->new_to_old[r0 + li];
@@ -314,6 +339,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         for (int64_t t = 0; t < nb; ++t) {
             gcol[Arp[li] + t] = cc[ix[t]];
             std::memcpy(&ctx->Av[9 * (Arp[li] + t)], &av[9 * (rp[m] + ix[t])], 9 * sizeof(double));
+            if (ctx->refactor) ctx->Asrc[Arp[li] + t] = rp[m] + ix[t];
         }
     }
     // global drop statistics (count of same-label blocks over all rows)
@@ -516,6 +542,88 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     ctx->max_lev_L = mL + 1;
     ctx->max_lev_U = mU + 1;
+    if (ctx->refactor) {
+        // A_dd working layout W (rank-local rows, same order as the host ILU0)
+        ctx->Wrp.assign(nl + 1, 0);
+        for (int64_t li = 0; li < nl; ++li)
+            ctx->Wrp[li + 1] = ctx->Wrp[li] + (ctx->Lrp[li + 1] - ctx->Lrp[li]) + 1 + (ctx->Urp[li + 1] - ctx->Urp[li]);
+        const int64_t nW = ctx->Wrp[nl];
+        if (nW >= INT32_MAX) {
+            set_error("dd_setup: refactor maps need fewer than 2^31 dropped-pattern blocks per rank");
+            return DD_E_INVALID_ARG;
+        }
+        ctx->Wsrc.assign(nW, 0);
+        ctx->Wcol.assign(nW, 0);
+        ctx->Wdiag.assign(nl, 0);
+        ctx->Uptr.assign(nW + 1, 0);
+        std::vector<int32_t> nupd(nW, 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t li = 0; li < nl; ++li) {
+            const int32_t s = row_sub[li];
+            const int64_t a = ctx->sub_ptr[s], e = ctx->sub_ptr[s + 1];
+            int64_t q = ctx->Wrp[li];
+            for (int64_t p = Arp[li]; p < Arp[li + 1]; ++p) {
+                const int64_t g = gcol[p];
+                if (g >= a && g < e) {
+                    ctx->Wsrc[q] = ctx->Asrc[p];
+                    ctx->Wcol[q] = (int32_t)(g - r0);
+                    if (g == r0 + li) ctx->Wdiag[li] = q;
+                    ++q;
+                }
+            }
+        }
+        // update lists: for lower position p = (i, k): every U_kj (j > k) whose
+        // column j is in row i's pattern -> (position of U_kj, position of W_ij),
+        // in ascending j (the order of the host / oracle elimination)
+        auto for_updates = [&](int64_t li, auto &&fn) {
+            for (int64_t p = ctx->Wrp[li]; p < ctx->Wdiag[li]; ++p) {
+                const int64_t k = ctx->Wcol[p];
+                for (int64_t qk = ctx->Wdiag[k] + 1; qk < ctx->Wrp[k + 1]; ++qk) {
+                    const int32_t j = ctx->Wcol[qk];
+                    // position of column j in row li (rows are short: linear scan)
+                    for (int64_t t = p + 1; t < ctx->Wrp[li + 1]; ++t)
+                        if (ctx->Wcol[t] == j) {
+                            fn(p, qk, t);
+                            break;
+                        }
+                }
+            }
+        };
+#pragma omp parallel for schedule(static)
+        for (int64_t li = 0; li < nl; ++li) for_updates(li, [&](int64_t p, int64_t, int64_t) { ++nupd[p]; });
+        for (int64_t p = 0; p < nW; ++p) ctx->Uptr[p + 1] = ctx->Uptr[p] + nupd[p];
+        ctx->UpdQ.assign(ctx->Uptr[nW], 0);
+        ctx->UpdT.assign(ctx->Uptr[nW], 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t li = 0; li < nl; ++li) {
+            std::vector<int64_t> fill;
+            for_updates(li, [&](int64_t p, int64_t qk, int64_t t) {
+                const int64_t at = ctx->Uptr[p] + (int64_t)std::count(fill.begin(), fill.end(), p);
+                fill.push_back(p);
+                ctx->UpdQ[at] = (int32_t)qk;
+                ctx->UpdT[at] = (int32_t)t;
+            });
+        }
+        // level lists per local subdomain: L levels ascending, rows ascending
+        ctx->SubLev.assign(nsl + 1, 0);
+        ctx->LevPtr.clear();
+        ctx->LevRows.clear();
+        ctx->LevRows.reserve(nl);
+        for (int32_t q = 0; q < nsl; ++q) {
+            const int64_t a = ctx->sub_ptr[s0 + q] - r0, e = ctx->sub_ptr[s0 + q + 1] - r0;
+            int32_t hl = 0;
+            for (int64_t li = a; li < e; ++li) hl = std::max(hl, ctx->hmapL[li]);
+            std::vector<std::vector<int32_t>> lv(hl + 1);
+            for (int64_t li = a; li < e; ++li) lv[ctx->hmapL[li]].push_back((int32_t)li);
+            ctx->SubLev[q] = (int32_t)ctx->LevPtr.size();
+            for (auto &l : lv) {
+                ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
+                ctx->LevRows.insert(ctx->LevRows.end(), l.begin(), l.end());
+            }
+        }
+        ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
+        ctx->SubLev[nsl] = (int32_t)ctx->LevPtr.size() - 1;
+    }
     const double t4 = now_ms();
     ctx->setup_ms[3] = t4 - t3;
 
@@ -540,6 +648,17 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         ctx->slab_lvl.rows_per_rec = rmax;
         ctx->slab_spin.rows_per_rec = rmax;
     }
+    SlabMaps mp;
+    if (ctx->refactor) {
+        ctx->SlabLoff.assign(ctx->Lci.size(), 0);
+        ctx->SlabLst.assign(ctx->Lci.size(), 0);
+        ctx->SlabUoff.assign(ctx->Uci.size(), 0);
+        ctx->SlabUst.assign(ctx->Uci.size(), 0);
+        ctx->SlabDoff.assign(nl, 0);
+        ctx->SlabDst.assign(nl, 0);
+        mp = SlabMaps{ctx->SlabLoff.data(), ctx->SlabUoff.data(), ctx->SlabDoff.data(),
+                      ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data()};
+    }
     auto build_slab = [&](ddi::Slab &slab, bool spin) {
         const int rmax = slab.rows_per_rec;
         std::vector<std::vector<uint8_t>> per(nsl);
@@ -553,12 +672,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             auto rowL = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Lrp[li + 1] - ctx->Lrp[li]), &ctx->Lci[ctx->Lrp[li]],
-                              &ctx->Lv[9 * ctx->Lrp[li]], nullptr};
+                              &ctx->Lv[9 * ctx->Lrp[li]], nullptr, ctx->Lrp[li], li};
             };
             auto rowU = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Urp[li + 1] - ctx->Urp[li]), &ctx->Uci[ctx->Urp[li]],
-                              &ctx->Uv[9 * ctx->Urp[li]], &ctx->Dinv[9 * li]};
+                              &ctx->Uv[9 * ctx->Urp[li]], &ctx->Dinv[9 * li], ctx->Urp[li], li};
             };
             std::vector<std::vector<RowRef>> gL, gU;
             std::vector<bool> bL, bU;
@@ -593,8 +712,8 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             }
             int32_t nrec = 0;
             int64_t mr = 0;
-            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false);
-            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true);
+            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp);
+            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp);
             slab.info[q].stream_bytes = (int32_t)per[q].size();
             slab.info[q].row0 = (int32_t)la;
             slab.info[q].nrows = (int32_t)P;
@@ -611,6 +730,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         for (int32_t q = 0; q < nsl; ++q) {
             std::memcpy(slab.bytes.data() + slab.info[q].stream_off, per[q].data(), per[q].size());
             std::vector<uint8_t>().swap(per[q]);
+            if (mp.Loff) {  // stream-relative -> slab-absolute offsets
+                const int64_t so = slab.info[q].stream_off;
+                for (int64_t li = slab.info[q].row0; li < slab.info[q].row0 + slab.info[q].nrows; ++li) {
+                    mp.Doff[li] += so;
+                    for (int64_t b = ctx->Lrp[li]; b < ctx->Lrp[li + 1]; ++b) mp.Loff[b] += so;
+                    for (int64_t b = ctx->Urp[li]; b < ctx->Urp[li + 1]; ++b) mp.Uoff[b] += so;
+                }
+            }
         }
         slab.max_rec_bytes = max_rec;
     };

@@ -193,3 +193,69 @@ def test_cfg3_bicgstab_iterations(cfg3):
     assert rg["converged"] == 1 and ro["status"] == 0
     assert abs(rg["iterations"] - ro["iterations"]) <= 2, (rg["iterations"], ro["iterations"])
     assert rg["true_rel_resid"] <= 1e-7
+
+
+# --------------------------------------------- GPU numeric refactor (8(f2))
+@pytest.mark.parametrize("grid,tiles", [((12, 10, 8), (6, 5, 4)), ((20, 16, 16), (10, 8, 8))])
+def test_refactor_matches_oracle_on_new_values(grid, tiles):
+    """dd_refactor with new values of the same pattern: the slab (every apply
+    variant) and the SpMV operand equal a fresh oracle setup, bit for bit;
+    refactoring back restores the original results."""
+    import torch
+    rp, ci, v1 = random_block_grid(*grid, seed=31)
+    _, _, v2 = random_block_grid(*grid, seed=32)
+    ctx = dd.dd_setup(rp, ci, v1, grid=grid, tiles=tiles, enable_refactor=True)
+    S1 = oracle.setup(rp, ci, v1, grid=grid, tiles=tiles)
+    S2 = oracle.setup(rp, ci, v2, grid=grid, tiles=tiles)
+    r = apply_input(S1["n"], seed=7)
+    rd = torch_vec(r)
+    for vals, S, on_dev in ((v2, S2, False), (v1, S1, True), (v2, S2, True)):
+        ctx.refactor(torch_vec(vals) if on_dev else vals)
+        z_ref = oracle.apply(S, r)
+        for var in VARIANTS:
+            z = torch.empty_like(rd)
+            ctx.apply(rd, z, var)
+            torch.cuda.synchronize()
+            assert np.array_equal(z.cpu().numpy(), z_ref), var
+        y = torch.empty_like(rd)
+        ctx.spmv(rd, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], r))
+
+
+def test_refactor_singular_pivot_and_recovery():
+    import torch
+    from tests.helpers import kron_blocks
+    rp, ci, a = kron_blocks([[4.0, 1.0], [2.0, 3.0]])
+    ctx = dd.dd_setup(rp, ci, a, P=2, enable_refactor=True)
+    _, _, bad = kron_blocks([[1.0, 1.0], [1.0, 1.0]])
+    with pytest.raises(dd.DDError) as e:
+        ctx.refactor(bad)
+    assert e.value.name == "DD_E_SINGULAR_PIVOT" and "row 1" in str(e.value)
+    ctx.refactor(a)
+    r = torch_vec(np.repeat([2.0, 3.0], 3))
+    z = torch.empty_like(r)
+    ctx.apply(r, z)
+    torch.cuda.synchronize()
+    assert np.allclose(z.cpu().numpy(), np.repeat([0.3, 0.8], 3), atol=1e-15)
+
+
+def test_refactor_cfg3_full_size_timing_and_parity(cfg3):
+    """Config 3: GPU refactor reproduces the host setup's slab (bitwise apply)."""
+    import time
+    import torch
+    rp, ci, v, S, _ = cfg3
+    ctx = dd.dd_setup(rp, ci, v, grid=(160, 160, 160), tiles=(16, 16, 8), enable_refactor=True)
+    vd = torch_vec(v)
+    ctx.refactor(vd)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.refactor(vd)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    r = apply_input(S["n"], seed=2)
+    z = torch.empty(3 * S["n"], dtype=torch.float64, device="cuda")
+    ctx.apply(torch_vec(r), z)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), oracle.apply(S, r))
+    print(f"refactor 160^3: {dt * 1e3:.1f} ms")
