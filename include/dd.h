@@ -114,7 +114,16 @@ typedef struct {
                                  return DD_E_INVALID_ARG)                       */
     int32_t n_threads;        /* host setup threads, 0 = all                   */
     int32_t enable_refactor;  /* 1: keep the symbolic maps dd_refactor needs    */
+    int32_t partitioner;      /* without grid: DD_PART_CHUNKS or DD_PART_BFS    */
 } dd_opts;
+
+/* Partitioners used when dd_opts.grid == NULL (P = subdomain_rows):
+ * contiguous chunks of P rows (R26), or graph growing (METIS stand-in, P:236,
+ * S:145-153, R35): parts of exactly P rows (last smaller), each grown
+ * breadth-first over the block pattern from the lowest-index unassigned row,
+ * neighbours in ascending column order. */
+#define DD_PART_CHUNKS 0
+#define DD_PART_BFS 1
 
 typedef struct dd_ctx dd_ctx;
 

@@ -48,6 +48,7 @@ def lib():
             "orc_get_threads": (C.c_int, []),
             "orc_labels_geometric": (C.c_int, [i32] * 6 + [P]),
             "orc_labels_chunks": (None, [i64, i32, P]),
+            "orc_labels_bfs": (None, [i64, P, P, i32, P]),
             "orc_permutation": (None, [i64, P, P, P]),
             "orc_subdomain_ptr": (None, [i64, P, i32, P]),
             "orc_reorder": (None, [i64, P, P, P, P, P, P, P, P]),
@@ -99,6 +100,13 @@ def labels_geometric(grid, tiles):
 def labels_chunks(n, P):
     out = np.empty(n, dtype=np.int32)
     lib().orc_labels_chunks(n, P, _p(out))
+    return out
+
+
+def labels_bfs(rp, ci, P):
+    rp, ci = _c(rp, np.int64), _c(ci, np.int32)
+    out = np.empty(rp.shape[0] - 1, dtype=np.int32)
+    lib().orc_labels_bfs(rp.shape[0] - 1, _p(rp), _p(ci), P, _p(out))
     return out
 
 
@@ -203,11 +211,15 @@ def dot(x, y):
     return float(lib().orc_dot(x.shape[0], _p(x), _p(y)))
 
 
-def setup(rp, ci, v, *, grid=None, tiles=None, P=None, pivot_floor=1e-300):
-    """The paper's setup pipeline, in the paper's order. Returns a dict."""
+def setup(rp, ci, v, *, grid=None, tiles=None, P=None, partitioner="chunks", pivot_floor=1e-300):
+    """The paper's setup pipeline, in the paper's order. Returns a dict.
+    Labels: geometric cuts (tiles given), else contiguous chunks or BFS graph
+    growing ("bfs") of P rows."""
     n = rp.shape[0] - 1
     if tiles is not None:
         labels = labels_geometric(grid, tiles)
+    elif partitioner == "bfs":
+        labels = labels_bfs(rp, ci, P)
     else:
         labels = labels_chunks(n, P)
     n_sub = int(labels.max()) + 1 if n else 0

@@ -52,6 +52,38 @@ int orc_labels_geometric(int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t
     return 0;
 }
 
+void orc_labels_bfs(int64_t n, const int64_t *rp, const int32_t *ci, int32_t P, int32_t *part_id) {
+    int64_t *queue = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    for (int64_t i = 0; i < n; i++) part_id[i] = -1;
+    int64_t assigned = 0, seed = 0;
+    int32_t part = 0;
+    while (assigned < n) {
+        int64_t head = 0, tail = 0, filled = 0;
+        while (filled < P && assigned < n) {
+            if (head == tail) { /* new BFS source: the lowest unassigned row */
+                while (part_id[seed] != -1) seed++;
+                part_id[seed] = part;
+                filled++;
+                assigned++;
+                queue[tail++] = seed;
+                continue;
+            }
+            int64_t u = queue[head++];
+            for (int64_t p = rp[u]; p < rp[u + 1] && filled < P; p++) {
+                int64_t v = ci[p];
+                if (v != u && part_id[v] == -1) {
+                    part_id[v] = part;
+                    filled++;
+                    assigned++;
+                    queue[tail++] = v;
+                }
+            }
+        }
+        part++;
+    }
+    free(queue);
+}
+
 void orc_labels_chunks(int64_t n, int32_t P, int32_t *part_id) {
     for (int64_t i = 0; i < n; i++) part_id[i] = (int32_t)(i / P);
 }

@@ -41,6 +41,11 @@ int orc_get_threads(void);
  * Returns 0, or -1 if a grid dim is not divisible by its tile dim (R26). */
 int orc_labels_geometric(int32_t nx, int32_t ny, int32_t nz, int32_t tx, int32_t ty,
                          int32_t tz, int32_t *part_id);
+/* Graph-growing partition (METIS stand-in, P:236 / P:1041 "manually
+ * balancing"; R35): parts of exactly P rows (last smaller), each
+ * grown breadth-first from the lowest-index unassigned row, neighbours visited
+ * in ascending column order, part closed as soon as it holds P rows. */
+void orc_labels_bfs(int64_t n, const int64_t *rp, const int32_t *ci, int32_t P, int32_t *part_id);
 /* Contiguous chunks of P rows (R26: last chunk may be smaller). */
 void orc_labels_chunks(int64_t n, int32_t P, int32_t *part_id);
 

@@ -21,6 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdd.so")
 
 DD_LEVELSET, DD_SPINLOOP, DD_DIRECT = 1, 2, 4
+DD_PART_CHUNKS, DD_PART_BFS = 0, 1
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",
           "DD_E_SINGULAR_PIVOT", "DD_E_SUBDOMAIN_TOO_LARGE", "DD_E_GRID_NOT_DIVISIBLE", "DD_E_CUDA",
           "DD_E_NCCL", "DD_E_OOM", "DD_E_BREAKDOWN", "DD_E_MAXITER", "DD_E_NO_DEVICE"]
@@ -50,7 +51,7 @@ class Opts(C.Structure):
     _fields_ = [("subdomain_rows", C.c_int32), ("grid", C.c_void_p), ("variants", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("pivot_floor", C.c_double), ("host_only", C.c_int32),
-                ("n_threads", C.c_int32), ("enable_refactor", C.c_int32)]
+                ("n_threads", C.c_int32), ("enable_refactor", C.c_int32), ("partitioner", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -261,7 +262,7 @@ class Context:
 
 def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=DD_LEVELSET, device=0, rank=0,
              world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0,
-             enable_refactor=False) -> Context:
+             enable_refactor=False, partitioner="chunks") -> Context:
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
@@ -281,6 +282,7 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     o.host_only = int(bool(host_only))
     o.n_threads = n_threads
     o.enable_refactor = int(bool(enable_refactor))
+    o.partitioner = {"chunks": DD_PART_CHUNKS, "bfs": DD_PART_BFS}[partitioner]
     h = C.c_void_p()
     _check(lib().dd_setup(C.byref(A), C.byref(o), C.byref(h)))
     return Context(h, n, keep=(g, idbuf))

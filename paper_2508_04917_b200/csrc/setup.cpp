@@ -265,8 +265,41 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             return DD_E_INVALID_ARG;
         }
         const int64_t P = o->subdomain_rows;
+        if (o->partitioner == DD_PART_BFS) {
+            // graph growing: BFS from the lowest unassigned row, exact part size P
+            std::fill(ctx->labels.begin(), ctx->labels.end(), -1);
+            std::vector<int64_t> q(N);
+            int64_t assigned = 0, seed = 0;
+            int32_t part = 0;
+            while (assigned < N) {
+                size_t head = 0, tail = 0;
+                int64_t filled = 0;
+                while (filled < P && assigned < N) {
+                    if (head == tail) {
+                        while (ctx->labels[seed] != -1) ++seed;
+                        ctx->labels[seed] = part;
+                        ++filled;
+                        ++assigned;
+                        q[tail++] = seed;
+                        continue;
+                    }
+                    const int64_t u = q[head++];
+                    for (int64_t e = rp[u]; e < rp[u + 1] && filled < P; ++e) {
+                        const int64_t w = ci[e];
+                        if (w != u && ctx->labels[w] == -1) {
+                            ctx->labels[w] = part;
+                            ++filled;
+                            ++assigned;
+                            q[tail++] = w;
+                        }
+                    }
+                }
+                ++part;
+            }
+        } else {
 #pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < N; ++i) ctx->labels[i] = (int32_t)(i / P);
+            for (int64_t i = 0; i < N; ++i) ctx->labels[i] = (int32_t)(i / P);
+        }
     }
     int32_t maxl = 0;
     for (int64_t i = 0; i < N; ++i) maxl = std::max(maxl, ctx->labels[i]);

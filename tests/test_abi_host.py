@@ -56,6 +56,8 @@ CASES = {
     "one_subdomain": (lambda: random_block_grid(9, 8, 7, seed=7), dict(grid=(9, 8, 7), tiles=(9, 8, 7))),
     "spe10_small": (lambda: spe10_style_bsr3(20, 40, 20, upper_ness_from=10)[:3],
                     dict(grid=(20, 40, 20), tiles=(10, 20, 10))),
+    "bfs_random": (lambda: random_block_grid(12, 10, 8, seed=13), dict(P=100, partitioner="bfs")),
+    "bfs_spe10_small": (lambda: spe10_style_bsr3(20, 40, 20, upper_ness_from=10)[:3], dict(P=1000, partitioner="bfs")),
 }
 
 

@@ -29,6 +29,7 @@ CASES = {
     "P1": (lambda: random_block_grid(6, 5, 4, seed=6), dict(P=1)),
     "one_subdomain": (lambda: random_block_grid(12, 12, 12, seed=7), dict(grid=(12, 12, 12), tiles=(12, 12, 12))),
     "spe10_style_cfg4": (lambda: spe10_style_bsr3()[:3], dict(grid=(60, 220, 85), tiles=(10, 20, 17))),
+    "spe10_style_bfs_P2048": (lambda: spe10_style_bsr3()[:3], dict(P=2048, partitioner="bfs")),
 }
 
 _cache = {}
@@ -109,7 +110,7 @@ def test_spmv_bitwise(name):
 
 @pytest.mark.parametrize("name,tol", [("cfg1_16^3", 1e-8), ("cfg2a_64^3", 1e-8), ("random_blocks", 1e-8),
                                       ("spe10_style_cfg4", 1e-8), ("spe10_style_cfg4", 1e-6),
-                                      ("chunks_ragged_oddP", 1e-8)])
+                                      ("chunks_ragged_oddP", 1e-8), ("spe10_style_bfs_P2048", 1e-8)])
 def test_bicgstab_iterations(name, tol):
     import torch
     rp, ci, v, S, ctx = get_case(name)

@@ -361,3 +361,31 @@ def test_o8_alg5_marking_loop_and_brute_force(seed):
     hu = oracle.levels_upper(rpu, ciu)
     rev = alg5_marking(n, [list(n - 1 - np.nonzero(S.T[n - 1 - i, n - i:])[0] - (n - i)) for i in range(n)])
     assert np.array_equal(hu, rev[::-1])
+
+
+# ------------------------------------------------ O2b graph-growing partition
+def test_o2b_bfs_worked_example_and_trivial_cases():
+    """path graph n=8, P=2 -> [0,0,1,1,2,2,3,3]; P = n -> one part; P = 1
+    -> singleton parts in seed order (ascending)."""
+    rp, ci, _ = random_block_chain(8, seed=1)
+    assert oracle.labels_bfs(rp, ci, 2).tolist() == [0, 0, 1, 1, 2, 2, 3, 3]
+    rp, ci, _ = random_block_grid(5, 4, 3, seed=2)
+    assert np.all(oracle.labels_bfs(rp, ci, 60) == 0)
+    assert np.array_equal(oracle.labels_bfs(rp, ci, 1), np.arange(60))
+
+
+@pytest.mark.parametrize("grid,P", [((8, 8, 8), 37), ((12, 10, 6), 64), ((20, 3, 2), 7)])
+def test_o2b_bfs_sizes_and_first_part_is_scipy_bfs(grid, P):
+    """Exact part sizes (last smaller); part 0 = the first P vertices of
+    scipy.sparse.csgraph.breadth_first_order from vertex 0 (library routine,
+    same ascending neighbour order)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import breadth_first_order
+    rp, ci, _ = grid_stencil_pattern(*grid)
+    n = rp.shape[0] - 1
+    lab = oracle.labels_bfs(rp, ci, P)
+    cnt = np.bincount(lab)
+    assert np.all(cnt[:-1] == P) and 0 < cnt[-1] <= P and cnt.sum() == n
+    A = sp.csr_matrix((np.ones(ci.shape[0]), ci, rp), shape=(n, n))
+    order = breadth_first_order(A, 0, directed=True, return_predecessors=False)
+    assert set(np.nonzero(lab == 0)[0].tolist()) == set(order[:P].tolist())
