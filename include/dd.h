@@ -41,8 +41,9 @@
  * Streams: dd_apply, dd_spmv, dd_permute, dd_unpermute are ordered on the
  *   given cudaStream_t (passed as void*, NULL = legacy default stream) and do
  *   not synchronise the host unless stated. dd_bicgstab returns when the
- *   solve is done (it synchronises the stream once per half-iteration to
- *   test convergence).
+ *   solve is done: the convergence test runs on the device,
+ *   the host enqueues iterations in batches and reads the solver state one
+ *   batch behind.
  *
  * Errors: every call returns a dd_status and never aborts; dd_last_error()
  *   gives a thread-local message for the last failing call. dd_setup failure
@@ -51,8 +52,10 @@
  * Multi-GPU (sec. 4.5 P:730-734 extended to the solver): one process per GPU;
  *   rank r owns a contiguous, count-balanced range of subdomains (R32).
  *   Every rank passes the same full host matrix. dd_setup, dd_spmv and
- *   dd_bicgstab are collective when world > 1 (NCCL: halo exchange for SpMV,
- *   all-gather of double-double dot partials). dd_apply never communicates.
+ *   dd_bicgstab are collective when world > 1 (halo exchange for SpMV,
+ *   all-gather of double-double dot partials; NCCL, or device-to-device
+ *   copies between contexts of one process, see DD_COMM_LOCAL).
+ *   dd_apply never communicates.
  */
 #ifndef DD_H
 #define DD_H
@@ -115,7 +118,21 @@ typedef struct {
     int32_t n_threads;        /* host setup threads, 0 = all                   */
     int32_t enable_refactor;  /* 1: keep the symbolic maps dd_refactor needs    */
     int32_t partitioner;      /* without grid: DD_PART_CHUNKS or DD_PART_BFS    */
+    int32_t comm;             /* world > 1: DD_COMM_NCCL (default) or DD_COMM_LOCAL */
 } dd_opts;
+
+/* Exchange transports for world > 1 (the SpMV halo and the dot partials):
+ *   DD_COMM_NCCL   one process per GPU; nccl_unique_id is an ncclUniqueId.
+ *   DD_COMM_LOCAL  the ranks are contexts of ONE process (one per GPU, or
+ *                  several sharing a GPU), each created and driven by its own
+ *                  host thread (dd_setup, dd_spmv, dd_bicgstab, dd_solve_host
+ *                  and dd_destroy are collective over the group);
+ *                  nccl_unique_id is any 128-byte key the ranks share. Data
+ *                  moves by device-to-device (peer) copies ordered with CUDA
+ *                  events and one host rendezvous per exchange; a rendezvous
+ *                  that waits > 120 s fails with DD_E_NCCL. */
+#define DD_COMM_NCCL 0
+#define DD_COMM_LOCAL 1
 
 /* Partitioners used when dd_opts.grid == NULL (P = subdomain_rows):
  * contiguous chunks of P rows (R26), or graph growing (METIS stand-in, P:236,

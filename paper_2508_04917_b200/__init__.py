@@ -19,9 +19,13 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdd.so")
+# development A/B runs may point at another in-tree build of the same library
+if os.environ.get("DD_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["DD_LIB"])
 
 DD_LEVELSET, DD_SPINLOOP, DD_DIRECT = 1, 2, 4
 DD_PART_CHUNKS, DD_PART_BFS = 0, 1
+DD_COMM_NCCL, DD_COMM_LOCAL = 0, 1
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",
           "DD_E_SINGULAR_PIVOT", "DD_E_SUBDOMAIN_TOO_LARGE", "DD_E_GRID_NOT_DIVISIBLE", "DD_E_CUDA",
           "DD_E_NCCL", "DD_E_OOM", "DD_E_BREAKDOWN", "DD_E_MAXITER", "DD_E_NO_DEVICE"]
@@ -51,7 +55,8 @@ class Opts(C.Structure):
     _fields_ = [("subdomain_rows", C.c_int32), ("grid", C.c_void_p), ("variants", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_unique_id", C.c_void_p), ("pivot_floor", C.c_double), ("host_only", C.c_int32),
-                ("n_threads", C.c_int32), ("enable_refactor", C.c_int32), ("partitioner", C.c_int32)]
+                ("n_threads", C.c_int32), ("enable_refactor", C.c_int32), ("partitioner", C.c_int32),
+                ("comm", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -262,7 +267,10 @@ class Context:
 
 def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=DD_LEVELSET, device=0, rank=0,
              world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0,
-             enable_refactor=False, partitioner="chunks") -> Context:
+             enable_refactor=False, partitioner="chunks", comm="nccl") -> Context:
+    """world > 1: comm="nccl" (one process per GPU, nccl_id from dd_nccl_unique_id)
+    or comm="local" (ranks are contexts of this process, each created and driven
+    from its own thread; nccl_id is any 128-byte key the ranks share)."""
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
@@ -283,6 +291,7 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     o.n_threads = n_threads
     o.enable_refactor = int(bool(enable_refactor))
     o.partitioner = {"chunks": DD_PART_CHUNKS, "bfs": DD_PART_BFS}[partitioner]
+    o.comm = {"nccl": DD_COMM_NCCL, "local": DD_COMM_LOCAL}[comm]
     h = C.c_void_p()
     _check(lib().dd_setup(C.byref(A), C.byref(o), C.byref(h)))
     return Context(h, n, keep=(g, idbuf))

@@ -53,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OBJ, f + ".o")
         if f.endswith(".cu"):
             cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+                   *os.environ.get("DD_NVCC_DEFS", "").split(),
                    "--expt-relaxed-constexpr", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
                    *inc, "-c", src, "-o", obj]
         else:

@@ -5,8 +5,12 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -60,7 +64,42 @@ struct Workspace {
     double *sendbuf = nullptr;   // [3 * total send rows]
     int32_t *d_send_idx = nullptr;
     std::vector<int64_t> send_off;  // [world + 1]
+    // DD_COMM_LOCAL: "my send data is ready" / "I have copied my peers' data"
+    cudaEvent_t xev_ready = nullptr, xev_done = nullptr;
 };
+
+// ---------------------------------------------------------------- DD_COMM_LOCAL
+// Ranks that are contexts of one process. Each exchange: every rank records
+// xev_ready after producing its outgoing data; rendezvous; every rank makes
+// its stream wait on the producers' events and copies device-to-device;
+// records xev_done; rendezvous; every producer's stream waits on its
+// consumers' xev_done before it can overwrite the outgoing buffer. All waits
+// name events recorded before the rendezvous, so the GPU work of all ranks is
+// enqueued before anything waits on it (no cycles).
+struct LocalGroup {
+    int world = 0;
+    std::vector<dd_ctx *> members;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0, refs = 0;
+    uint64_t gen = 0;
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return true;
+        }
+        return cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; });
+    }
+};
+
+std::mutex g_groups_m;
+std::map<std::string, LocalGroup *> g_groups;
+
+LocalGroup *group_of(const dd_ctx *c) { return reinterpret_cast<LocalGroup *>(c->group); }
 
 template <class T>
 dd_status dmalloc(T **p, size_t count) {
@@ -151,10 +190,76 @@ dd_status upload_slab(Slab &sl) {
     return DD_OK;
 }
 
+// DD_COMM_LOCAL: join the group named by the 128-byte key; returns once
+// every rank has joined (its workspace is then visible to the peers).
+dd_status local_join(dd_ctx *ctx, const void *key) {
+    LocalGroup *G;
+    {
+        std::lock_guard<std::mutex> lk(g_groups_m);
+        const std::string k(reinterpret_cast<const char *>(key), 128);
+        auto it = g_groups.find(k);
+        if (it == g_groups.end()) {
+            G = new LocalGroup();
+            G->world = ctx->world;
+            G->members.assign(ctx->world, nullptr);
+            g_groups[k] = G;
+        } else {
+            G = it->second;
+        }
+        if (G->world != ctx->world || G->members[ctx->rank]) {
+            set_error("dd_setup: DD_COMM_LOCAL group key reused with another world size or rank");
+            return DD_E_INVALID_ARG;
+        }
+        G->members[ctx->rank] = ctx;
+        ++G->refs;
+        ctx->group = G;
+    }
+    if (!G->barrier()) {
+        set_error("dd_setup: DD_COMM_LOCAL rendezvous timed out (every rank must call dd_setup from its own thread)");
+        return DD_E_NCCL;
+    }
+    // peer access between distinct devices (copies also work without it)
+    for (dd_ctx *q : G->members)
+        if (q->device != ctx->device) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, ctx->device, q->device);
+            if (can && cudaDeviceEnablePeerAccess(q->device, 0) != cudaSuccess) cudaGetLastError();
+        }
+    return DD_OK;
+}
+
+void local_leave(dd_ctx *ctx) {
+    LocalGroup *G = group_of(ctx);
+    if (!G) return;
+    std::lock_guard<std::mutex> lk(g_groups_m);
+    // no live peer may still be copying from this rank's buffers: its copies
+    // precede its last xev_done record
+    for (dd_ctx *q : G->members)
+        if (q && q != ctx && q->dev_ws && ws_of(q)->xev_done) cudaEventSynchronize(ws_of(q)->xev_done);
+    G->members[ctx->rank] = nullptr;
+    ctx->group = nullptr;
+    if (--G->refs == 0) {
+        for (auto it = g_groups.begin(); it != g_groups.end(); ++it)
+            if (it->second == G) {
+                g_groups.erase(it);
+                break;
+            }
+        delete G;
+    }
+}
+
+#define RENDEZVOUS(G)                                                              \
+    do {                                                                           \
+        if (!(G)->barrier()) {                                                     \
+            set_error("DD_COMM_LOCAL rendezvous timed out (a rank stopped calling)"); \
+            return DD_E_NCCL;                                                      \
+        }                                                                          \
+    } while (0)
+
 dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     const double t0 = now_ms();
     CK(cudaSetDevice(ctx->device));
-    if (ctx->world > 1) {
+    if (ctx->world > 1 && ctx->comm == DD_COMM_NCCL) {
         ncclComm_t comm;
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof id);
@@ -243,6 +348,11 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     if (!sidx.empty())
         CK(cudaMemcpy(ws->d_send_idx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(cudaDeviceSynchronize());
+    if (ctx->world > 1 && ctx->comm == DD_COMM_LOCAL) {
+        CK(cudaEventCreateWithFlags(&ws->xev_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ws->xev_done, cudaEventDisableTiming));
+        TRY(local_join(ctx, nccl_id));
+    }
     ctx->setup_ms[5] = now_ms() - t0;
     return DD_OK;
 }
@@ -254,10 +364,55 @@ ddk::RedArgs red_args(dd_ctx *c) {
 }
 
 // world > 1: all-gather the rank-local (s, c) pairs and finalize in rank order.
+// DD_COMM_LOCAL all-gather of the ranks' loc[0 .. 2nv) into gathered[q * 2nv]
+dd_status local_allgather(dd_ctx *c, int nv, cudaStream_t st) {
+    LocalGroup *G = group_of(c);
+    Workspace *ws = ws_of(c);
+    const size_t bytes = 2 * (size_t)nv * sizeof(double);
+    CK(cudaEventRecord(ws->xev_ready, st));
+    RENDEZVOUS(G);
+    for (int q = 0; q < c->world; ++q) {
+        Workspace *pw = ws_of(G->members[q]);
+        if (q != c->rank) CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
+        CK(cudaMemcpyAsync(ws->gathered + 2 * (size_t)nv * q, pw->loc, bytes, cudaMemcpyDefault, st));
+    }
+    CK(cudaEventRecord(ws->xev_done, st));
+    RENDEZVOUS(G);
+    for (int q = 0; q < c->world; ++q)
+        if (q != c->rank) CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_done, 0));
+    return DD_OK;
+}
+
+// DD_COMM_LOCAL halo: copy every peer's send segment for this rank into xg
+dd_status local_halo(dd_ctx *c, cudaStream_t st) {
+    LocalGroup *G = group_of(c);
+    Workspace *ws = ws_of(c);
+    CK(cudaEventRecord(ws->xev_ready, st));
+    RENDEZVOUS(G);
+    for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) continue;
+        const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
+        if (!rn) continue;
+        Workspace *pw = ws_of(G->members[q]);
+        CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
+        CK(cudaMemcpyAsync(ws->xg + 3 * ro, pw->sendbuf + 3 * pw->send_off[c->rank], 3 * rn * sizeof(double),
+                           cudaMemcpyDefault, st));
+    }
+    CK(cudaEventRecord(ws->xev_done, st));
+    RENDEZVOUS(G);
+    for (int q = 0; q < c->world; ++q)
+        if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
+            CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_done, 0));
+    return DD_OK;
+}
+
 dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaStream_t st) {
     if (c->world <= 1) return DD_OK;
     Workspace *ws = ws_of(c);
-    NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
+    if (c->comm == DD_COMM_LOCAL)
+        TRY(local_allgather(c, nv, st));
+    else
+        NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
     ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ra, op, st);
     ++c->n_launches;
     return DD_OK;
@@ -269,6 +424,7 @@ dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
     Workspace *ws = ws_of(c);
     const int64_t ns = ws->send_off[c->world];
     if (ns) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
+    if (c->comm == DD_COMM_LOCAL) return local_halo(c, st);
     auto comm = reinterpret_cast<ncclComm_t>(c->nccl);
     NK(ncclGroupStart());
     for (int q = 0; q < c->world; ++q) {
@@ -418,6 +574,12 @@ dd_status dd_setup(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out) {
     ctx->rank = o->rank;
     ctx->world = std::max(1, o->world);
     ctx->host_only = o->host_only != 0;
+    ctx->comm = o->comm;
+    if (ctx->comm != DD_COMM_NCCL && ctx->comm != DD_COMM_LOCAL) {
+        set_error("dd_setup: unknown comm");
+        delete ctx;
+        return DD_E_INVALID_ARG;
+    }
     if (ctx->rank < 0 || ctx->rank >= ctx->world || (ctx->world > 1 && !o->nccl_unique_id && !ctx->host_only)) {
         set_error("dd_setup: bad rank/world or missing nccl_unique_id");
         delete ctx;
@@ -448,6 +610,7 @@ void dd_destroy(dd_ctx *c) {
     if (!c->host_only) {
         cudaSetDevice(c->device);
         cudaDeviceSynchronize();
+        local_leave(c);
         for (Slab *sl : {&c->slab_lvl, &c->slab_spin}) {
             cudaFree(sl->d_bytes);
             cudaFree(sl->d_info);
@@ -468,6 +631,8 @@ void dd_destroy(dd_ctx *c) {
             cudaFreeHost(ws->h_ctl);
             cudaFreeHost(ws->h_tol);
             for (auto e : ws->ev)
+                if (e) cudaEventDestroy(e);
+            for (auto e : {ws->xev_ready, ws->xev_done})
                 if (e) cudaEventDestroy(e);
             cudaFree(ws->d_send_idx);
             cudaFreeHost(ws->h_sc);

@@ -464,6 +464,15 @@ static RingFn pick_ring(int ring, bool spin) {
 
 static int ring_chunk(int ring) { return ring / 8; }
 
+// the dynamic shared-memory attribute is per function and shared by every
+// context: always raise it to the device maximum minus the static part
+template <class F>
+static void allow_max_smem(F fn, int smem_max) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max - (int)fa.sharedSizeBytes);
+}
+
 }  // namespace ddk
 
 namespace ddi {
@@ -498,7 +507,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         // the attribute is per function and shared by every context: set the maximum
-        cudaFuncSetAttribute(k_apply_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        allow_max_smem(k_apply_direct, smem_max);
     }
     // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
     // Ring choice: the consumer sweep is latency-bound, so maximise resident
@@ -513,7 +522,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             const int nst = rc / ring_chunk(rc);
             const int sm = vec_bytes + rc + 16 * nst + (spin ? vec_bytes / 6 : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
-            cudaFuncSetAttribute(pick_ring(rc, spin), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+            allow_max_smem(pick_ring(rc, spin), smem_max);
             int occ = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(rc, spin), TC + 32, sm);
             if (occ > best_occ) {

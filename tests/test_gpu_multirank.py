@@ -1,0 +1,148 @@
+"""Multi-rank device path on ONE GPU: world 2 and 3 as contexts of this process
+(DD_COMM_LOCAL, one host thread per rank), so the rank ranges, ghost columns
+of the SpMV, send-row gathers, halo copies, rank-ordered dot combination and
+the collective BiCGSTAB all run on the device and are checked against the
+oracle. The NCCL transport differs only in the two exchange calls (halo and
+all-gather, api.cpp); its host-side logic is covered by test_multirank_host.py.
+"""
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2508_04917_b200 as dd
+from inputs.gen import (apply_input, bsr_to_scipy, laplacian_bsr3, manufactured_rhs, random_block_grid,
+                        spe10_style_bsr3)
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "random_8sub": (lambda: random_block_grid(16, 12, 10, seed=21), dict(grid=(16, 12, 10), tiles=(8, 6, 5))),
+    "laplace_24^3": (lambda: laplacian_bsr3(24, 24, 24), dict(grid=(24, 24, 24), tiles=(8, 8, 8))),
+    "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),
+    "spe10_small": (lambda: spe10_style_bsr3(20, 40, 20, upper_ness_from=10)[:3],
+                    dict(grid=(20, 40, 20), tiles=(10, 20, 10))),
+}
+
+
+def run_ranks(world, fn):
+    """fn(rank, barrier) in `world` threads; returns the per-rank results."""
+    bar = threading.Barrier(world)
+    with ThreadPoolExecutor(world) as ex:
+        futs = [ex.submit(fn, r, bar) for r in range(world)]
+        return [f.result(timeout=600) for f in futs]
+
+
+@pytest.mark.parametrize("name,world", [("random_8sub", 2), ("random_8sub", 3), ("laplace_24^3", 2),
+                                        ("chunks_ragged_oddP", 2), ("spe10_small", 3)])
+def test_local_world_parity(name, world):
+    import torch
+    gen, kw = CASES[name]
+    rp, ci, v = gen()
+    S = oracle.setup(rp, ci, v, **kw)
+    N = S["n"]
+    r_glob = apply_input(N)
+    z_ref = oracle.apply(S, r_glob)
+    y_ref = oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], r_glob)
+    xs, b = manufactured_rhs(rp, ci, v)
+    n2o = S["new_to_old"]
+    b_re = b.reshape(-1, 3)[n2o].ravel()
+    _, rep_ref = oracle.bicgstab(S, b_re, tol=1e-8, max_iter=2000)
+    key = os.urandom(128)
+
+    def rank_fn(rank, bar):
+        torch.cuda.set_device(0)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = dd.dd_setup(rp, ci, v, rank=rank, world=world, nccl_id=key, comm="local", **kw)
+            f, n = ctx.row_first, ctx.n_local
+            sl = slice(3 * f, 3 * (f + n))
+            out = {"first": f, "n": n}
+            r = torch.from_numpy(r_glob[sl].copy()).cuda()
+            z = torch.empty_like(r)
+            ctx.apply(r, z, stream=st)          # never communicates
+            y = torch.empty_like(r)
+            ctx.spmv(r, y, stream=st)           # collective: halo
+            st.synchronize()
+            out["z"], out["y"] = z.cpu().numpy(), y.cpu().numpy()
+            bl = torch.from_numpy(b_re[sl].copy()).cuda()
+            x = torch.zeros_like(bl)
+            out["rep"] = ctx.bicgstab(bl, x, tol=1e-8, max_iter=2000, stream=st)
+            out["x"] = x.cpu().numpy()
+            xh = np.zeros(3 * N)
+            out["rep_host"] = ctx.solve_host(b, xh, tol=1e-8, max_iter=2000, stream=st)
+            out["xh"] = xh
+            bar.wait()
+            ctx.destroy()
+            return out
+
+    res = run_ranks(world, rank_fn)
+    # the ranks own a contiguous cover of the reordered rows, in rank order
+    assert res[0]["first"] == 0 and sum(o["n"] for o in res) == N
+    assert all(res[q]["first"] + res[q]["n"] == res[q + 1]["first"] for q in range(world - 1))
+    assert all(o["n"] > 0 for o in res)
+    z = np.concatenate([o["z"] for o in res])
+    y = np.concatenate([o["y"] for o in res])
+    assert np.array_equal(z, z_ref), "apply not bitwise across ranks"
+    assert np.array_equal(y, y_ref), "SpMV with halo not bitwise"
+    its = {o["rep"]["iterations"] for o in res}
+    assert len(its) == 1, f"ranks disagree on the iteration count: {its}"
+    it = its.pop()
+    assert all(o["rep"]["converged"] == 1 for o in res)
+    assert abs(it - rep_ref["iterations"]) <= 2, (it, rep_ref["iterations"])
+    assert max(o["rep"]["true_rel_resid"] for o in res) <= 10 * 1e-8
+    # the assembled solution solves the ORIGINAL system (residual computed
+    # here with scipy; the SPE10-style case is too ill-conditioned for a
+    # forward-error bar at tol 1e-8)
+    A = bsr_to_scipy(rp, ci, v)
+    x = np.concatenate([o["x"] for o in res])
+    x_orig = np.empty_like(x)
+    x_orig.reshape(-1, 3)[n2o] = x.reshape(-1, 3)
+    assert np.linalg.norm(b - A @ x_orig) <= 10 * 1e-8 * np.linalg.norm(b)
+    # dd_solve_host: every rank writes its own rows of the original-order x
+    xh = sum(o["xh"] for o in res)
+    assert np.linalg.norm(b - A @ xh) <= 10 * 1e-8 * np.linalg.norm(b)
+    assert all(o["rep_host"]["iterations"] == it for o in res)
+
+
+def test_local_world_matches_single_rank_iterations():
+    """The same solve at world 1 and world 2 takes the same number of
+    iterations (dots combined in rank order in double-double)."""
+    import torch
+    gen, kw = CASES["laplace_24^3"]
+    rp, ci, v = gen()
+    xs, b = manufactured_rhs(rp, ci, v)
+    ctx1 = dd.dd_setup(rp, ci, v, **kw)
+    x1 = np.zeros_like(b)
+    it1 = ctx1.solve_host(b, x1, tol=1e-10)["iterations"]
+    key = os.urandom(128)
+
+    def rank_fn(rank, bar):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = dd.dd_setup(rp, ci, v, rank=rank, world=2, nccl_id=key, comm="local", **kw)
+            xh = np.zeros_like(b)
+            rep = ctx.solve_host(b, xh, tol=1e-10, stream=st)
+            bar.wait()
+            ctx.destroy()
+            return rep["iterations"], xh
+
+    res = run_ranks(2, rank_fn)
+    assert res[0][0] == res[1][0]
+    assert abs(res[0][0] - it1) <= 0.5
+    assert np.abs(res[0][1] + res[1][1] - x1).max() <= 1e-9 * np.abs(x1).max()
+
+
+def test_local_world_bad_arguments():
+    """world > 1 without a group key, or a rank outside the world, fail loudly
+    before any rendezvous."""
+    rp, ci, v = random_block_grid(8, 8, 8, seed=2)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, v, P=64, rank=0, world=2, nccl_id=None, comm="local")
+    assert e.value.name == "DD_E_INVALID_ARG"
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup(rp, ci, v, P=64, rank=2, world=2, nccl_id=os.urandom(128), comm="local")
+    assert e.value.name == "DD_E_INVALID_ARG"
