@@ -101,6 +101,8 @@ typedef struct {
 #define DD_LEVELSET 1  /* level sets + CTA barriers between levels (Alg. 6)        */
 #define DD_SPINLOOP 2  /* per-row ready flags in shared memory, no level barriers (Alg. 4) */
 #define DD_DIRECT 4    /* ablation: level-set kernel reading factors straight from HBM  */
+#define DD_UNFUSED 8   /* ablation of the L->D->U fusion (sec. 4.4): the L sweep and the
+                          D+U sweep as two launches, z makes an HBM round trip between */
 
 typedef struct {
     int32_t subdomain_rows;   /* P when grid == NULL: contiguous chunks (R26)   */

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libdd.so")
 if os.environ.get("DD_LIB"):
     LIB_PATH = os.path.abspath(os.environ["DD_LIB"])
 
-DD_LEVELSET, DD_SPINLOOP, DD_DIRECT = 1, 2, 4
+DD_LEVELSET, DD_SPINLOOP, DD_DIRECT, DD_UNFUSED = 1, 2, 4, 8
 DD_PART_CHUNKS, DD_PART_BFS = 0, 1
 DD_COMM_NCCL, DD_COMM_LOCAL = 0, 1
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",

@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
 template <uint32_t RING, uint32_t CH, bool SPIN>
 __global__ void __launch_bounds__(TC + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
-                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip) {
+                 const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
+                 int phase) {
     // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
@@ -323,10 +324,13 @@ __global__ void __launch_bounds__(TC + 32, 1)
                 const int64_t rlo = (24 * (int64_t)si.row0) & ~(int64_t)15;
                 const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
                 const uint32_t rb = (uint32_t)(rhi - rlo);
-                const uint32_t total = rb + (uint32_t)si.stream_bytes;
+                // phase 0: the whole stream; 1: the L section; 2: the D+U section
+                const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
+                const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
+                const uint32_t total = rb + (sec_hi - sec_lo);
                 const uint32_t nch = (total + CH - 1) / CH;
                 const uint8_t *rsrc = reinterpret_cast<const uint8_t *>(r) + rlo;
-                const uint8_t *fsrc = slab + si.stream_off;
+                const uint8_t *fsrc = slab + si.stream_off + sec_lo;
                 for (uint32_t c = 0; c < nch; ++c, ++g) {
                     const uint32_t st = g % NST;
                     if (g >= NST) mbar_wait(&empty[st], ((g / NST) - 1u) & 1u);
@@ -371,7 +375,9 @@ __global__ void __launch_bounds__(TC + 32, 1)
         const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
         const uint32_t rb = (uint32_t)(rhi - rlo);
         const uint32_t shift = (uint32_t)(24 * (int64_t)si.row0 - rlo);
-        const uint32_t total = rb + (uint32_t)si.stream_bytes;
+        const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
+        const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
+        const uint32_t total = rb + (sec_hi - sec_lo);
         const uint32_t nch = (total + CH - 1) / CH;
         const uint32_t nd = 3u * si.nrows;
         const uint32_t abs0 = gbase * CH;
@@ -402,7 +408,8 @@ __global__ void __launch_bounds__(TC + 32, 1)
             // records and the ring are 16-byte aligned
             const uint4 c8 = *reinterpret_cast<const uint4 *>(ring + ((pos + 16u) & (RING - 1u)));
             const bool upper = (h.flags & ddi::REC_UPPER) != 0;
-            const bool last = (h.flags & ddi::REC_LAST) != 0;
+            // the section ends with its last record (phase 1 stops before D+U)
+            const bool last = (h.flags & ddi::REC_LAST) != 0 || ro + h.bytes >= total;
             // L level 0 carries no blocks (z_i = r_i in place): the level set
             // skips it (no work, no barrier); the sync-free sweep publishes flags
             const bool skip = !SPIN && !upper && h.K == 0 && !last;
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
 }
 
 // ------------------------------------------------------------ host side
-using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *);
+using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int);
 
 template <uint32_t RING, uint32_t CH, bool SPIN>
 static RingFn ring_fn() {
@@ -544,7 +551,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
         return DD_OK;
     };
     // every variant walks the same level-ordered slab: prepare all of them
-    ctx->variants = DD_LEVELSET | DD_SPINLOOP | DD_DIRECT;
+    ctx->variants = DD_LEVELSET | DD_SPINLOOP | DD_DIRECT | DD_UNFUSED;
     {
         dd_status st = choose(ctx->cfg_lvl, false, ctx->slab_lvl.max_rec_bytes);
         if (st != DD_OK) return st;
@@ -573,7 +580,17 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     } else if (variant == DD_LEVELSET) {
         const LaunchCfg &c = ctx->cfg_lvl;
         pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode, skip);
+                                                                   nsl, r, z, vec_bytes, mode, skip, 0);
+    } else if (variant == DD_UNFUSED) {
+        // ablation of the fusion (sec. 4.4): the L sweep and the D+U
+        // sweep as two launches of the same kernel; the vector makes a round
+        // trip through HBM in between (z holds L^-1 r after the first)
+        const LaunchCfg &c = ctx->cfg_lvl;
+        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+                                                                   nsl, r, z, vec_bytes, mode, skip, 1);
+        ++ctx->n_launches;
+        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+                                                                   nsl, z, z, vec_bytes, mode, skip, 2);
     } else if (variant == DD_SPINLOOP) {
         if (!(ctx->variants & DD_SPINLOOP)) {
             set_error("dd_apply: sync-free variant unavailable (its ready flags do not fit shared memory)");
@@ -581,7 +598,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
         }
         const LaunchCfg &c = ctx->cfg_spin;
         pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                  nsl, r, z, vec_bytes, mode, skip);
+                                                                  nsl, r, z, vec_bytes, mode, skip, 0);
     } else {
         set_error("dd_apply: unknown variant");
         return DD_E_INVALID_ARG;

@@ -57,8 +57,10 @@ struct SubInfo {
     int32_t row0;         // first local block row
     int32_t nrows;        // P_s
     int32_t n_rec;        // number of records
+    int32_t u_off;        // byte offset of the first D+U record (the L section's size)
+    int32_t pad_;
 };
-static_assert(sizeof(SubInfo) == 24, "SubInfo layout");
+static_assert(sizeof(SubInfo) == 32, "SubInfo layout");
 
 // Sliced-ELL SpMV operand: slices of 32 consecutive rows, slot (k, lane) of
 // slice s at slot_ptr[s] + 32*k + lane; values as 9 planes of 32 per k.

@@ -10,6 +10,8 @@
 // final rounding except in rare straddling cases.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdlib>
 
 #include "dd_internal.h"
@@ -169,17 +171,28 @@ __device__ __forceinline__ bool grid_reduce(DD (&v)[NV], DD *partials, unsigned 
     __syncthreads();
     if (!last) return false;
     __threadfence();
-    if (wid == 0) {
+    // the last block combines the partials: thread t takes blocks t, t + bd,
+    // ... in order, then warps and the block combine in a fixed tree (the
+    // grid is fixed per context, so the result is deterministic)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        DD acc{0.0, 0.0};
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+            const double2 pv = __ldcg(reinterpret_cast<const double2 *>(&partials[b * NV + q]));
+            acc = dd_plus(acc, DD{pv.x, pv.y});
+        }
+        acc = warp_reduce_dd(acc);
+        if (lane == 0) sh[q][wid] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-            DD acc{0.0, 0.0};
-            for (int b = lane; b < (int)gridDim.x; b += 32) {
-                const double2 pv = __ldcg(reinterpret_cast<const double2 *>(&partials[b * NV + q]));
-                acc = dd_plus(acc, DD{pv.x, pv.y});
-            }
-            out[q] = warp_reduce_dd(acc);
+            DD acc = sh[q][0];
+            for (int w = 1; w < nw; ++w) acc = dd_plus(acc, sh[q][w]);
+            out[q] = acc;
         }
-        if (lane == 0) *counter = 0u;
+        *counter = 0u;
     }
     return threadIdx.x == 0;
 }
@@ -214,7 +227,10 @@ __global__ void __launch_bounds__(256, MINB) k_spmv(int64_t n_rows, int64_t n_sl
     const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     DD d0{0.0, 0.0}, d1{0.0, 0.0};
-    for (int64_t sl = warp0; sl < n_slices; sl += nwarps) {
+    // plain mode: grid-stride over slices; fused-dot modes are launched with
+    // one warp per slice, so the dot accumulators are not live across the
+    // block loop (register pressure -> occupancy, the SpMV is latency-bound)
+    for (int64_t sl = warp0; sl < n_slices; sl += (MODE == SPMV_PLAIN ? nwarps : n_slices)) {
         const int64_t base = slot_ptr[sl];
         const int K = (int)((slot_ptr[sl + 1] - base) >> 5);
         const int64_t row = 32 * sl + lane;
@@ -466,17 +482,22 @@ static int env_i(const char *n, int d) {
     return v ? atoi(v) : d;
 }
 
+static int spmv_fused_grid(const dd_ctx *ctx) {
+    return (int)std::max<int64_t>(1, (ctx->spmv.n_slices + 7) / 8);
+}
+
 void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
                  const RedArgs &ra, cudaStream_t st) {
     ++ctx->n_launches;
     const auto &S = ctx->spmv;
-    const int grid = ctx->num_sms * 8;  // fixed: determinism of the fused dots
+    const int grid = ctx->num_sms * 8;           // plain: grid-stride
+    const int grid1 = spmv_fused_grid(ctx);      // fused dots: one warp per slice (fixed per context)
     static const int mb0 = env_i("DD_SPMV_MINB_0", 1), mb1 = env_i("DD_SPMV_MINB_1", 5),
                      mb2 = env_i("DD_SPMV_MINB_2", 5);
     switch (mode) {
         case SPMV_PLAIN: spmv_go<SPMV_PLAIN>(mb0, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
-        case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(mb1, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
-        case SPMV_TS_TT: spmv_go<SPMV_TS_TT>(mb2, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(mb1, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_TS_TT: spmv_go<SPMV_TS_TT>(mb2, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
     }
 }
 
@@ -530,6 +551,8 @@ void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const dou
     ++ctx->n_launches;
     k_scatter3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
 }
-size_t partials_bytes(const dd_ctx *ctx) { return sizeof(DD) * 2 * (size_t)(ctx->num_sms * 8); }
+size_t partials_bytes(const dd_ctx *ctx) {
+    return sizeof(DD) * 2 * (size_t)std::max<int64_t>(ctx->num_sms * 8, spmv_fused_grid(ctx));
+}
 
 }  // namespace ddk

@@ -746,6 +746,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             int32_t nrec = 0;
             int64_t mr = 0;
             pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp);
+            slab.info[q].u_off = (int32_t)per[q].size();
             pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp);
             slab.info[q].stream_bytes = (int32_t)per[q].size();
             slab.info[q].row0 = (int32_t)la;

@@ -15,7 +15,7 @@ from tests.parity import assert_setup_bitwise
 
 pytestmark = pytest.mark.gpu
 ALL = dd.DD_LEVELSET | dd.DD_SPINLOOP | dd.DD_DIRECT
-VARIANTS = [dd.DD_LEVELSET, dd.DD_SPINLOOP, dd.DD_DIRECT]
+VARIANTS = [dd.DD_LEVELSET, dd.DD_SPINLOOP, dd.DD_DIRECT, dd.DD_UNFUSED]
 
 CASES = {
     # name: (generator, setup kwargs)
@@ -57,7 +57,7 @@ def test_setup_bitwise(name):
     assert_setup_bitwise(ctx, S)
 
 
-@pytest.mark.parametrize("variant", VARIANTS, ids=["levelset", "spin", "direct"])
+@pytest.mark.parametrize("variant", VARIANTS, ids=["levelset", "spin", "direct", "unfused"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_apply_parity(name, variant):
     import torch

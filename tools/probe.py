@@ -35,7 +35,7 @@ def timeit(fn, reps):
         e0.record(); fn(); e1.record(); torch.cuda.synchronize()
         if i >= 3: ts.append(e0.elapsed_time(e1))
     return float(np.median(ts)), float(np.min(ts))
-for var, name in ((1, "levelset"), (2, "spin"), (4, "direct")):
+for var, name in ((1, "levelset"), (2, "spin"), (4, "direct"), (8, "unfused")):
     med, mn = timeit(lambda: ctx.apply(r, z, var), a.reps)
     print(f"apply {name:9s} median {med*1e3:8.1f} us  min {mn*1e3:8.1f} us  canonical {st['apply_canonical_bytes']/med/1e6:7.1f} GB/s  slab {st['slab_bytes_levelset']/med/1e6:7.1f} GB/s  launch {ctx.launch_info(var)}", flush=True)
 y = torch.empty_like(r)
