@@ -199,6 +199,8 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     refactor_ms = 1e3 * (time.perf_counter() - t0) / 3
     del vd
+    # Alg. 5 level assignment on the device, kernel time
+    levels_device_ms = ctx.levels_device()[2]
     st = ctx.stats()
     m = 3 * ctx.n_local
     stream = torch.cuda.current_stream()
@@ -289,6 +291,7 @@ def run_ours(args, cfg):
         "iterations": r0["iterations"], "n_applies": r0["n_applies"], "true_rel_resid": r0["true_rel_resid"],
         "setup_ms": round(setup_ms, 1),
         "refactor_ms": round(refactor_ms, 2),
+        "levels_device_ms": round(levels_device_ms, 3),
         "apply": {"ms": round(apply_ms, 4), "launches": prof["n_apply"],
                   "canonical_bytes": canon, "gbs_canonical": round(achieved, 1),
                   "frac_of_8TBs": round(achieved / 8000.0, 4), "frac_of_measured": round(achieved / peak, 4),

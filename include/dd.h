@@ -212,6 +212,14 @@ dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original or
                            int32_t *new_to_old /*[N]*/);
 /* which: 0 = L (hmapL), 1 = U (hmapU); local rows, reordered order. */
 dd_status dd_get_levels(const dd_ctx *ctx, int32_t which, int32_t *hmap);
+
+/* Alg. 5 on the device: the paper's fixpoint
+ * level marking, one CTA per subdomain, over this rank's L and U factor
+ * patterns. Writes hmapL and hmapU (host arrays of n_local int32 each, may be
+ * NULL) and the kernel time in ms (may be NULL). The result equals
+ * dd_get_levels (longest path, R16). Synchronous; DD_E_INVALID_ARG for a
+ * host_only context. */
+dd_status dd_levels_device(dd_ctx *ctx, int32_t *hmapL, int32_t *hmapU, double *ms);
 /* Factors of the local rows in the dropped pattern, reordered local numbering
  * (columns local too). Pass NULL arrays to query sizes only.
  *   L: strictly-lower blocks (unit diagonal implied); U: strictly-upper

@@ -31,7 +31,7 @@ STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP"
           "DD_E_NCCL", "DD_E_OOM", "DD_E_BREAKDOWN", "DD_E_MAXITER", "DD_E_NO_DEVICE"]
 EXPORTS = ["dd_setup", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
-           "dd_get_levels", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
+           "dd_get_levels", "dd_levels_device", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
            "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_last_error"]
 
 
@@ -84,7 +84,7 @@ def lib():
             "dd_apply": [P, P, P, P], "dd_apply_variant": [P, i32, P, P, P], "dd_spmv": [P, P, P, P],
             "dd_bicgstab": [P, P, P, d, i32, P, P, P], "dd_solve_host": [P, P, P, d, i32, P, P],
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
-            "dd_get_levels": [P, i32, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
+            "dd_get_levels": [P, i32, P], "dd_levels_device": [P, P, P, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
             "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_refactor": [P, P, i32, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
             "dd_last_error": [],
         }
@@ -213,6 +213,14 @@ class Context:
         _check(lib().dd_get_levels(self.h, 0 if which in (0, "L") else 1, _ptr(h)))
         return h
 
+    def levels_device(self):
+        """Alg. 5 on the device: (hmapL, hmapU, kernel ms)."""
+        hl = np.empty(self.n_local, np.int32)
+        hu = np.empty(self.n_local, np.int32)
+        ms = C.c_double()
+        _check(lib().dd_levels_device(self.h, _ptr(hl), _ptr(hu), C.byref(ms)))
+        return hl, hu, ms.value
+
     def factors(self):
         nL, nU = C.c_int64(), C.c_int64()
         _check(lib().dd_get_factors(self.h, C.byref(nL), C.byref(nU), *([None] * 7)))
@@ -336,6 +344,10 @@ def dd_local_range(ctx):
 
 def dd_get_partition(ctx):
     return ctx.partition()
+
+
+def dd_levels_device(ctx):
+    return ctx.levels_device()
 
 
 def dd_get_levels(ctx, which):

@@ -16,6 +16,7 @@
 
 #include "dd_internal.h"
 #include "krylov.cuh"
+#include "levels.cuh"
 #include "refactor.cuh"
 
 namespace ddi {
@@ -885,6 +886,59 @@ dd_status dd_get_levels(const dd_ctx *c, int32_t which, int32_t *hmap) {
     const auto &h = which == 0 ? c->hmapL : c->hmapU;
     std::memcpy(hmap, h.data(), h.size() * sizeof(int32_t));
     return DD_OK;
+}
+
+dd_status dd_levels_device(dd_ctx *c, int32_t *hmapL, int32_t *hmapU, double *ms) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    CK(cudaSetDevice(c->device));
+    const int nsl = c->sub_last - c->sub_first;
+    const int64_t nl = c->n_local;
+    std::vector<int64_t> sub(nsl + 1);
+    for (int q = 0; q <= nsl; ++q) sub[q] = c->sub_ptr[c->sub_first + q] - c->row_first;
+    int64_t *d_sub = nullptr, *d_rp = nullptr;
+    int32_t *d_ci = nullptr, *d_h = nullptr;
+    const int64_t nci = std::max<int64_t>(1, std::max(c->Lci.size(), c->Uci.size()));
+    dd_status st = DD_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    float tot = 0.0f;
+    do {
+        if ((st = dmalloc(&d_sub, nsl + 1)) != DD_OK || (st = dmalloc(&d_rp, nl + 1)) != DD_OK ||
+            (st = dmalloc(&d_ci, nci)) != DD_OK || (st = dmalloc(&d_h, std::max<int64_t>(1, nl))) != DD_OK)
+            break;
+        if (cudaMemcpy(d_sub, sub.data(), sub.size() * sizeof(int64_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+            set_error("dd_levels_device: CUDA setup failed");
+            st = DD_E_CUDA;
+            break;
+        }
+        for (int which = 0; which < 2 && st == DD_OK; ++which) {
+            const auto &rp = which == 0 ? c->Lrp : c->Urp;
+            const auto &ci = which == 0 ? c->Lci : c->Uci;
+            int32_t *out = which == 0 ? hmapL : hmapU;
+            cudaMemcpy(d_rp, rp.data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
+            if (!ci.empty()) cudaMemcpy(d_ci, ci.data(), ci.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+            cudaEventRecord(e0);
+            if (nsl) ddk::launch_levels(nsl, d_sub, d_rp, d_ci, d_h, c->max_P, nullptr);
+            cudaEventRecord(e1);
+            if (cudaEventSynchronize(e1) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+                set_error("dd_levels_device: kernel failed");
+                st = DD_E_CUDA;
+                break;
+            }
+            float t = 0.0f;
+            cudaEventElapsedTime(&t, e0, e1);
+            tot += t;
+            if (out && nl) cudaMemcpy(out, d_h, nl * sizeof(int32_t), cudaMemcpyDeviceToHost);
+        }
+    } while (0);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(d_sub);
+    cudaFree(d_rp);
+    cudaFree(d_ci);
+    cudaFree(d_h);
+    if (ms) *ms = tot;
+    return st;
 }
 
 dd_status dd_get_factors(const dd_ctx *c, int64_t *nL, int64_t *nU, int64_t *Lrp, int32_t *Lci, double *Lv,

@@ -260,3 +260,13 @@ def test_refactor_cfg3_full_size_timing_and_parity(cfg3):
     torch.cuda.synchronize()
     assert np.array_equal(z.cpu().numpy(), oracle.apply(S, r))
     print(f"refactor 160^3: {dt * 1e3:.1f} ms")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_levels_device_alg5_bitwise(name):
+    """Alg. 5 fixpoint marking on the device (one CTA per subdomain) gives the
+    oracle's longest-path levels exactly."""
+    _, _, _, S, ctx = get_case(name)
+    hl, hu, ms = ctx.levels_device()
+    assert np.array_equal(hl, S["hmapL"]) and np.array_equal(hu, S["hmapU"])
+    assert ms > 0
