@@ -67,6 +67,13 @@ struct Workspace {
     std::vector<int64_t> send_off;  // [world + 1]
     // DD_COMM_LOCAL: "my send data is ready" / "I have copied my peers' data"
     cudaEvent_t xev_ready = nullptr, xev_done = nullptr;
+    // CUDA-graph solve loop (one executable graph per solution vector)
+    cudaStream_t cap = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    double *gx = nullptr, *ghist = nullptr;  // the captured body's x and history buffers
+    int64_t g_launches = 0;
+    int *h_max = nullptr;  // pinned
 };
 
 // ---------------------------------------------------------------- DD_COMM_LOCAL
@@ -333,6 +340,7 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     CK(cudaMemset(ws->ctl, 0, 8 * sizeof(int)));
     CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_ctl), 16 * sizeof(int)));
     CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_tol), sizeof(double)));
+    CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_max), sizeof(int)));
     CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     // halo buffers
@@ -631,6 +639,10 @@ void dd_destroy(dd_ctx *c) {
             cudaFree(ws->d_hist);
             cudaFreeHost(ws->h_ctl);
             cudaFreeHost(ws->h_tol);
+            cudaFreeHost(ws->h_max);
+            if (ws->gexec) cudaGraphExecDestroy(ws->gexec);
+            if (ws->graph) cudaGraphDestroy(ws->graph);
+            if (ws->cap) cudaStreamDestroy(ws->cap);
             for (auto e : ws->ev)
                 if (e) cudaEventDestroy(e);
             for (auto e : {ws->xev_ready, ws->xev_done})
@@ -677,6 +689,86 @@ dd_status dd_spmv(dd_ctx *c, const double *x, double *y, void *stream) {
     return DD_OK;
 }
 
+// One Alg. 1 iteration (both half steps). k > 0: the host's iteration index;
+// k < 0: graph mode, the kernels read it from ctl[C_ITER].
+dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaStream_t st) {
+    Workspace *ws = ws_of(c);
+    const int64_t m = ws->m;
+    void *stream = reinterpret_cast<void *>(st);
+    ra.k = k;
+    TRY(timed(c, PK_BLAS, k, st, [&] {
+        ddk::launch_update_p(c, m, k < 0 ? -1 : (k == 1), ws->r, ws->v, ws->p, ws->sc, ws->ctl, st);
+        return DD_OK;
+    }));
+    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream, ws->ctl); }));
+    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st); }));
+    TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
+    TRY(timed(c, PK_BLAS, k, st, [&] {
+        ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
+        return DD_OK;
+    }));
+    TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
+    ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
+    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream, ws->ctl); }));
+    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st); }));
+    TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
+    TRY(timed(c, PK_BLAS, k, st, [&] {
+        ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
+        return DD_OK;
+    }));
+    TRY(reduce_across(c, 2, ddk::FIN_RHO, ra, st));
+    return DD_OK;
+}
+
+// CUDA-graph solve loop: the iteration body captured once per
+// solution vector under a conditional WHILE node, so a whole solve is one
+// graph launch -- no host round trip per iteration or batch. Used for
+// world == 1 when per-kernel profiling is off (DD_GRAPH=0 disables it).
+dd_status graph_solve(dd_ctx *c, const ddk::RedArgs &ra, double *x, int32_t max_iter, cudaStream_t st,
+                      int64_t *launches_per_iter) {
+    Workspace *ws = ws_of(c);
+    if (!ws->gexec || ws->gx != x || ws->ghist != ws->d_hist) {
+        if (ws->gexec) cudaGraphExecDestroy(ws->gexec);
+        if (ws->graph) cudaGraphDestroy(ws->graph);
+        ws->gexec = nullptr;
+        ws->graph = nullptr;
+        if (!ws->cap) CK(cudaStreamCreateWithFlags(&ws->cap, cudaStreamNonBlocking));
+        CK(cudaGraphCreate(&ws->graph, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, ws->graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, ws->graph, nullptr, 0, &p));
+        cudaGraph_t body = p.conditional.phGraph_out[0];
+        const int64_t n0 = c->n_launches;
+        CK(cudaStreamBeginCaptureToGraph(ws->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        ddk::launch_iter_head(ws->ctl, ws->cap);
+        dd_status e = enqueue_iteration(c, ra, -1, x, ws->cap);
+        ddk::launch_iter_tail(ws->ctl, h, ws->cap);
+        cudaGraph_t out = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(ws->cap, &out);
+        if (e != DD_OK) return e;
+        if (ce != cudaSuccess) {
+            set_error(std::string("dd_bicgstab: graph capture failed: ") + cudaGetErrorString(ce));
+            return DD_E_CUDA;
+        }
+        ws->g_launches = c->n_launches - n0;
+        c->n_launches = n0;
+        CK(cudaGraphInstantiate(&ws->gexec, ws->graph, 0));
+        ws->gx = x;
+        ws->ghist = ws->d_hist;
+    }
+    *ws->h_max = max_iter;
+    CK(cudaMemcpyAsync(ws->ctl + ddk::C_MAX, ws->h_max, sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaGraphLaunch(ws->gexec, st));
+    *launches_per_iter = ws->g_launches;
+    return DD_OK;
+}
+
 dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t max_iter, double *hist,
                       dd_report *rep, void *stream) {
     if (!usable(c)) return DD_E_INVALID_ARG;
@@ -715,31 +807,16 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     // every rank waits on the same batch, so all ranks stop together.
     constexpr int BATCH = 2;
     int k_enq = 0, j = 0;
-    for (bool stop = false; !stop; ++j) {
+    static const bool graphs_env = !getenv("DD_GRAPH") || atoi(getenv("DD_GRAPH")) != 0;
+    // world == 1 only: NCCL calls are capturable, but that path is not exercised on this pool
+    const bool use_graph = graphs_env && c->world <= 1 && !(c->prof && reinterpret_cast<Prof *>(c->prof)->on);
+    int64_t g_per_iter = 0;
+    if (use_graph) TRY(graph_solve(c, ra, x, max_iter, st, &g_per_iter));
+    for (bool stop = use_graph; !stop; ++j) {
         for (int q = 0; q < BATCH && k_enq < max_iter; ++q) {
             const int k = ++k_enq;
             ra.k = k;
-            TRY(timed(c, PK_BLAS, k, st, [&] {
-                ddk::launch_update_p(c, m, k == 1, ws->r, ws->v, ws->p, ws->sc, ws->ctl, st);
-                return DD_OK;
-            }));
-            TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream, ws->ctl); }));
-            TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st); }));
-            TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
-            TRY(timed(c, PK_BLAS, k, st, [&] {
-                ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
-                return DD_OK;
-            }));
-            TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
-            ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
-            TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream, ws->ctl); }));
-            TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st); }));
-            TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
-            TRY(timed(c, PK_BLAS, k, st, [&] {
-                ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
-                return DD_OK;
-            }));
-            TRY(reduce_across(c, 2, ddk::FIN_RHO, ra, st));
+            TRY(enqueue_iteration(c, ra, k, x, st));
         }
         int *snap = ws->h_ctl + 8 * (j % 2);
         CK(cudaMemcpyAsync(snap, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -753,6 +830,7 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     CK(cudaMemcpyAsync(ws->h_ctl, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int state = ws->h_ctl[ddk::C_STATE], kf = ws->h_ctl[ddk::C_K], nh = ws->h_ctl[ddk::C_NH];
+    if (use_graph) c->n_launches += g_per_iter * std::max(1, ws->h_ctl[ddk::C_ITER]) + 2 * std::max(1, ws->h_ctl[ddk::C_ITER]);
     std::vector<double> hv(std::max(1, nh));
     CK(cudaMemcpy(hv.data(), ws->d_hist, sizeof(double) * std::max(1, nh), cudaMemcpyDeviceToHost));
     if (hist) std::memcpy(hist, hv.data(), sizeof(double) * nh);

@@ -60,6 +60,7 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 //   FIN_OMEGA tau < 1e-30 -> breakdown, else omega = (t.s) / tau
 //   FIN_RHO   ||r|| < thr -> converged; else |rho_next| < 1e-30 -> breakdown
 __device__ __forceinline__ void finalize(double *sc, int op, const double *val, int *ctl, double *hist, int k) {
+    if (k < 0 && ctl) k = ctl[C_ITER];  // graph mode: the iteration counter lives on the device
     switch (op) {
         case FIN_INIT: {  // ||r0||^2 and rho_1 = rh.r = r.r
             sc[S_RR] = val[0];
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(256) k_update_p(int64_t m, int first, const do
                                                   const double *__restrict__ v, double *__restrict__ p,
                                                   const double *__restrict__ sc, const int *ctl) {
     if (stopped(ctl)) return;
+    if (first < 0) first = ctl[C_ITER] == 1;  // graph mode
     const double omega = sc[S_OMEGA];
     const double beta = (sc[S_RHO] / sc[S_RHO_PREV]) * (sc[S_ALPHA] / omega);
     auto one = [&](double rv, double vv, double pv) { return first ? rv : __fma_rn(beta, __fma_rn(-omega, vv, pv), rv); };
@@ -502,6 +504,15 @@ void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg,
 }
 
 int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 8; }
+
+__global__ void k_iter_head(int *ctl) {
+    if (ctl[C_STATE] == ST_RUN) ctl[C_ITER] += 1;
+}
+__global__ void k_iter_tail(int *ctl, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, (ctl[C_STATE] == ST_RUN && ctl[C_ITER] < ctl[C_MAX]) ? 1u : 0u);
+}
+void launch_iter_head(int *ctl, cudaStream_t st) { k_iter_head<<<1, 1, 0, st>>>(ctl); }
+void launch_iter_tail(int *ctl, cudaGraphConditionalHandle h, cudaStream_t st) { k_iter_tail<<<1, 1, 0, st>>>(ctl, h); }
 
 static inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

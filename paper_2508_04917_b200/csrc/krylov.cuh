@@ -34,7 +34,7 @@ enum : int { FIN_INIT = 1, FIN_ALPHA, FIN_SS, FIN_OMEGA, FIN_RHO, FIN_RESID };
 // convergence / breakdown (R21, R25) and every iteration kernel returns at
 // entry unless ctl[C_STATE] == ST_RUN, so the host can enqueue iterations
 // ahead without synchronising at each half step.
-enum : int { C_STATE = 0, C_K = 1, C_NH = 2, C_CNT = 3 };
+enum : int { C_STATE = 0, C_K = 1, C_NH = 2, C_CNT = 3, C_ITER = 4, C_MAX = 5 };
 enum : int {
     ST_RUN = 0,
     ST_HALF = 1,       // ||s|| < tol ||r0||: x += alpha p_hat pending
@@ -57,8 +57,14 @@ struct RedArgs {
     int finalize;           // 1: last block finalizes (world == 1)
     int *ctl;               // solver control (nullptr: no control, e.g. plain SpMV)
     double *hist;           // residual history [2*max_iter+1] (device)
-    int k;                  // iteration the launch belongs to
+    int k;                  // iteration the launch belongs to (< 0: ctl[C_ITER], graph mode)
 };
+
+// CUDA-graph BiCGSTAB (f4): the iteration body runs under a conditional WHILE
+// node; the head kernel advances ctl[C_ITER], the tail kernel sets the loop
+// condition from the device-side control state.
+void launch_iter_head(int *ctl, cudaStream_t st);
+void launch_iter_tail(int *ctl, cudaGraphConditionalHandle h, cudaStream_t st);
 
 void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg, double *y, const double *aux,
                  const RedArgs &ra, cudaStream_t st);

@@ -270,3 +270,28 @@ def test_levels_device_alg5_bitwise(name):
     hl, hu, ms = ctx.levels_device()
     assert np.array_equal(hl, S["hmapL"]) and np.array_equal(hu, S["hmapU"])
     assert ms > 0
+
+
+@pytest.mark.parametrize("name", ["cfg1_16^3", "random_blocks", "chunks_ragged_oddP", "spe10_style_cfg4"])
+def test_graph_solve_equals_batched_solve(name):
+    """The CUDA-graph solve loop (conditional WHILE node, device-side control)
+    and the host-batched loop (taken while per-kernel profiling is on) run the
+    same kernels on the same data: same iteration count, bitwise-equal x and
+    residual history; max_iter is honoured inside the graph."""
+    import torch
+    rp, ci, v, S, ctx = get_case(name)
+    _, b = manufactured_rhs(rp, ci, v, seed=1)
+    br = torch_vec(b.reshape(-1, 3)[S["new_to_old"]].ravel())
+    xg = torch.zeros_like(br)
+    rg = ctx.bicgstab(br, xg, tol=1e-8, max_iter=5000, hist=True)       # graph
+    ctx.profile(1)
+    xb = torch.zeros_like(br)
+    rb = ctx.bicgstab(br, xb, tol=1e-8, max_iter=5000, hist=True)       # batched
+    ctx.profile(0)
+    assert rg["iterations"] == rb["iterations"]
+    assert torch.equal(xg, xb)
+    assert np.array_equal(rg["resid_hist"], rb["resid_hist"])
+    # max_iter stops the graph loop with DD_E_MAXITER
+    x3 = torch.zeros_like(br)
+    r3 = ctx.bicgstab(br, x3, tol=1e-30, max_iter=3)
+    assert r3["status_name"] == "DD_E_MAXITER" and r3["iterations"] == 3
