@@ -33,6 +33,11 @@ __all__ = [
     "apply_input",
     "bsr_to_scipy",
     "grid_stencil_pattern",
+    "laplacian_csr",
+    "spe10_style_csr",
+    "random_csr_grid",
+    "csr_to_scipy",
+    "manufactured_rhs_csr",
 ]
 
 
@@ -165,6 +170,101 @@ def spe10_style_bsr3(nx: int = 60, ny: int = 220, nz: int = 85, *, seed: int = 1
     dblk[:, d3, d3] += dsum
     vals[diag_pos] = dblk
     return row_ptr, col_idx, vals.reshape(-1), logk
+
+
+# ------------------------------------------------------- scalar CSR inputs
+# (the paper's CSR half; rhd is a scalar 128^3 7-point matrix
+# and spe10 a scalar 7-point matrix on the 60x220x85 grid, Appendix A)
+
+def laplacian_csr(nx: int, ny: int, nz: int):
+    """Scalar 7-point Laplacian: 6 on the diagonal, -1 off it."""
+    row_ptr, col_idx, slot = grid_stencil_pattern(nx, ny, nz)
+    vals = np.where(slot == 3, 6.0, -1.0).astype(np.float64)
+    return row_ptr, col_idx, vals
+
+
+def spe10_style_csr(nx: int = 60, ny: int = 220, nz: int = 85, *, seed: int = 10,
+                    dx: float = 20.0, dy: float = 10.0, dz: float = 2.0, upper_ness_from: int = 35):
+    """Scalar SPE10-style two-point-flux pressure matrix on the same
+    permeability field as spe10_style_bsr3 (seed, seed+1): off-diagonal
+    -T_face, diagonal sum(T_face) + c, c = 1e-3 * mean(T). Returns
+    (row_ptr, col_idx, vals, log10_kx)."""
+    rng_xi = np.random.default_rng(seed)
+    rng_ch = np.random.default_rng(seed + 1)
+    xi = rng_xi.standard_normal((nz, ny, nx))
+    xi = _renorm(_box_smooth_xy(_box_smooth_xy(xi)))
+    logk = np.empty((nz, ny, nx))
+    top = slice(0, min(upper_ness_from, nz))
+    logk[top] = 1.0 + 1.0 * xi[top]
+    if nz > upper_ness_from:
+        low = slice(upper_ness_from, nz)
+        logk[low] = -1.0 + 0.5 * xi[low]
+        xg = np.arange(nx)[None, :]
+        yg = np.arange(ny)[:, None]
+        for kk in range(upper_ness_from, nz):
+            for _ in range(4):
+                x0 = rng_ch.uniform(0.1 * nx, 0.9 * nx)
+                amp = rng_ch.uniform(0.05 * nx, 0.15 * nx)
+                wl = rng_ch.uniform(0.2 * ny, 0.6 * ny)
+                ph = rng_ch.uniform(0.0, 2.0 * np.pi)
+                xc = x0 + amp * np.sin(2.0 * np.pi * yg / wl + ph)
+                logk[kk][np.abs(xg - xc) <= 1.5] = 3.0 + 0.3 * xi[kk][np.abs(xg - xc) <= 1.5]
+    np.clip(logk, -3.0, 4.3, out=logk)
+    kx = 10.0 ** logk
+    kz = 0.1 * kx
+
+    def harm(a, b):
+        return 2.0 * a * b / (a + b)
+
+    tx = (dy * dz / dx) * harm(kx[:, :, :-1], kx[:, :, 1:])
+    ty = (dx * dz / dy) * harm(kx[:, :-1, :], kx[:, 1:, :])
+    tz = (dx * dy / dz) * harm(kz[:-1, :, :], kz[1:, :, :])
+    c = 1e-3 * np.mean(np.concatenate([tx.ravel(), ty.ravel(), tz.ravel()]))
+    n = nx * ny * nz
+    coup = np.zeros((nz, ny, nx, 7))
+    coup[:, :, :-1, 4] = tx
+    coup[:, :, 1:, 2] = tx
+    coup[:, :-1, :, 5] = ty
+    coup[:, 1:, :, 1] = ty
+    coup[:-1, :, :, 6] = tz
+    coup[1:, :, :, 0] = tz
+    coup = coup.reshape(n, 7)
+    row_ptr, col_idx, slot = grid_stencil_pattern(nx, ny, nz)
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    vals = -coup[rows, slot.astype(np.int64)]
+    diag = slot == 3
+    vals[diag] = coup.sum(axis=1)[rows[diag]] + c
+    return row_ptr, col_idx, vals, logk
+
+
+def random_csr_grid(nx: int, ny: int, nz: int, seed: int, dominance: float = 1.0):
+    """7-point grid pattern, random off-diagonals in [-1, 1), row-diagonally
+    dominant diagonal (sum |off| + dominance) with a random sign."""
+    rng = np.random.default_rng(seed)
+    row_ptr, col_idx, slot = grid_stencil_pattern(nx, ny, nz)
+    n = nx * ny * nz
+    vals = rng.uniform(-1.0, 1.0, col_idx.shape[0])
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    off = slot != 3
+    absrow = np.zeros(n)
+    np.add.at(absrow, rows[off], np.abs(vals[off]))
+    dpos = np.nonzero(~off)[0]
+    sign = np.where(rng.uniform(size=n) < 0.5, -1.0, 1.0)
+    vals[dpos] = sign * (absrow + dominance)
+    return row_ptr, col_idx, vals
+
+
+def csr_to_scipy(row_ptr, col_idx, vals):
+    import scipy.sparse as sp
+    n = row_ptr.shape[0] - 1
+    return sp.csr_matrix((vals, col_idx, row_ptr), shape=(n, n))
+
+
+def manufactured_rhs_csr(row_ptr, col_idx, vals, seed: int = 1):
+    """x* ~ U[0,1)^N from default_rng(seed); b = A x* via scipy (library)."""
+    n = row_ptr.shape[0] - 1
+    xs = np.random.default_rng(seed).random(n)
+    return xs, csr_to_scipy(row_ptr, col_idx, vals) @ xs
 
 
 def random_block_grid(nx: int, ny: int, nz: int, seed: int, dominance: float = 1.0):

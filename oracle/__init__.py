@@ -62,6 +62,14 @@ def lib():
             "orc_dot": (dbl, [i64, P, P]),
             "orc_bicgstab": (C.c_int, [i64, P, P, P, i32, P, P, P, P, P, P, P, P, dbl, i32,
                                        P, P]),
+            "orc_s_reorder": (None, [i64, P, P, P, P, P, P, P, P]),
+            "orc_s_drop": (i64, [i64, P, P, P, P, P, P, P]),
+            "orc_s_ilu0": (C.c_int, [i64, P, P, P, dbl, P, P, P]),
+            "orc_s_ildu0": (None, [i64, P, P, P, P, P]),
+            "orc_s_apply": (None, [i64, i32, P, P, P, P, P, P, P, P]),
+            "orc_s_spmv": (None, [i64, P, P, P, P, P]),
+            "orc_s_bicgstab": (C.c_int, [i64, P, P, P, i32, P, P, P, P, P, P, P, P, dbl, i32,
+                                         P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -194,8 +202,9 @@ def levels_upper(rp, ci):
 def apply(S, r):
     r = _c(r, np.float64)
     z = np.empty_like(r)
-    lib().orc_apply(S["n"], S["n_sub"], _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]),
-                    _p(S["lu"]), _p(S["dinv"]), _p(S["uunit"]), _p(r), _p(z))
+    f = lib().orc_s_apply if S.get("bs", 3) == 1 else lib().orc_apply
+    f(S["n"], S["n_sub"], _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]),
+      _p(S["lu"]), _p(S["dinv"]), _p(S["uunit"]), _p(r), _p(z))
     return z
 
 
@@ -239,11 +248,13 @@ def setup(rp, ci, v, *, grid=None, tiles=None, P=None, partitioner="chunks", piv
 def bicgstab(S, b, x0=None, tol=1e-8, max_iter=1000, hist=True):
     """Returns (x, report dict)."""
     n = S["n"]
+    bs = S.get("bs", 3)
     b = _c(b, np.float64)
-    x = np.zeros(3 * n) if x0 is None else _c(x0, np.float64).copy()
+    x = np.zeros(bs * n) if x0 is None else _c(x0, np.float64).copy()
     rh = np.zeros(2 * max_iter + 1) if hist else None
     out = np.zeros(8)
-    lib().orc_bicgstab(n, _p(S["rp_r"]), _p(S["ci_r"]), _p(S["v_r"]), S["n_sub"],
+    f = lib().orc_s_bicgstab if bs == 1 else lib().orc_bicgstab
+    f(n, _p(S["rp_r"]), _p(S["ci_r"]), _p(S["v_r"]), S["n_sub"],
                        _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]), _p(S["lu"]),
                        _p(S["dinv"]), _p(S["uunit"]), _p(b), _p(x), tol, max_iter,
                        _p(rh), _p(out))
@@ -252,3 +263,71 @@ def bicgstab(S, b, x0=None, tol=1e-8, max_iter=1000, hist=True):
     if hist:
         rep["resid_hist"] = rh[: int(out[5])]
     return x, rep
+
+
+# ------------------------------------------------- scalar CSR path (8(f3))
+def s_reorder(rp, ci, v, n2o, o2n):
+    rp, ci, v = _c(rp, np.int64), _c(ci, np.int32), _c(v, np.float64)
+    n2o, o2n = _c(n2o, np.int32), _c(o2n, np.int32)
+    rpo, cio, vo = np.empty_like(rp), np.empty_like(ci), np.empty_like(v)
+    lib().orc_s_reorder(rp.shape[0] - 1, _p(rp), _p(ci), _p(v), _p(n2o), _p(o2n), _p(rpo), _p(cio), _p(vo))
+    return rpo, cio, vo
+
+
+def s_drop(rp, ci, v, label_new):
+    rp, ci, v = _c(rp, np.int64), _c(ci, np.int32), _c(v, np.float64)
+    label_new = _c(label_new, np.int32)
+    n = rp.shape[0] - 1
+    L = lib()
+    kept = L.orc_s_drop(n, _p(rp), _p(ci), _p(v), _p(label_new), None, None, None)
+    rpo, cio, vo = np.empty(n + 1, np.int64), np.empty(kept, np.int32), np.empty(kept, np.float64)
+    L.orc_s_drop(n, _p(rp), _p(ci), _p(v), _p(label_new), _p(rpo), _p(cio), _p(vo))
+    return rpo, cio, vo
+
+
+def s_ilu0(rp, ci, a, pivot_floor=1e-300):
+    rp, ci, a = _c(rp, np.int64), _c(ci, np.int32), _c(a, np.float64)
+    n = rp.shape[0] - 1
+    lu, dinv, bad = np.empty_like(a), np.empty(n, np.float64), np.zeros(1, np.int64)
+    rc = lib().orc_s_ilu0(n, _p(rp), _p(ci), _p(a), pivot_floor, _p(lu), _p(dinv), _p(bad))
+    if rc != 0:
+        raise OracleError(rc, int(bad[0]))
+    return lu, dinv
+
+
+def s_ildu0(rp, ci, lu, dinv):
+    rp, ci = _c(rp, np.int64), _c(ci, np.int32)
+    uunit = np.zeros_like(lu)
+    lib().orc_s_ildu0(rp.shape[0] - 1, _p(rp), _p(ci), _p(lu), _p(dinv), _p(uunit))
+    return uunit
+
+
+def s_spmv(rp, ci, v, x):
+    x = _c(x, np.float64)
+    y = np.empty_like(x)
+    lib().orc_s_spmv(rp.shape[0] - 1, _p(rp), _p(ci), _p(v), _p(x), _p(y))
+    return y
+
+
+def setup_csr(rp, ci, v, *, grid=None, tiles=None, P=None, partitioner="chunks", pivot_floor=1e-300):
+    """The paper's setup pipeline for a SCALAR CSR matrix (vals[nnz]), in the
+    paper's order; the same dict as setup() with bs = 1."""
+    n = rp.shape[0] - 1
+    if tiles is not None:
+        labels = labels_geometric(grid, tiles)
+    elif partitioner == "bfs":
+        labels = labels_bfs(rp, ci, P)
+    else:
+        labels = labels_chunks(n, P)
+    n_sub = int(labels.max()) + 1 if n else 0
+    n2o, o2n = permutation(labels)
+    rp_r, ci_r, v_r = s_reorder(rp, ci, v, n2o, o2n)
+    label_new = labels[n2o]
+    rp_d, ci_d, v_d = s_drop(rp_r, ci_r, v_r, label_new)
+    lu, dinv = s_ilu0(rp_d, ci_d, v_d, pivot_floor)
+    uunit = s_ildu0(rp_d, ci_d, lu, dinv)
+    return dict(bs=1, n=n, n_sub=n_sub, labels=labels, new_to_old=n2o, old_to_new=o2n,
+                sub_ptr=subdomain_ptr(label_new, n_sub), label_new=label_new,
+                rp_r=rp_r, ci_r=ci_r, v_r=v_r, rp_d=rp_d, ci_d=ci_d, v_d=v_d,
+                lu=lu, dinv=dinv, uunit=uunit,
+                hmapL=levels_lower(rp_d, ci_d), hmapU=levels_upper(rp_d, ci_d))

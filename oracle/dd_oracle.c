@@ -356,11 +356,31 @@ double orc_dot(int64_t m, const double *x, const double *y) {
 }
 
 /* ------------------------------------------------------------ BiCGSTAB */
+typedef void (*spmv_fn)(int64_t, const int64_t *, const int32_t *, const double *, const double *, double *);
+typedef void (*apply_fn)(int64_t, int32_t, const int64_t *, const int64_t *, const int32_t *, const double *,
+                         const double *, const double *, const double *, double *);
+
+/* Alg. 1 with K1 = I, K2 = M; bs = unknowns per row (3: BSR3, 1: CSR). */
+static int bicgstab_impl(int64_t n, int bs, spmv_fn orc_spmv_, apply_fn orc_apply_, const int64_t *rp_r,
+                         const int32_t *ci_r, const double *v_r, int32_t n_sub, const int64_t *sub_ptr,
+                         const int64_t *rp_d, const int32_t *ci_d, const double *lu, const double *dinv,
+                         const double *uunit, const double *b, double *x, double tol, int32_t max_iter,
+                         double *resid_hist, double *out);
+
 int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const double *v_r,
                  int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp_d, const int32_t *ci_d,
                  const double *lu, const double *dinv, const double *uunit, const double *b,
                  double *x, double tol, int32_t max_iter, double *resid_hist, double *out) {
-    int64_t m = 3 * n;
+    return bicgstab_impl(n, 3, orc_spmv, orc_apply, rp_r, ci_r, v_r, n_sub, sub_ptr, rp_d, ci_d, lu, dinv, uunit,
+                         b, x, tol, max_iter, resid_hist, out);
+}
+
+static int bicgstab_impl(int64_t n, int bs, spmv_fn orc_spmv_, apply_fn orc_apply_, const int64_t *rp_r,
+                         const int32_t *ci_r, const double *v_r, int32_t n_sub, const int64_t *sub_ptr,
+                         const int64_t *rp_d, const int32_t *ci_d, const double *lu, const double *dinv,
+                         const double *uunit, const double *b, double *x, double tol, int32_t max_iter,
+                         double *resid_hist, double *out) {
+    int64_t m = bs * n;
     size_t bytes = (size_t)m * sizeof(double);
     double *r = malloc(bytes), *rh = malloc(bytes), *p = calloc((size_t)m, sizeof(double));
     double *v = calloc((size_t)m, sizeof(double)), *ph = malloc(bytes), *s = malloc(bytes);
@@ -369,7 +389,7 @@ int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const doub
     double iters = (double)max_iter;
 
     /* r = b - A x0 */
-    orc_spmv(n, rp_r, ci_r, v_r, x, t);
+    orc_spmv_(n, rp_r, ci_r, v_r, x, t);
 #pragma omp parallel for
     for (int64_t i = 0; i < m; i++) r[i] = b[i] - t[i];
     memcpy(rh, r, bytes);
@@ -395,9 +415,9 @@ int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const doub
 #pragma omp parallel for
             for (int64_t i = 0; i < m; i++) p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
         }
-        orc_apply(n, n_sub, sub_ptr, rp_d, ci_d, lu, dinv, uunit, p, ph);
+        orc_apply_(n, n_sub, sub_ptr, rp_d, ci_d, lu, dinv, uunit, p, ph);
         n_app++;
-        orc_spmv(n, rp_r, ci_r, v_r, ph, v);
+        orc_spmv_(n, rp_r, ci_r, v_r, ph, v);
         double sigma = orc_dot(m, rh, v);
         if (fabs(sigma) < 1e-30) { status = 1; iters = k - 1; break; }
         alpha = rho / sigma;
@@ -414,9 +434,9 @@ int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const doub
             rel = ns / n0;
             break;
         }
-        orc_apply(n, n_sub, sub_ptr, rp_d, ci_d, lu, dinv, uunit, s, sh);
+        orc_apply_(n, n_sub, sub_ptr, rp_d, ci_d, lu, dinv, uunit, s, sh);
         n_app++;
-        orc_spmv(n, rp_r, ci_r, v_r, sh, t);
+        orc_spmv_(n, rp_r, ci_r, v_r, sh, t);
         double tau = orc_dot(m, t, t);
         if (tau < 1e-30) { status = 1; iters = k - 0.5; break; }
         omega = orc_dot(m, t, s) / tau;
@@ -438,7 +458,7 @@ int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const doub
     }
 done:;
     /* true residual ||b - A x|| / ||b|| */
-    orc_spmv(n, rp_r, ci_r, v_r, x, t);
+    orc_spmv_(n, rp_r, ci_r, v_r, x, t);
 #pragma omp parallel for
     for (int64_t i = 0; i < m; i++) t[i] = b[i] - t[i];
     double nb = sqrt(orc_dot(m, b, b));
@@ -455,4 +475,140 @@ done:;
     }
     free(r); free(rh); free(p); free(v); free(ph); free(s); free(sh); free(t);
     return status;
+}
+
+/* ======================================================================
+ * Scalar CSR path (the paper's CSR half: P:110, P:279-305,
+ * Alg. 7 P:680-711 in its scalar form). Same steps and arithmetic order as
+ * the block functions above with 1x1 blocks: L_ik = w_ik * dinv_k,
+ * w_ij = fma(-l_ik, u_kj, w_ij), dinv_i = 1 / u_ii (R15 floor on |u_ii|),
+ * uunit_ij = dinv_i * u_ij. The pattern-only steps (labels, permutation,
+ * subdomain_ptr, levels) are shared with the block path.
+ * ==================================================================== */
+
+void orc_s_reorder(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   const int32_t *new_to_old, const int32_t *old_to_new, int64_t *rp_out,
+                   int32_t *ci_out, double *v_out) {
+    rp_out[0] = 0;
+    for (int64_t i = 0; i < n; i++) rp_out[i + 1] = rp_out[i] + (rp[new_to_old[i] + 1] - rp[new_to_old[i]]);
+    int64_t nn = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int64_t m = new_to_old[i];
+        for (int64_t j = rp[m]; j < rp[m + 1]; j++) {
+            ci_out[nn] = old_to_new[ci[j]];
+            v_out[nn] = v[j];
+            nn++;
+        }
+        /* "Sort colidx[rowptr[i] .. rowptr[i+1]]": insertion sort */
+        for (int64_t a = rp_out[i] + 1; a < rp_out[i + 1]; a++) {
+            int32_t c = ci_out[a];
+            double x = v_out[a];
+            int64_t b = a - 1;
+            while (b >= rp_out[i] && ci_out[b] > c) {
+                ci_out[b + 1] = ci_out[b];
+                v_out[b + 1] = v_out[b];
+                b--;
+            }
+            ci_out[b + 1] = c;
+            v_out[b + 1] = x;
+        }
+    }
+}
+
+int64_t orc_s_drop(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   const int32_t *label_new, int64_t *rp_out, int32_t *ci_out, double *v_out) {
+    int64_t kept = 0;
+    if (rp_out) rp_out[0] = 0;
+    for (int64_t r = 0; r < n; r++) {
+        for (int64_t p = rp[r]; p < rp[r + 1]; p++) {
+            if (label_new[r] == label_new[ci[p]]) {
+                if (rp_out) {
+                    ci_out[kept] = ci[p];
+                    v_out[kept] = v[p];
+                }
+                kept++;
+            }
+        }
+        if (rp_out) rp_out[r + 1] = kept;
+    }
+    return kept;
+}
+
+int orc_s_ilu0(int64_t n, const int64_t *rp, const int32_t *ci, const double *a,
+               double pivot_floor, double *lu, double *dinv, int64_t *bad_row) {
+    memcpy(lu, a, (size_t)rp[n] * sizeof(double));
+    for (int64_t i = 0; i < n; i++) {
+        int64_t pd = -1;
+        for (int64_t p = rp[i]; p < rp[i + 1]; p++)
+            if (ci[p] == i) pd = p;
+        if (pd < 0) {
+            if (bad_row) *bad_row = i;
+            return 1;
+        }
+        for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < i; p++) {
+            int64_t k = ci[p];
+            lu[p] = lu[p] * dinv[k];                       /* l_ik = w_ik / u_kk */
+            for (int64_t q = p + 1; q < rp[i + 1]; q++) {
+                int64_t j = ci[q];
+                for (int64_t r = rp[k]; r < rp[k + 1]; r++) {
+                    if (ci[r] == j && j > k) {
+                        lu[q] = fma(-lu[p], lu[r], lu[q]);  /* w_ij -= l_ik u_kj */
+                        break;
+                    }
+                }
+            }
+        }
+        if (!(fabs(lu[pd]) >= pivot_floor)) {
+            if (bad_row) *bad_row = i;
+            return 2;
+        }
+        dinv[i] = 1.0 / lu[pd];
+    }
+    return 0;
+}
+
+void orc_s_ildu0(int64_t n, const int64_t *rp, const int32_t *ci, const double *lu,
+                 const double *dinv, double *uunit) {
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t p = rp[i]; p < rp[i + 1]; p++)
+            if (ci[p] > i) uunit[p] = dinv[i] * lu[p];
+}
+
+void orc_s_apply(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp,
+                 const int32_t *ci, const double *lu, const double *dinv, const double *uunit,
+                 const double *r, double *z) {
+    (void)n;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t s = 0; s < n_sub; s++) {
+        int64_t a = sub_ptr[s], e = sub_ptr[s + 1];
+        for (int64_t i = a; i < e; i++) {
+            double acc = r[i];
+            for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < i; p++) acc = fma(-lu[p], z[ci[p]], acc);
+            z[i] = acc;
+        }
+        for (int64_t i = e - 1; i >= a; i--) {
+            double acc = dinv[i] * z[i];
+            for (int64_t p = rp[i]; p < rp[i + 1]; p++)
+                if (ci[p] > i) acc = fma(-uunit[p], z[ci[p]], acc);
+            z[i] = acc;
+        }
+    }
+}
+
+void orc_s_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                const double *x, double *y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        double acc = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; p++) acc = fma(v[p], x[ci[p]], acc);
+        y[i] = acc;
+    }
+}
+
+int orc_s_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const double *v_r,
+                   int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp_d, const int32_t *ci_d,
+                   const double *lu, const double *dinv, const double *uunit, const double *b,
+                   double *x, double tol, int32_t max_iter, double *resid_hist, double *out) {
+    return bicgstab_impl(n, 1, orc_s_spmv, orc_s_apply, rp_r, ci_r, v_r, n_sub, sub_ptr, rp_d, ci_d, lu, dinv,
+                         uunit, b, x, tol, max_iter, resid_hist, out);
 }

@@ -112,6 +112,31 @@ int orc_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const doub
                  const double *lu, const double *dinv, const double *uunit, const double *b,
                  double *x, double tol, int32_t max_iter, double *resid_hist, double *out);
 
+/* ---- Scalar CSR path (the paper's CSR half): the
+ * same steps with 1x1 blocks -- vals double[nnz], vectors double[n]. The
+ * pattern-only functions above (labels, permutation, subdomain_ptr, levels)
+ * serve both paths. Arithmetic: DESIGN.md section 4 with 1x1 blocks
+ * (l_ik = w_ik * dinv_k; w_ij = fma(-l_ik, u_kj, w_ij); dinv_i = 1/u_ii;
+ * uunit_ij = dinv_i * u_ij; sweeps and SpMV as single FMA chains). */
+void orc_s_reorder(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   const int32_t *new_to_old, const int32_t *old_to_new, int64_t *rp_out,
+                   int32_t *ci_out, double *v_out);
+int64_t orc_s_drop(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                   const int32_t *label_new, int64_t *rp_out, int32_t *ci_out, double *v_out);
+int orc_s_ilu0(int64_t n, const int64_t *rp, const int32_t *ci, const double *a,
+               double pivot_floor, double *lu, double *dinv, int64_t *bad_row);
+void orc_s_ildu0(int64_t n, const int64_t *rp, const int32_t *ci, const double *lu,
+                 const double *dinv, double *uunit);
+void orc_s_apply(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp,
+                 const int32_t *ci, const double *lu, const double *dinv, const double *uunit,
+                 const double *r, double *z);
+void orc_s_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                const double *x, double *y);
+int orc_s_bicgstab(int64_t n, const int64_t *rp_r, const int32_t *ci_r, const double *v_r,
+                   int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp_d, const int32_t *ci_d,
+                   const double *lu, const double *dinv, const double *uunit, const double *b,
+                   double *x, double tol, int32_t max_iter, double *resid_hist, double *out);
+
 #ifdef __cplusplus
 }
 #endif
