@@ -136,6 +136,17 @@ typedef struct {
 #define DD_COMM_NCCL 0
 #define DD_COMM_LOCAL 1
 
+/* Borrowed scalar CSR matrix (the paper's CSR half, P:110,
+ * P:279-305): the same pipeline with 1x1 blocks. vals[nnz]; vectors passed
+ * to the compute calls then hold n_local doubles (one unknown per row). */
+typedef struct {
+    int64_t n_rows;
+    int64_t nnz;
+    const int64_t *row_ptr;  /* [n_rows + 1]                               */
+    const int32_t *col_idx;  /* [nnz], ascending, unique per row, diagonal present */
+    const double *vals;      /* [nnz]                                      */
+} dd_csr;
+
 /* Partitioners used when dd_opts.grid == NULL (P = subdomain_rows):
  * contiguous chunks of P rows (R26), or graph growing (METIS stand-in, P:236,
  * S:145-153, R35): parts of exactly P rows (last smaller), each grown
@@ -212,6 +223,11 @@ dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original or
                            int32_t *new_to_old /*[N]*/);
 /* which: 0 = L (hmapL), 1 = U (hmapU); local rows, reordered order. */
 dd_status dd_get_levels(const dd_ctx *ctx, int32_t which, int32_t *hmap);
+
+/* Scalar CSR variant of dd_setup: identical steps, errors and
+ * options (enable_refactor is not supported: DD_E_INVALID_ARG). Every other
+ * call works on the returned context; vectors carry one double per row. */
+dd_status dd_setup_csr(const dd_csr *A, const dd_opts *o, dd_ctx **out);
 
 /* Alg. 5 on the device: the paper's fixpoint
  * level marking, one CTA per subdomain, over this rank's L and U factor

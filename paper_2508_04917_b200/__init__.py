@@ -29,7 +29,7 @@ DD_COMM_NCCL, DD_COMM_LOCAL = 0, 1
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",
           "DD_E_SINGULAR_PIVOT", "DD_E_SUBDOMAIN_TOO_LARGE", "DD_E_GRID_NOT_DIVISIBLE", "DD_E_CUDA",
           "DD_E_NCCL", "DD_E_OOM", "DD_E_BREAKDOWN", "DD_E_MAXITER", "DD_E_NO_DEVICE"]
-EXPORTS = ["dd_setup", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
+EXPORTS = ["dd_setup", "dd_setup_csr", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
            "dd_get_levels", "dd_levels_device", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
            "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_last_error"]
@@ -80,7 +80,7 @@ def lib():
         L = C.CDLL(LIB_PATH)
         P, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
         sig = {
-            "dd_setup": [P, P, P], "dd_destroy": [P], "dd_local_range": [P, P, P],
+            "dd_setup": [P, P, P], "dd_setup_csr": [P, P, P], "dd_destroy": [P], "dd_local_range": [P, P, P],
             "dd_apply": [P, P, P, P], "dd_apply_variant": [P, i32, P, P, P], "dd_spmv": [P, P, P, P],
             "dd_bicgstab": [P, P, P, d, i32, P, P, P], "dd_solve_host": [P, P, P, d, i32, P, P],
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
@@ -135,9 +135,10 @@ def dd_nccl_unique_id() -> bytes:
 class Context:
     """A dd_ctx*. Build with dd_setup(...)."""
 
-    def __init__(self, handle, N, keep):
+    def __init__(self, handle, N, keep, bs=3):
         self.h = handle
         self.N = N
+        self.bs = bs  # unknowns per row: 3 (BSR3) or 1 (scalar CSR)
         self._keep = keep
         first, nl = C.c_int64(), C.c_int64()
         lib().dd_local_range(self.h, C.byref(first), C.byref(nl))
@@ -154,15 +155,15 @@ class Context:
 
     # --- compute
     def apply(self, r, z, variant=DD_LEVELSET, stream=None):
-        m = 3 * self.n_local
+        m = self.bs * self.n_local
         _check(lib().dd_apply_variant(self.h, variant, _dev_vec(r, m, "r"), _dev_vec(z, m, "z"), _stream(stream)))
 
     def spmv(self, x, y, stream=None):
-        m = 3 * self.n_local
+        m = self.bs * self.n_local
         _check(lib().dd_spmv(self.h, _dev_vec(x, m, "x"), _dev_vec(y, m, "y"), _stream(stream)))
 
     def bicgstab(self, b, x, tol=1e-8, max_iter=1000, hist=False, stream=None):
-        m = 3 * self.n_local
+        m = self.bs * self.n_local
         rep = Report()
         h = np.zeros(2 * max_iter + 1) if hist else None
         st = lib().dd_bicgstab(self.h, _dev_vec(b, m, "b"), _dev_vec(x, m, "x"), tol, max_iter, _ptr(h),
@@ -186,10 +187,10 @@ class Context:
 
     def permute(self, v_orig_host: np.ndarray, v_reord_dev, stream=None):
         _check(lib().dd_permute(self.h, _ptr(np.ascontiguousarray(v_orig_host, np.float64)),
-                                _dev_vec(v_reord_dev, 3 * self.n_local, "v"), _stream(stream)))
+                                _dev_vec(v_reord_dev, self.bs * self.n_local, "v"), _stream(stream)))
 
     def unpermute(self, v_reord_dev, v_orig_host: np.ndarray, stream=None):
-        _check(lib().dd_unpermute(self.h, _dev_vec(v_reord_dev, 3 * self.n_local, "v"), _ptr(v_orig_host),
+        _check(lib().dd_unpermute(self.h, _dev_vec(v_reord_dev, self.bs * self.n_local, "v"), _ptr(v_orig_host),
                                   _stream(stream)))
 
     def refactor(self, vals, stream=None):
@@ -225,9 +226,10 @@ class Context:
         nL, nU = C.c_int64(), C.c_int64()
         _check(lib().dd_get_factors(self.h, C.byref(nL), C.byref(nU), *([None] * 7)))
         n = self.n_local
-        Lrp = np.empty(n + 1, np.int64); Lci = np.empty(nL.value, np.int32); Lv = np.empty(9 * nL.value)
-        Urp = np.empty(n + 1, np.int64); Uci = np.empty(nU.value, np.int32); Uv = np.empty(9 * nU.value)
-        D = np.empty(9 * n)
+        b2 = self.bs * self.bs
+        Lrp = np.empty(n + 1, np.int64); Lci = np.empty(nL.value, np.int32); Lv = np.empty(b2 * nL.value)
+        Urp = np.empty(n + 1, np.int64); Uci = np.empty(nU.value, np.int32); Uv = np.empty(b2 * nU.value)
+        D = np.empty(b2 * n)
         _check(lib().dd_get_factors(self.h, None, None, _ptr(Lrp), _ptr(Lci), _ptr(Lv), _ptr(Urp), _ptr(Uci),
                                     _ptr(Uv), _ptr(D)))
         return dict(Lrp=Lrp, Lci=Lci, Lv=Lv, Urp=Urp, Uci=Uci, Uv=Uv, Dinv=D)
@@ -275,10 +277,11 @@ class Context:
 
 def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=DD_LEVELSET, device=0, rank=0,
              world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0,
-             enable_refactor=False, partitioner="chunks", comm="nccl") -> Context:
+             enable_refactor=False, partitioner="chunks", comm="nccl", csr=False) -> Context:
     """world > 1: comm="nccl" (one process per GPU, nccl_id from dd_nccl_unique_id)
     or comm="local" (ranks are contexts of this process, each created and driven
-    from its own thread; nccl_id is any 128-byte key the ranks share)."""
+    from its own thread; nccl_id is any 128-byte key the ranks share).
+    csr=True: a scalar CSR matrix (vals[nnz]) through dd_setup_csr."""
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
@@ -301,8 +304,13 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     o.partitioner = {"chunks": DD_PART_CHUNKS, "bfs": DD_PART_BFS}[partitioner]
     o.comm = {"nccl": DD_COMM_NCCL, "local": DD_COMM_LOCAL}[comm]
     h = C.c_void_p()
-    _check(lib().dd_setup(C.byref(A), C.byref(o), C.byref(h)))
-    return Context(h, n, keep=(g, idbuf))
+    _check((lib().dd_setup_csr if csr else lib().dd_setup)(C.byref(A), C.byref(o), C.byref(h)))
+    return Context(h, n, keep=(g, idbuf), bs=1 if csr else 3)
+
+
+def dd_setup_csr(row_ptr, col_idx, vals, **kw) -> Context:
+    """Scalar CSR path; same options as dd_setup."""
+    return dd_setup(row_ptr, col_idx, vals, csr=True, **kw)
 
 
 # C-ABI-named thin wrappers

@@ -46,7 +46,7 @@ using namespace ddi;
 namespace {
 
 struct Workspace {
-    int64_t m = 0;  // 3 * n_local
+    int64_t m = 0;  // bs * n_local
     double *r = nullptr, *rh = nullptr, *p = nullptr, *v = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr,
            *t = nullptr, *bd = nullptr, *xd = nullptr;
     double *sc = nullptr;        // device scalars [S_COUNT]
@@ -61,8 +61,8 @@ struct Workspace {
     int64_t hist_cap = 0;
     double *h_tol = nullptr;     // pinned scalar (tolerance upload)
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    double *xg = nullptr;        // ghost rows of the SpMV input [3 * n_ghost]
-    double *sendbuf = nullptr;   // [3 * total send rows]
+    double *xg = nullptr;        // ghost rows of the SpMV input [bs * n_ghost]
+    double *sendbuf = nullptr;   // [bs * total send rows]
     int32_t *d_send_idx = nullptr;
     std::vector<int64_t> send_off;  // [world + 1]
     // DD_COMM_LOCAL: "my send data is ready" / "I have copied my peers' data"
@@ -289,7 +289,8 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
             sp[s + 1] = sp[s] + 32 * K;
         }
         std::vector<int32_t> cols(S.n_slots, -1);
-        std::vector<double> vals(9 * S.n_slots, 0.0);
+        const int b2 = ctx->bs * ctx->bs;
+        std::vector<double> vals(b2 * S.n_slots, 0.0);
 #pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < S.n_slices; ++s) {
             for (int lane = 0; lane < 32; ++lane) {
@@ -298,13 +299,13 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
                 for (int64_t k = 0; k < ctx->Arp[li + 1] - ctx->Arp[li]; ++k) {
                     const int64_t p = ctx->Arp[li] + k;
                     cols[sp[s] + 32 * k + lane] = ctx->Aci[p];
-                    for (int v = 0; v < 9; ++v) vals[9 * (sp[s] + 32 * k) + 32 * v + lane] = ctx->Av[9 * p + v];
+                    for (int v = 0; v < b2; ++v) vals[b2 * (sp[s] + 32 * k) + 32 * v + lane] = ctx->Av[b2 * p + v];
                 }
             }
         }
         TRY(dmalloc(&S.slot_ptr, sp.size()));
         TRY(dmalloc(&S.cols, std::max<int64_t>(1, S.n_slots)));
-        TRY(dmalloc(&S.vals, std::max<int64_t>(1, 9 * S.n_slots)));
+        TRY(dmalloc(&S.vals, std::max<int64_t>(1, b2 * S.n_slots)));
         CK(cudaMemcpy(S.slot_ptr, sp.data(), sp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
         if (S.n_slots) {
             CK(cudaMemcpy(S.cols, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -319,12 +320,12 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
         TRY(dmalloc(&d, std::max<int64_t>(1, nl)));
         if (nl) CK(cudaMemcpy(d, idx.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice));
         ctx->d_new_to_old_local = d;
-        TRY(dmalloc(&ctx->d_stage, 3 * ctx->N + 2));
+        TRY(dmalloc(&ctx->d_stage, ctx->bs * ctx->N + 2));
     }
     // BiCGSTAB workspace
     auto *ws = new Workspace();
     ctx->dev_ws = ws;
-    ws->m = 3 * nl;
+    ws->m = ctx->bs * nl;
     const size_t mm = (size_t)ws->m + 2;  // +2: 16-byte slack past the end (dd.h)
     for (double **q : {&ws->r, &ws->rh, &ws->p, &ws->v, &ws->ph, &ws->s, &ws->sh, &ws->t, &ws->bd, &ws->xd})
         TRY(dmalloc(q, mm));
@@ -345,14 +346,14 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
     // halo buffers
     const int64_t ng = (int64_t)ctx->ghost_rows.size();
-    TRY(dmalloc(&ws->xg, std::max<int64_t>(1, 3 * ng)));
+    TRY(dmalloc(&ws->xg, std::max<int64_t>(1, ctx->bs * ng)));
     ws->send_off.assign(ctx->world + 1, 0);
     std::vector<int32_t> sidx;
     for (int q = 0; q < ctx->world; ++q) {
         if (q < (int)ctx->send_rows.size()) sidx.insert(sidx.end(), ctx->send_rows[q].begin(), ctx->send_rows[q].end());
         ws->send_off[q + 1] = (int64_t)sidx.size();
     }
-    TRY(dmalloc(&ws->sendbuf, std::max<size_t>(1, 3 * sidx.size())));
+    TRY(dmalloc(&ws->sendbuf, std::max<size_t>(1, ctx->bs * sidx.size())));
     TRY(dmalloc(&ws->d_send_idx, std::max<size_t>(1, sidx.size())));
     if (!sidx.empty())
         CK(cudaMemcpy(ws->d_send_idx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -404,7 +405,7 @@ dd_status local_halo(dd_ctx *c, cudaStream_t st) {
         if (!rn) continue;
         Workspace *pw = ws_of(G->members[q]);
         CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
-        CK(cudaMemcpyAsync(ws->xg + 3 * ro, pw->sendbuf + 3 * pw->send_off[c->rank], 3 * rn * sizeof(double),
+        CK(cudaMemcpyAsync(ws->xg + c->bs * ro, pw->sendbuf + c->bs * pw->send_off[c->rank], c->bs * rn * sizeof(double),
                            cudaMemcpyDefault, st));
     }
     CK(cudaEventRecord(ws->xev_done, st));
@@ -440,8 +441,8 @@ dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
         if (q == c->rank) continue;
         const int64_t so = ws->send_off[q], sn = ws->send_off[q + 1] - so;
         const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
-        if (sn) NK(ncclSend(ws->sendbuf + 3 * so, 3 * sn, ncclDouble, q, comm, st));
-        if (rn) NK(ncclRecv(ws->xg + 3 * ro, 3 * rn, ncclDouble, q, comm, st));
+        if (sn) NK(ncclSend(ws->sendbuf + c->bs * so, c->bs * sn, ncclDouble, q, comm, st));
+        if (rn) NK(ncclRecv(ws->xg + c->bs * ro, c->bs * rn, ncclDouble, q, comm, st));
     }
     NK(ncclGroupEnd());
     return DD_OK;
@@ -568,7 +569,22 @@ dd_status dd_nccl_unique_id(void *out128) {
     return DD_OK;
 }
 
-dd_status dd_setup(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out) {
+static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out, int bs);
+
+dd_status dd_setup(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out) { return setup_common(A, o, out, 3); }
+
+dd_status dd_setup_csr(const dd_csr *A, const dd_opts *o, dd_ctx **out) {
+    if (!A) {
+        if (out) *out = nullptr;
+        set_error("dd_setup_csr: NULL argument");
+        return DD_E_INVALID_ARG;
+    }
+    // same layout with 1x1 blocks: n_block_rows = n_rows, nnzb = nnz
+    const dd_bsr3 B{A->n_rows, A->nnz, A->row_ptr, A->col_idx, A->vals};
+    return setup_common(&B, o, out, 1);
+}
+
+static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out, int bs) {
     if (!out) {
         set_error("dd_setup: out is NULL");
         return DD_E_INVALID_ARG;
@@ -579,6 +595,7 @@ dd_status dd_setup(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out) {
         return DD_E_INVALID_ARG;
     }
     auto *ctx = new dd_ctx();
+    ctx->bs = bs;
     ctx->device = o->device;
     ctx->rank = o->rank;
     ctx->world = std::max(1, o->world);
@@ -912,7 +929,7 @@ dd_status dd_refactor(dd_ctx *c, const double *vals, int32_t on_device, void *st
 dd_status dd_permute(dd_ctx *c, const double *v_orig_host, double *v_reord_dev, void *stream) {
     if (!usable(c) || !v_orig_host || !v_reord_dev) return DD_E_INVALID_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    CK(cudaMemcpyAsync(c->d_stage, v_orig_host, 3 * c->N * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_stage, v_orig_host, c->bs * c->N * sizeof(double), cudaMemcpyHostToDevice, st));
     ddk::launch_gather3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), c->d_stage,
                         v_reord_dev, st);
     CK(cudaGetLastError());
@@ -925,15 +942,16 @@ dd_status dd_unpermute(dd_ctx *c, const double *v_reord_dev, double *v_orig_host
     if (c->world <= 1) {
         ddk::launch_scatter3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), v_reord_dev,
                              c->d_stage, st);
-        CK(cudaMemcpyAsync(v_orig_host, c->d_stage, 3 * c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(v_orig_host, c->d_stage, c->bs * c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     } else {
-        std::vector<double> tmp(3 * c->n_local);
+        const int bs = c->bs;
+        std::vector<double> tmp(bs * c->n_local);
         CK(cudaMemcpyAsync(tmp.data(), v_reord_dev, tmp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         for (int64_t li = 0; li < c->n_local; ++li) {
             const int64_t g = c->new_to_old[c->row_first + li];
-            for (int q = 0; q < 3; ++q) v_orig_host[3 * g + q] = tmp[3 * li + q];
+            for (int q = 0; q < bs; ++q) v_orig_host[bs * g + q] = tmp[bs * li + q];
         }
     }
     return DD_OK;
@@ -1068,10 +1086,12 @@ dd_status dd_stats(const dd_ctx *c, int64_t *stats, double *setup_ms) {
         stats[7] = slab_l;
         stats[8] = slab_s;
         stats[9] = c->spmv_bytes;
-        // canonical bytes: 72(nL+nU+n) + 4(nL+nU) + 4*2(n+1) + 48 n
-        stats[10] = 72 * (nL + nU + nl) + 4 * (nL + nU) + 8 * (nl + 1) + 48 * nl;
+        // canonical bytes: 8 b2 (nL+nU+n) + 4(nL+nU) + 4*2(n+1) + 16 bs n
+        // (BSR3: 72(nL+nU+n) + 4(nL+nU) + 8(n+1) + 48n)
+        const int64_t b2 = (int64_t)c->bs * c->bs;
+        stats[10] = 8 * b2 * (nL + nU + nl) + 4 * (nL + nU) + 8 * (nl + 1) + 16 * c->bs * nl;
         const int64_t nnzA_loc = c->Arp.empty() ? 0 : c->Arp.back();
-        stats[11] = 76 * nnzA_loc + 4 * (nl + 1) + 48 * nl;
+        stats[11] = (8 * b2 + 4) * nnzA_loc + 4 * (nl + 1) + 16 * c->bs * nl;
         stats[12] = nl;
         stats[13] = (int64_t)c->ghost_rows.size();
         stats[14] = c->n_launches;

@@ -1,6 +1,6 @@
 // apply.cu -- fused per-subdomain ILDU0 apply z = U_unit^-1 D^-1 L^-1 r.
 //
-// One CTA owns one subdomain at a time; the subdomain vector (24*P bytes)
+// One CTA owns one subdomain at a time; the subdomain vector (8*bs*P bytes)
 // lives in shared memory for the whole L -> D -> U sequence (sec. 4.4
 // P:715-725; Alg. 6 P:582-615 with unit L per sec. 4.3). The
 // factor slab is level-ordered and read exactly once.
@@ -82,8 +82,8 @@ __device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, ui
 // all are in flight before the first FMA; the only dependent step is the
 // gather of vec[3j..3j+2] through the descriptor's column ids.
 template <bool SPIN, class Rd>
-__device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
-                                               double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+__device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
+                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
     if (t >= (int)w) return;
     const bool upper = (h.flags & ddi::REC_UPPER) != 0;
@@ -208,6 +208,90 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
     }
 }
 
+// Scalar CSR rows: the same record walk with 1x1 blocks --
+// one value plane per k, one Dinv plane, one FMA chain per row
+// (lower: acc = r_i, fma(-l_ij, z_j, acc); upper: acc = dinv_i * z_i,
+// fma(-u_ij, x_j, acc); blocks ascending).
+template <bool SPIN, class Rd>
+__device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
+                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+    const uint32_t w = h.w, K = h.K;
+    if (t >= (int)w) return;
+    const bool upper = (h.flags & ddi::REC_UPPER) != 0;
+    const uint32_t off_desc = ddi::rec_off_desc(K);
+    const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
+    const uint32_t off_val = h.off_val;
+    if (K <= 3) {
+        const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
+        const uint32_t i = d.x & 0xffffu;
+        const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
+        const uint32_t cnt[3] = {K > 0 ? (c8.x & 0xffffu) : 0u, K > 1 ? (c8.x >> 16) : 0u, K > 2 ? (c8.y & 0xffffu) : 0u};
+        double b[3];
+        uint32_t pre = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if ((uint32_t)t < cnt[k]) b[k] = rd.template ld<double>(off_val + 8u * (pre + t));
+            pre += cnt[k];
+        }
+        double a;
+        if (upper) {
+            const double D = rd.template ld<double>(off_dinv + 8u * t);
+            if (SPIN) spin_until(flags, i, ep - 1);
+            a = D * vec[i];
+        } else {
+            a = vec[i];
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if ((uint32_t)t < cnt[k]) {
+                const uint32_t j = col[k];
+                if (SPIN) spin_until(flags, j, ep);
+                a = __fma_rn(-b[k], vec[j], a);
+            }
+        }
+        vec[i] = a;
+        if (SPIN) {
+            __threadfence_block();
+            *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
+        }
+        return;
+    }
+    const uint32_t dw = ddi::rec_dw(K);
+    const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * t);
+    double a;
+    if (upper) {
+        const double D = rd.template ld<double>(off_dinv + 8u * t);
+        if (SPIN) spin_until(flags, i, ep - 1);
+        a = D * vec[i];
+    } else {
+        a = vec[i];
+    }
+    uint32_t pre = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
+        if ((uint32_t)t >= ck) break;
+        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k));
+        const double b = rd.template ld<double>(off_val + 8u * (pre + t));
+        if (SPIN) spin_until(flags, j, ep);
+        a = __fma_rn(-b, vec[j], a);
+        pre += ck;
+    }
+    vec[i] = a;
+    if (SPIN) {
+        __threadfence_block();
+        *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
+    }
+}
+
+template <int BS, bool SPIN, class Rd>
+__device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
+                                               double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+    if constexpr (BS == 3)
+        process_record3<SPIN>(rd, h, c8, t, vec, flags, ep);
+    else
+        process_record1<SPIN>(rd, h, c8, t, vec, flags, ep);
+}
+
 __device__ __forceinline__ RecHdr hdr_from(uint4 q) {
     RecHdr h;
     h.w = (uint16_t)(q.x & 0xffffu);
@@ -227,6 +311,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // Ablation: level-set sweep reading the records straight from global memory;
 // only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
 // keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
+template <int BS>
 __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
@@ -245,8 +330,8 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
             pf = min(sz, pf_bytes);
             prefetch_l2(base, pf);
         }
-        const int nd = 3 * si.nrows;
-        const double *rs = r + 3 * (int64_t)si.row0;
+        const int nd = BS * si.nrows;
+        const double *rs = r + BS * (int64_t)si.row0;
         for (int q = t; q < nd; q += TC) vec[q] = __ldg(rs + q);
         __syncthreads();
         uint32_t ro = 0;
@@ -263,13 +348,13 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
             // L level 0 carries no blocks (z_i = r_i in place): no work, no barrier
             const bool skip = !(h.flags & ddi::REC_UPPER) && h.K == 0 && !last;
             if (!skip) {
-                process_record<false>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
+                process_record<BS, false>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
                 __syncthreads();
             }
             ro += h.bytes;
             if (last) break;
         }
-        double *zs = z + 3 * (int64_t)si.row0;
+        double *zs = z + BS * (int64_t)si.row0;
         for (int q = t; q < nd; q += TC) zs[q] = vec[q];
     }
 }
@@ -284,7 +369,7 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
 //   barriers count NW arrivals).
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
 //   the streaming ceiling of the ring.
-template <uint32_t RING, uint32_t CH, bool SPIN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN>
 __global__ void __launch_bounds__(TC + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
@@ -310,7 +395,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
         fence_mbar_init();
     }
     if (SPIN) {
-        for (int q = tid; q < vec_bytes / 24; q += TC + 32) flags[q] = 0;
+        for (int q = tid; q < vec_bytes / (8 * BS); q += TC + 32) flags[q] = 0;
     }
     __syncthreads();
 
@@ -321,8 +406,8 @@ __global__ void __launch_bounds__(TC + 32, 1)
             uint32_t g = 0;
             for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
                 const SubInfo si = info[s];
-                const int64_t rlo = (24 * (int64_t)si.row0) & ~(int64_t)15;
-                const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
+                const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
+                const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
                 const uint32_t rb = (uint32_t)(rhi - rlo);
                 // phase 0: the whole stream; 1: the L section; 2: the D+U section
                 const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
@@ -371,15 +456,15 @@ __global__ void __launch_bounds__(TC + 32, 1)
     };
     for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
         const SubInfo si = info[s];
-        const int64_t rlo = (24 * (int64_t)si.row0) & ~(int64_t)15;
-        const int64_t rhi = (24 * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
+        const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
+        const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
         const uint32_t rb = (uint32_t)(rhi - rlo);
-        const uint32_t shift = (uint32_t)(24 * (int64_t)si.row0 - rlo);
+        const uint32_t shift = (uint32_t)(8 * BS * (int64_t)si.row0 - rlo);
         const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
         const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
         const uint32_t total = rb + (sec_hi - sec_lo);
         const uint32_t nch = (total + CH - 1) / CH;
-        const uint32_t nd = 3u * si.nrows;
+        const uint32_t nd = (uint32_t)BS * si.nrows;
         const uint32_t abs0 = gbase * CH;
         // ---- r slice: ring -> vec, chunk by chunk
         const uint32_t nrc = (rb + CH - 1) / CH;
@@ -416,9 +501,9 @@ __global__ void __launch_bounds__(TC + 32, 1)
             const uint32_t ep_set = upper ? ep : ep - 1;
             if (mode == 1 || skip) {
             } else if (pos + h.bytes <= RING) {
-                process_record<SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
             } else {
-                process_record<SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
             }
             ro += h.bytes;
             if (SPIN) {
@@ -436,7 +521,7 @@ __global__ void __launch_bounds__(TC + 32, 1)
             }
             release_to(gbase + ro / CH);
         }
-        double *zs = z + 3 * (int64_t)si.row0;
+        double *zs = z + BS * (int64_t)si.row0;
         for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[q];
         gbase += nch;
     }
@@ -445,29 +530,37 @@ __global__ void __launch_bounds__(TC + 32, 1)
 // ------------------------------------------------------------ host side
 using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int);
 
-template <uint32_t RING, uint32_t CH, bool SPIN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN>
 static RingFn ring_fn() {
-    return k_apply_ring<RING, CH, SPIN>;
+    return k_apply_ring<BS, RING, CH, SPIN>;
 }
 
-static RingFn pick_ring(int ring, bool spin) {
+template <int BS>
+static RingFn pick_ring_bs(int ring, bool spin) {
     if (!spin) {
         switch (ring) {
-            case 131072: return ring_fn<131072, 16384, false>();
-            case 65536: return ring_fn<65536, 8192, false>();
-            case 32768: return ring_fn<32768, 4096, false>();
-            case 16384: return ring_fn<16384, 2048, false>();
+            case 131072: return ring_fn<BS, 131072, 16384, false>();
+            case 65536: return ring_fn<BS, 65536, 8192, false>();
+            case 32768: return ring_fn<BS, 32768, 4096, false>();
+            case 16384: return ring_fn<BS, 16384, 2048, false>();
         }
     } else {
         switch (ring) {
-            case 131072: return ring_fn<131072, 16384, true>();
-            case 65536: return ring_fn<65536, 8192, true>();
-            case 32768: return ring_fn<32768, 4096, true>();
-            case 16384: return ring_fn<16384, 2048, true>();
+            case 131072: return ring_fn<BS, 131072, 16384, true>();
+            case 65536: return ring_fn<BS, 65536, 8192, true>();
+            case 32768: return ring_fn<BS, 32768, 4096, true>();
+            case 16384: return ring_fn<BS, 16384, 2048, true>();
         }
     }
     return nullptr;
 }
+
+static RingFn pick_ring(int bs, int ring, bool spin) {
+    return bs == 1 ? pick_ring_bs<1>(ring, spin) : pick_ring_bs<3>(ring, spin);
+}
+
+using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *);
+static DirectFn pick_direct(int bs) { return bs == 1 ? k_apply_direct<1> : k_apply_direct<3>; }
 
 static int ring_chunk(int ring) { return ring / 8; }
 
@@ -500,7 +593,9 @@ dd_status apply_prepare(dd_ctx *ctx) {
     const int smem_max = (int)prop.sharedMemPerBlockOptin;       // 232448 on B200
     const int smem_sm = (int)prop.sharedMemPerMultiprocessor;    // 233472 on B200
     const int nsl = ctx->sub_last - ctx->sub_first;
-    const int vec_bytes = ((24 * ctx->max_P + 127) / 128) * 128;
+    const int bs = ctx->bs;
+    const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
+    const int flag_bytes = ((4 * ctx->max_P + 127) / 128) * 128;  // sync-free ready flags, 4 B per row
     // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
     {
         LaunchCfg &c = ctx->cfg_direct;
@@ -514,7 +609,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         // the attribute is per function and shared by every context: set the maximum
-        allow_max_smem(k_apply_direct, smem_max);
+        allow_max_smem(pick_direct(bs), smem_max);
     }
     // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
     // Ring choice: the consumer sweep is latency-bound, so maximise resident
@@ -527,11 +622,11 @@ dd_status apply_prepare(dd_ctx *ctx) {
         for (int rc : cands) {
             if (want && rc != want) continue;
             const int nst = rc / ring_chunk(rc);
-            const int sm = vec_bytes + rc + 16 * nst + (spin ? vec_bytes / 6 : 0);
+            const int sm = vec_bytes + rc + 16 * nst + (spin ? flag_bytes : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
-            allow_max_smem(pick_ring(rc, spin), smem_max);
+            allow_max_smem(pick_ring(bs, rc, spin), smem_max);
             int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(rc, spin), TC + 32, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin), TC + 32, sm);
             if (occ > best_occ) {
                 best_occ = occ;
                 best_ring = rc;
@@ -543,7 +638,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
         }
         const int nst = best_ring / ring_chunk(best_ring);
         c.ring = best_ring;
-        c.smem = vec_bytes + best_ring + 16 * nst + (spin ? vec_bytes / 6 : 0);
+        c.smem = vec_bytes + best_ring + 16 * nst + (spin ? flag_bytes : 0);
         c.threads = TC + 32;
         c.consumers = TC;
         c.grid = std::min(nsl, ctx->num_sms * std::max(1, best_occ));
@@ -570,26 +665,28 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int nsl = ctx->sub_last - ctx->sub_first;
     if (nsl == 0) return DD_OK;
-    const int vec_bytes = ((24 * ctx->max_P + 127) / 128) * 128;
+    const int bs = ctx->bs;
+    const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
     if (variant == 0) variant = DD_LEVELSET;
     static const int mode = env_int("DD_APPLY_MODE", 0);  // 1: streaming ceiling (measurement only)
     if (variant == DD_DIRECT) {
         static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
         const LaunchCfg &c = ctx->cfg_direct;
-        k_apply_direct<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf, skip);
+        pick_direct(bs)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf,
+                                                           skip);
     } else if (variant == DD_LEVELSET) {
         const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, r, z, vec_bytes, mode, skip, 0);
     } else if (variant == DD_UNFUSED) {
         // ablation of the fusion (sec. 4.4): the L sweep and the D+U
         // sweep as two launches of the same kernel; the vector makes a round
         // trip through HBM in between (z holds L^-1 r after the first)
         const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, r, z, vec_bytes, mode, skip, 1);
         ++ctx->n_launches;
-        pick_ring(c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, z, z, vec_bytes, mode, skip, 2);
     } else if (variant == DD_SPINLOOP) {
         if (!(ctx->variants & DD_SPINLOOP)) {
@@ -597,7 +694,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         const LaunchCfg &c = ctx->cfg_spin;
-        pick_ring(c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                   nsl, r, z, vec_bytes, mode, skip, 0);
     } else {
         set_error("dd_apply: unknown variant");

@@ -90,6 +90,7 @@ struct LaunchCfg {
 struct dd_ctx {
     // --- topology
     int device = 0, rank = 0, world = 1;
+    int bs = 3;  // unknowns per row: 3 (BSR3) or 1 (scalar CSR)
     bool host_only = false;
     // --- global partition
     int64_t N = 0;                 // global block rows

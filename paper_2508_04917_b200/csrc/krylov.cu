@@ -218,7 +218,7 @@ __device__ __forceinline__ void deliver(const RedArgs &ra, int op, const DD (&ou
 
 // ------------------------------------------------------------------- SpMV
 // One warp per 32-row slice; thread = block row; 3 FMA chains per thread.
-template <int MODE, int MINB>
+template <int BS, int MODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_spmv(int64_t n_rows, int64_t n_slices, const int64_t *__restrict__ slot_ptr,
                                               const int32_t *__restrict__ cols, const double *__restrict__ vals,
                                               const double *__restrict__ x, const double *__restrict__ xg,
@@ -236,6 +236,26 @@ __global__ void __launch_bounds__(256, MINB) k_spmv(int64_t n_rows, int64_t n_sl
         const int K = (int)((slot_ptr[sl + 1] - base) >> 5);
         const int64_t row = 32 * sl + lane;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if constexpr (BS == 1) {
+            // scalar CSR rows: one value plane per k, acc = fma(a_ij, x_j, acc)
+            for (int k = 0; k < K; ++k) {
+                const int64_t slot = base + 32 * k + lane;
+                const int32_t j = __ldg(cols + slot);
+                if (j < 0) continue;
+                const double xj = j < n_rows ? __ldg(x + j) : __ldg(xg + (j - n_rows));
+                a0 = __fma_rn(__ldg(vals + slot), xj, a0);
+            }
+            if (row < n_rows) {
+                y[row] = a0;
+                if (MODE == SPMV_SIGMA) {
+                    dot2_acc(d0.s, d0.c, aux[row], a0);
+                } else if (MODE == SPMV_TS_TT) {
+                    dot2_acc(d0.s, d0.c, a0, aux[row]);
+                    dot2_acc(d1.s, d1.c, a0, a0);
+                }
+            }
+            continue;
+        }
         for (int k = 0; k < K; ++k) {
             const int64_t slot = base + 32 * k + lane;
             const int32_t j = __ldg(cols + slot);
@@ -449,16 +469,19 @@ __global__ void k_finalize_gathered(int world, int nv, const double *__restrict_
 }
 
 // permutation helpers: out[3 li + c] = in[3 idx[li] + c] and the reverse
+// row gather / scatter of bs-wide rows (bs = 3: BSR3, 1: scalar CSR)
+template <int BS>
 __global__ void k_gather3(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
                           double *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = in[3 * (int64_t)idx[i / 3] + i % 3];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < BS * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[BS * (int64_t)idx[i / BS] + i % BS];
 }
 
+template <int BS>
 __global__ void k_scatter3(int64_t n, const int32_t *__restrict__ idx, const double *__restrict__ in,
                            double *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * blockDim.x)
-        out[3 * (int64_t)idx[i / 3] + i % 3] = in[i];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < BS * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[BS * (int64_t)idx[i / BS] + i % BS] = in[i];
 }
 
 }  // namespace ddk
@@ -469,13 +492,17 @@ namespace ddk {
 // DD_SPMV_MINB_<mode> (experiment knob): min resident blocks per SM for the
 // launch bounds of each SpMV mode (1 = compiler's choice).
 template <int MODE>
-static void spmv_go(int minb, int grid, cudaStream_t st, int64_t n, const ddi::SpmvDev &S, const double *x, const double *xg,
-                    double *y, const double *aux, const RedArgs &ra) {
+static void spmv_go(int bs, int minb, int grid, cudaStream_t st, int64_t n, const ddi::SpmvDev &S, const double *x,
+                    const double *xg, double *y, const double *aux, const RedArgs &ra) {
+    if (bs == 1) {
+        k_spmv<1, MODE, 1><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra);
+        return;
+    }
     switch (minb) {
-        case 8: k_spmv<MODE, 8><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
-        case 6: k_spmv<MODE, 6><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
-        case 5: k_spmv<MODE, 5><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
-        default: k_spmv<MODE, 1><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        case 8: k_spmv<3, MODE, 8><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        case 6: k_spmv<3, MODE, 6><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        case 5: k_spmv<3, MODE, 5><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
+        default: k_spmv<3, MODE, 1><<<grid, 256, 0, st>>>(n, S.n_slices, S.slot_ptr, S.cols, S.vals, x, xg, y, aux, ra); break;
     }
 }
 
@@ -497,9 +524,9 @@ void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg,
     static const int mb0 = env_i("DD_SPMV_MINB_0", 1), mb1 = env_i("DD_SPMV_MINB_1", 5),
                      mb2 = env_i("DD_SPMV_MINB_2", 5);
     switch (mode) {
-        case SPMV_PLAIN: spmv_go<SPMV_PLAIN>(mb0, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
-        case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(mb1, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
-        case SPMV_TS_TT: spmv_go<SPMV_TS_TT>(mb2, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_PLAIN: spmv_go<SPMV_PLAIN>(ctx->bs, mb0, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(ctx->bs, mb1, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
+        case SPMV_TS_TT: spmv_go<SPMV_TS_TT>(ctx->bs, mb2, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
     }
 }
 
@@ -555,12 +582,14 @@ void launch_finalize_gathered(int world, int nv, const double *gathered, const R
 }
 void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st) {
     ++ctx->n_launches;
-    k_gather3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+    if (ctx->bs == 1) k_gather3<1><<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+    else k_gather3<3><<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
 }
 void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out,
                      cudaStream_t st) {
     ++ctx->n_launches;
-    k_scatter3<<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+    if (ctx->bs == 1) k_scatter3<1><<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
+    else k_scatter3<3><<<ctx->num_sms * 8, 256, 0, st>>>(n, idx, in, out);
 }
 size_t partials_bytes(const dd_ctx *ctx) {
     return sizeof(DD) * 2 * (size_t)std::max<int64_t>(ctx->num_sms * 8, spmv_fused_grid(ctx));

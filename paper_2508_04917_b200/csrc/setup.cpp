@@ -77,6 +77,23 @@ static inline bool blk_inv(const double *m, double floor_, double *out) {
     return true;
 }
 
+// block size dispatch: bs = 3 (BSR3, the ops above) or 1 (scalar CSR, the
+// same formulas with 1x1 blocks: c = a*b, w = fma(-l, u, w), inv = 1/a)
+static inline void bmul(int bs, const double *A, const double *B, double *C) {
+    if (bs == 3) blk_mul(A, B, C);
+    else C[0] = A[0] * B[0];
+}
+static inline void bsub_mul(int bs, double *W, const double *L, const double *U) {
+    if (bs == 3) blk_sub_mul(W, L, U);
+    else W[0] = std::fma(-L[0], U[0], W[0]);
+}
+static inline bool binv(int bs, const double *m, double floor_, double *out) {
+    if (bs == 3) return blk_inv(m, floor_, out);
+    if (!(std::fabs(m[0]) >= floor_)) return false;
+    out[0] = 1.0 / m[0];
+    return true;
+}
+
 // ---------------------------------------------------------- slab packing
 namespace {
 
@@ -102,7 +119,7 @@ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Append one record for `rows` (already sorted by nblk descending, stable).
 void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool upper,
-                uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp) {
+                uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp, int b2) {
     const int w = (int)rows.size();
     int K = 0;
     int nnz = 0;
@@ -112,8 +129,8 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
     }
     const size_t off_desc = rec_off_desc(K), dw = rec_dw(K);
     const size_t off_dinv = rec_off_dinv(K, w);
-    const size_t off_val = off_dinv + (upper ? 72 * (size_t)w : 0);
-    const size_t bytes = al(off_val + 72 * (size_t)nnz, 16);
+    const size_t off_val = off_dinv + (upper ? 8 * (size_t)b2 * w : 0);
+    const size_t bytes = al(off_val + 8 * (size_t)b2 * nnz, 16);
     const size_t base = out.size();
     out.resize(base + bytes, 0);
     uint8_t *p = out.data() + base;
@@ -139,7 +156,7 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
     }
     if (upper) {
         double *dv = reinterpret_cast<double *>(p + off_dinv);
-        for (int v = 0; v < 9; ++v)
+        for (int v = 0; v < b2; ++v)
             for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
         if (mp.Doff)
             for (int t = 0; t < w; ++t) {
@@ -151,13 +168,13 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
     size_t pos = 0;
     for (int k = 0; k < K; ++k) {
         const int ck = cnt[k];
-        for (int v = 0; v < 9; ++v)
-            for (int t = 0; t < ck; ++t) vv[9 * pos + (size_t)v * ck + t] = rows[t].vals[9 * (size_t)k + v];
+        for (int v = 0; v < b2; ++v)
+            for (int t = 0; t < ck; ++t) vv[b2 * pos + (size_t)v * ck + t] = rows[t].vals[b2 * (size_t)k + v];
         int64_t *mo = upper ? mp.Uoff : mp.Loff;
         int32_t *ms = upper ? mp.Ust : mp.Lst;
         if (mo)
             for (int t = 0; t < ck; ++t) {
-                mo[rows[t].src0 + k] = (int64_t)(base + off_val + 8 * (9 * pos + (size_t)t));
+                mo[rows[t].src0 + k] = (int64_t)(base + off_val + 8 * (b2 * pos + (size_t)t));
                 ms[rows[t].src0 + k] = 8 * ck;
             }
         pos += ck;
@@ -168,7 +185,7 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
 // groups: sequences of rows; barrier after each group with barrier flag.
 void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &groups,
                  const std::vector<bool> &barrier, bool upper, int rmax, int32_t col_base,
-                 int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp) {
+                 int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp, int b2) {
     for (size_t g = 0; g < groups.size(); ++g) {
         auto &rows = groups[g];
         std::stable_sort(rows.begin(), rows.end(),
@@ -180,7 +197,7 @@ void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &gr
             uint16_t fl = 0;
             if (e == w && barrier[g]) fl |= REC_BARRIER;
             if (last_section && g + 1 == groups.size() && e == w) fl |= REC_LAST;
-            put_record(out, part, upper, fl, col_base, max_rec, mp);
+            put_record(out, part, upper, fl, col_base, max_rec, mp, b2);
             ++n_rec;
         }
     }
@@ -208,6 +225,11 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         return DD_E_INVALID_ARG;
     }
     if (o->n_threads > 0) omp_set_num_threads(o->n_threads);
+    const int bs = ctx->bs, b2 = bs * bs;  // 3: BSR3, 1: scalar CSR
+    if (bs == 1 && o->enable_refactor) {
+        set_error("dd_setup: enable_refactor is not supported for the scalar CSR path");
+        return DD_E_INVALID_ARG;
+    }
     ctx->N = N;
     ctx->nnzb_A = A->nnzb;
 
@@ -346,7 +368,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     const int64_t nnz_loc = Arp[nl];
     std::vector<int32_t> gcol(nnz_loc);
-    ctx->Av.assign(9 * nnz_loc, 0.0);
+    ctx->Av.assign(b2 * nnz_loc, 0.0);
     ctx->refactor = o->enable_refactor != 0;
     ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
     if (ctx->refactor) ctx->Asrc.assign(nnz_loc, -1);
@@ -371,7 +393,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         std::sort(ix, ix + nb, [&](int32_t a, int32_t b) { return cc[a] < cc[b]; });
         for (int64_t t = 0; t < nb; ++t) {
             gcol[Arp[li] + t] = cc[ix[t]];
-            std::memcpy(&ctx->Av[9 * (Arp[li] + t)], &av[9 * (rp[m] + ix[t])], 9 * sizeof(double));
+            std::memcpy(&ctx->Av[b2 * (Arp[li] + t)], &av[b2 * (rp[m] + ix[t])], b2 * sizeof(double));
             if (ctx->refactor) ctx->Asrc[Arp[li] + t] = rp[m] + ix[t];
         }
     }
@@ -470,9 +492,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     ctx->Lci.assign(ctx->Lrp[nl], 0);
     ctx->Uci.assign(ctx->Urp[nl], 0);
-    ctx->Lv.assign(9 * ctx->Lrp[nl], 0.0);
-    ctx->Uv.assign(9 * ctx->Urp[nl], 0.0);
-    ctx->Dinv.assign(9 * nl, 0.0);
+    ctx->Lv.assign(b2 * ctx->Lrp[nl], 0.0);
+    ctx->Uv.assign(b2 * ctx->Urp[nl], 0.0);
+    ctx->Dinv.assign(b2 * nl, 0.0);
     ctx->hmapL.assign(nl, 0);
     ctx->hmapU.assign(nl, 0);
 
@@ -499,7 +521,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                     const int64_t g = gcol[p];
                     if (g >= a && g < e) {
                         lci.push_back((int32_t)(g - a));
-                        W.insert(W.end(), &ctx->Av[9 * p], &ctx->Av[9 * p] + 9);
+                        W.insert(W.end(), &ctx->Av[b2 * p], &ctx->Av[b2 * p] + b2);
                     }
                 }
                 lrp[i + 1] = (int64_t)lci.size();
@@ -515,14 +537,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 for (int64_t p = lrp[i]; p < ldg[i]; ++p) {
                     const int64_t k = lci[p];
                     // L_ik = W_ik * U_kk^-1 (right multiplication, R12)
-                    blk_mul(&W[9 * p], &ctx->Dinv[9 * (la + k)], &W[9 * p]);
+                    bmul(bs, &W[b2 * p], &ctx->Dinv[b2 * (la + k)], &W[b2 * p]);
                     // W_ij -= L_ik U_kj for j in pattern(i) and (k,j) in U
                     for (int64_t q = ldg[k] + 1; q < lrp[k + 1]; ++q) {
                         const int64_t tgt = pos[lci[q]];
-                        if (tgt >= 0) blk_sub_mul(&W[9 * tgt], &W[9 * p], &W[9 * q]);
+                        if (tgt >= 0) bsub_mul(bs, &W[b2 * tgt], &W[b2 * p], &W[b2 * q]);
                     }
                 }
-                if (!blk_inv(&W[9 * ldg[i]], floor_, &ctx->Dinv[9 * (la + i)])) {
+                if (!binv(bs, &W[b2 * ldg[i]], floor_, &ctx->Dinv[b2 * (la + i)])) {
                     bad_pivot = std::min(bad_pivot, a + i);
                     failed = true;
                 }
@@ -536,11 +558,11 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) {
                     if (lci[p] < i) {
                         ctx->Lci[qL] = (int32_t)(la + lci[p]);
-                        std::memcpy(&ctx->Lv[9 * qL], &W[9 * p], 9 * sizeof(double));
+                        std::memcpy(&ctx->Lv[b2 * qL], &W[b2 * p], b2 * sizeof(double));
                         ++qL;
                     } else if (lci[p] > i) {
                         ctx->Uci[qU] = (int32_t)(la + lci[p]);
-                        blk_mul(&ctx->Dinv[9 * li], &W[9 * p], &ctx->Uv[9 * qU]);
+                        bmul(bs, &ctx->Dinv[b2 * li], &W[b2 * p], &ctx->Uv[b2 * qU]);
                         ++qU;
                     }
                 }
@@ -669,13 +691,15 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     for (int64_t li = 0; li < nl; ++li)
         Kmax = std::max<int32_t>(Kmax, (int32_t)std::max(ctx->Lrp[li + 1] - ctx->Lrp[li], ctx->Urp[li + 1] - ctx->Urp[li]));
     {
-        const int64_t vec = (24 * (int64_t)ctx->max_P + 127) / 128 * 128;
+        const int64_t vec = (8 * bs * (int64_t)ctx->max_P + 127) / 128 * 128;
         const int64_t avail = 232448 - vec - 2 * (int64_t)ctx->max_P - 1024;
         int64_t ring = 131072;
         while (ring > 16384 && ring > avail) ring /= 2;
         const int64_t ch = ring / 8;
         int32_t rmax = 128;
-        auto est = [&](int64_t R) { return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 72 * R + 72 * R * Kmax + 16; };
+        auto est = [&](int64_t R) {
+            return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 8 * b2 * R + 8 * b2 * R * Kmax + 16;
+        };
         while (rmax > 16 && est(rmax) + ch > ring) rmax /= 2;
         if (const char *e = getenv("DD_ROWS_PER_REC")) rmax = std::max(16, std::min(rmax, atoi(e)));
         ctx->slab_lvl.rows_per_rec = rmax;
@@ -705,12 +729,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             auto rowL = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Lrp[li + 1] - ctx->Lrp[li]), &ctx->Lci[ctx->Lrp[li]],
-                              &ctx->Lv[9 * ctx->Lrp[li]], nullptr, ctx->Lrp[li], li};
+                              &ctx->Lv[b2 * ctx->Lrp[li]], nullptr, ctx->Lrp[li], li};
             };
             auto rowU = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Urp[li + 1] - ctx->Urp[li]), &ctx->Uci[ctx->Urp[li]],
-                              &ctx->Uv[9 * ctx->Urp[li]], &ctx->Dinv[9 * li], ctx->Urp[li], li};
+                              &ctx->Uv[b2 * ctx->Urp[li]], &ctx->Dinv[b2 * li], ctx->Urp[li], li};
             };
             std::vector<std::vector<RowRef>> gL, gU;
             std::vector<bool> bL, bU;
@@ -745,9 +769,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             }
             int32_t nrec = 0;
             int64_t mr = 0;
-            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp);
+            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp, b2);
             slab.info[q].u_off = (int32_t)per[q].size();
-            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp);
+            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp, b2);
             slab.info[q].stream_bytes = (int32_t)per[q].size();
             slab.info[q].row0 = (int32_t)la;
             slab.info[q].nrows = (int32_t)P;
@@ -790,7 +814,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             sp[s + 1] = sp[s] + 32 * K;
         }
         S.n_slots = sp[S.n_slices];
-        ctx->spmv_bytes = S.n_slots * (4 + 72) + 8 * (S.n_slices + 1);
+        ctx->spmv_bytes = S.n_slots * (4 + 8 * b2) + 8 * (S.n_slices + 1);
     }
     ctx->setup_ms[4] = now_ms() - t4;
     return DD_OK;

@@ -10,6 +10,7 @@ def oracle_local_factors(S, row_first, n_local):
     [row_first, row_first + n_local), columns shifted to local numbering."""
     rp, ci = S["rp_d"], S["ci_d"]
     n = S["n"]
+    b2 = S.get("bs", 3) ** 2
     rows = np.repeat(np.arange(n), np.diff(rp))
     sel = (rows >= row_first) & (rows < row_first + n_local)
     lo = (ci < rows) & sel
@@ -19,8 +20,8 @@ def oracle_local_factors(S, row_first, n_local):
         r = rows[mask] - row_first
         out[key + "rp"] = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=n_local))]).astype(np.int64)
         out[key + "ci"] = (ci[mask] - row_first).astype(np.int32)
-        out[key + "v"] = vals.reshape(-1, 9)[mask].ravel()
-    out["Dinv"] = S["dinv"][9 * row_first:9 * (row_first + n_local)]
+        out[key + "v"] = vals.reshape(-1, b2)[mask].ravel()
+    out["Dinv"] = S["dinv"][b2 * row_first:b2 * (row_first + n_local)]
     return out
 
 

@@ -113,3 +113,50 @@ def test_errors_match_oracle():
     with pytest.raises(dd.DDError) as e:
         dd.dd_setup(rp, ci, a, P=2, host_only=True)
     assert e.value.name == "DD_E_SINGULAR_PIVOT" and f"row {eo.value.row}" in str(e.value)
+
+
+# ------------------------------------------- scalar CSR path
+from inputs.gen import laplacian_csr, random_csr_grid, spe10_style_csr  # noqa: E402
+
+CSR_CASES = {
+    "csr_laplace_16^3": (lambda: laplacian_csr(16, 16, 16), dict(grid=(16, 16, 16), tiles=(8, 8, 8))),
+    "csr_random_ragged": (lambda: random_csr_grid(12, 10, 8, seed=11), dict(P=77)),
+    "csr_random_bfs": (lambda: random_csr_grid(12, 10, 8, seed=12), dict(P=100, partitioner="bfs")),
+    "csr_spe10_small": (lambda: spe10_style_csr(20, 40, 20, upper_ness_from=10)[:3],
+                        dict(grid=(20, 40, 20), tiles=(10, 20, 10))),
+    "csr_P1": (lambda: random_csr_grid(5, 4, 3, seed=13), dict(P=1)),
+}
+
+
+@pytest.mark.parametrize("name", list(CSR_CASES))
+def test_host_setup_csr_bitwise_vs_oracle(name):
+    gen, kw = CSR_CASES[name]
+    rp, ci, v = gen()
+    S = oracle.setup_csr(rp, ci, v, **kw)
+    ctx = dd.dd_setup_csr(rp, ci, v, host_only=True, variants=7, **kw)
+    assert ctx.bs == 1
+    assert_setup_bitwise(ctx, S)
+    st = ctx.stats()
+    n = S["n"]
+    rows = np.repeat(np.arange(n), np.diff(S["rp_d"]))
+    nLU = int(np.sum(S["ci_d"] != rows))
+    # canonical scalar apply bytes: 8(nL+nU+n) + 4(nL+nU) + 8(n+1) + 16n
+    assert st["apply_canonical_bytes"] == 8 * (nLU + n) + 4 * nLU + 8 * (n + 1) + 16 * n
+
+
+def test_csr_errors_and_refactor_rejected():
+    rp = np.array([0, 1, 2], np.int64)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup_csr(rp, np.array([1, 0], np.int32), np.ones(2), P=2, host_only=True)
+    assert e.value.name == "DD_E_MISSING_DIAG"
+    rp, ci, v = random_csr_grid(4, 4, 4, seed=1)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup_csr(rp, ci, v, P=8, host_only=True, enable_refactor=True)
+    assert e.value.name == "DD_E_INVALID_ARG"
+    # singular pivot at the oracle's row
+    rp, ci, a = np.array([0, 2, 4], np.int64), np.array([0, 1, 0, 1], np.int32), np.ones(4)
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.s_ilu0(rp, ci, a)
+    with pytest.raises(dd.DDError) as e:
+        dd.dd_setup_csr(rp, ci, a, P=2, host_only=True)
+    assert e.value.name == "DD_E_SINGULAR_PIVOT" and f"row {eo.value.row}" in str(e.value)

@@ -1,0 +1,145 @@
+"""GPU parity of the scalar CSR path (the paper's CSR half,
+P:110) through the C ABI: setup bit-exact, every apply variant and the SpMV
+bitwise equal to the oracle's scalar functions, BiCGSTAB iterations within
++-2, device Alg. 5 levels, and the multi-rank device path at world 2."""
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2508_04917_b200 as dd
+from inputs.gen import csr_to_scipy, laplacian_csr, manufactured_rhs_csr, random_csr_grid, spe10_style_csr
+from tests.parity import assert_setup_bitwise
+
+pytestmark = pytest.mark.gpu
+ALL = dd.DD_LEVELSET | dd.DD_SPINLOOP | dd.DD_DIRECT
+VARIANTS = [dd.DD_LEVELSET, dd.DD_SPINLOOP, dd.DD_DIRECT, dd.DD_UNFUSED]
+
+CASES = {
+    "csr_laplace_32^3": (lambda: laplacian_csr(32, 32, 32), dict(grid=(32, 32, 32), tiles=(16, 16, 8))),
+    "csr_random_ragged": (lambda: random_csr_grid(20, 16, 12, seed=11), dict(P=777)),
+    "csr_random_P1": (lambda: random_csr_grid(6, 5, 4, seed=13), dict(P=1)),
+    "csr_spe10_bfs_P8192": (lambda: spe10_style_csr()[:3], dict(P=8192, partitioner="bfs")),
+    "csr_laplace_P16384": (lambda: laplacian_csr(64, 64, 64), dict(grid=(64, 64, 64), tiles=(32, 32, 16))),
+}
+
+_cache = {}
+
+
+def get_case(name):
+    if name not in _cache:
+        gen, kw = CASES[name]
+        rp, ci, v = gen()
+        S = oracle.setup_csr(rp, ci, v, **kw)
+        ctx = dd.dd_setup_csr(rp, ci, v, variants=ALL, **kw)
+        _cache[name] = (rp, ci, v, S, ctx)
+    return _cache[name]
+
+
+def tvec(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_csr_setup_bitwise(name):
+    _, _, _, S, ctx = get_case(name)
+    assert_setup_bitwise(ctx, S)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=["levelset", "spin", "direct", "unfused"])
+@pytest.mark.parametrize("name", list(CASES))
+def test_csr_apply_bitwise(name, variant):
+    import torch
+    _, _, _, S, ctx = get_case(name)
+    r = np.random.default_rng(2).uniform(-1, 1, S["n"])
+    z_ref = oracle.apply(S, r)
+    z = torch.full((S["n"],), float("nan"), dtype=torch.float64, device="cuda")
+    try:
+        ctx.apply(tvec(r), z, variant)
+    except dd.DDError as e:
+        assert variant == dd.DD_SPINLOOP and e.name == "DD_E_SUBDOMAIN_TOO_LARGE"
+        return
+    torch.cuda.synchronize()
+    zz = z.cpu().numpy()
+    assert np.array_equal(zz, z_ref), f"{np.count_nonzero(zz != z_ref)} entries differ"
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_csr_spmv_bitwise_and_levels(name):
+    import torch
+    _, _, _, S, ctx = get_case(name)
+    x = np.random.default_rng(3).standard_normal(S["n"])
+    y = torch.empty(S["n"], dtype=torch.float64, device="cuda")
+    ctx.spmv(tvec(x), y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle.s_spmv(S["rp_r"], S["ci_r"], S["v_r"], x))
+    hl, hu, _ = ctx.levels_device()
+    assert np.array_equal(hl, S["hmapL"]) and np.array_equal(hu, S["hmapU"])
+
+
+@pytest.mark.parametrize("name", ["csr_laplace_32^3", "csr_random_ragged", "csr_spe10_bfs_P8192"])
+def test_csr_bicgstab(name):
+    import torch
+    rp, ci, v, S, ctx = get_case(name)
+    xs, b = manufactured_rhs_csr(rp, ci, v)
+    br = b[S["new_to_old"]]
+    tol = 1e-8
+    xo, ro = oracle.bicgstab(S, br, tol=tol, max_iter=5000)
+    x = torch.zeros(S["n"], dtype=torch.float64, device="cuda")
+    rg = ctx.bicgstab(tvec(br), x, tol=tol, max_iter=5000, hist=True)
+    assert ro["status"] == 0 and rg["converged"] == 1
+    assert abs(rg["iterations"] - ro["iterations"]) <= 2, (rg["iterations"], ro["iterations"])
+    assert rg["true_rel_resid"] <= 10 * tol
+    k = min(len(rg["resid_hist"]), len(ro["resid_hist"]), 10)
+    assert np.allclose(rg["resid_hist"][:k], ro["resid_hist"][:k], rtol=1e-9, atol=0)
+    # end to end through the host API (original ordering)
+    xh = np.zeros_like(b)
+    rep = ctx.solve_host(b, xh, tol=tol)
+    A = csr_to_scipy(rp, ci, v)
+    assert rep["converged"] == 1 and np.linalg.norm(b - A @ xh) <= 10 * tol * np.linalg.norm(b)
+
+
+def test_csr_local_world2():
+    """Scalar path on two ranks of one process (DD_COMM_LOCAL): halo SpMV and
+    apply bitwise, collective BiCGSTAB converges with identical counts."""
+    import torch
+    rp, ci, v = random_csr_grid(20, 16, 12, seed=21)
+    kw = dict(grid=(20, 16, 12), tiles=(10, 8, 6))
+    S = oracle.setup_csr(rp, ci, v, **kw)
+    N = S["n"]
+    r_glob = np.random.default_rng(4).uniform(-1, 1, N)
+    z_ref = oracle.apply(S, r_glob)
+    y_ref = oracle.s_spmv(S["rp_r"], S["ci_r"], S["v_r"], r_glob)
+    xs, b = manufactured_rhs_csr(rp, ci, v)
+    br = b[S["new_to_old"]]
+    _, rep_ref = oracle.bicgstab(S, br, tol=1e-8, max_iter=2000)
+    key = os.urandom(128)
+    bar = threading.Barrier(2)
+
+    def rank_fn(rank):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = dd.dd_setup_csr(rp, ci, v, rank=rank, world=2, nccl_id=key, comm="local", **kw)
+            f, n = ctx.row_first, ctx.n_local
+            r = tvec(r_glob[f:f + n].copy())
+            z, y = torch.empty_like(r), torch.empty_like(r)
+            ctx.apply(r, z, stream=st)
+            ctx.spmv(r, y, stream=st)
+            x = torch.zeros_like(r)
+            rep = ctx.bicgstab(tvec(br[f:f + n].copy()), x, tol=1e-8, max_iter=2000, stream=st)
+            st.synchronize()
+            out = (z.cpu().numpy(), y.cpu().numpy(), rep)
+            bar.wait()
+            ctx.destroy()
+            return out
+
+    with ThreadPoolExecutor(2) as ex:
+        res = [f.result(timeout=600) for f in [ex.submit(rank_fn, q) for q in range(2)]]
+    assert np.array_equal(np.concatenate([o[0] for o in res]), z_ref)
+    assert np.array_equal(np.concatenate([o[1] for o in res]), y_ref)
+    assert res[0][2]["iterations"] == res[1][2]["iterations"]
+    assert abs(res[0][2]["iterations"] - rep_ref["iterations"]) <= 2
