@@ -38,7 +38,11 @@ namespace ddk {
 
 using ddi::RecHdr;
 using ddi::SubInfo;
-constexpr int TC = 128;  // consumer threads = rows per record (Slab::rows_per_rec)
+// consumer threads = rows per record (Slab::rows_per_rec): 128 for 3x3 rows;
+// 256 for scalar rows, whose per-row work is one short FMA chain, so a level
+// needs fewer records (and barriers)
+template <int BS>
+constexpr int TCB = BS == 1 ? 256 : 128;
 
 __host__ __device__ constexpr uint32_t al8(uint32_t x) { return (x + 7u) & ~7u; }
 
@@ -312,7 +316,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
 // keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
 template <int BS>
-__global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__ slab,
+__global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
                                                      uint32_t pf_bytes, const int *skip) {
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
         }
         const int nd = BS * si.nrows;
         const double *rs = r + BS * (int64_t)si.row0;
-        for (int q = t; q < nd; q += TC) vec[q] = __ldg(rs + q);
+        for (int q = t; q < nd; q += TCB<BS>) vec[q] = __ldg(rs + q);
         __syncthreads();
         uint32_t ro = 0;
         while (true) {
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
             if (last) break;
         }
         double *zs = z + BS * (int64_t)si.row0;
-        for (int q = t; q < nd; q += TC) zs[q] = vec[q];
+        for (int q = t; q < nd; q += TCB<BS>) zs[q] = vec[q];
     }
 }
 
@@ -370,13 +374,14 @@ __global__ void __launch_bounds__(TC) k_apply_direct(const uint8_t *__restrict__
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
 //   the streaming ceiling of the ring.
 template <int BS, uint32_t RING, uint32_t CH, bool SPIN>
-__global__ void __launch_bounds__(TC + 32, 1)
+__global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
                  int phase) {
     // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
+    constexpr int TC = TCB<BS>;
     constexpr uint32_t NW = TC / 32;
     static_assert((RING & (RING - 1)) == 0 && (CH & (CH - 1)) == 0 && NST >= 4, "ring shape");
     extern __shared__ __align__(128) uint8_t smem[];
@@ -596,13 +601,14 @@ dd_status apply_prepare(dd_ctx *ctx) {
     const int bs = ctx->bs;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
     const int flag_bytes = ((4 * ctx->max_P + 127) / 128) * 128;  // sync-free ready flags, 4 B per row
+    const int tc = bs == 1 ? TCB<1> : TCB<3>;
     // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
     {
         LaunchCfg &c = ctx->cfg_direct;
         c.smem = vec_bytes;
-        c.threads = TC;
+        c.threads = bs == 1 ? TCB<1> : TCB<3>;
         c.grid = nsl;
-        c.consumers = TC;
+        c.consumers = c.threads;
         c.ring = 0;
         if (c.smem > smem_max) {
             set_error("subdomain vector exceeds shared memory");
@@ -626,7 +632,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
             allow_max_smem(pick_ring(bs, rc, spin), smem_max);
             int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin), TC + 32, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin), tc + 32, sm);
             if (occ > best_occ) {
                 best_occ = occ;
                 best_ring = rc;
@@ -639,8 +645,8 @@ dd_status apply_prepare(dd_ctx *ctx) {
         const int nst = best_ring / ring_chunk(best_ring);
         c.ring = best_ring;
         c.smem = vec_bytes + best_ring + 16 * nst + (spin ? flag_bytes : 0);
-        c.threads = TC + 32;
-        c.consumers = TC;
+        c.threads = tc + 32;
+        c.consumers = tc;
         c.grid = std::min(nsl, ctx->num_sms * std::max(1, best_occ));
         if (env_int("DD_APPLY_GRID", 0) > 0) c.grid = std::min(nsl, env_int("DD_APPLY_GRID", 0));
         return DD_OK;

@@ -696,11 +696,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         int64_t ring = 131072;
         while (ring > 16384 && ring > avail) ring /= 2;
         const int64_t ch = ring / 8;
-        int32_t rmax = 128;
+        int32_t rmax = bs == 1 ? 256 : 128;  // = the kernels' consumer threads (TCB)
         auto est = [&](int64_t R) {
             return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 8 * b2 * R + 8 * b2 * R * Kmax + 16;
         };
         while (rmax > 16 && est(rmax) + ch > ring) rmax /= 2;
+        // records may use fewer rows than consumer threads, never more
         if (const char *e = getenv("DD_ROWS_PER_REC")) rmax = std::max(16, std::min(rmax, atoi(e)));
         ctx->slab_lvl.rows_per_rec = rmax;
         ctx->slab_spin.rows_per_rec = rmax;
