@@ -695,7 +695,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         const int64_t avail = 232448 - vec - 2 * (int64_t)ctx->max_P - 1024;
         int64_t ring = 131072;
         while (ring > 16384 && ring > avail) ring /= 2;
-        const int64_t ch = ring / 8;
+        const int64_t ch = ring / 4;  // = the kernels' ring chunk (apply.cu ring_chunk)
         int32_t rmax = bs == 1 ? 256 : 128;  // = the kernels' consumer threads (TCB)
         auto est = [&](int64_t R) {
             return (int64_t)rec_off_dinv(Kmax, (uint32_t)R) + 8 * b2 * R + 8 * b2 * R * Kmax + 16;
