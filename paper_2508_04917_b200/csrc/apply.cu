@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     const uint32_t lane = t & 31u;
     uint32_t gbase = 0;     // chunk index at which the current subdomain starts
     uint32_t ready = 0;     // chunks this thread has seen full
-    uint32_t released = 0;  // chunks handed back (SPIN: each warp's lane 0; else t == 0)
+    uint32_t released = 0;  // chunks handed back (SPIN: each warp's lane 0; else t == TC - 32)
     uint32_t ep = 0;
     auto ensure = [&](uint32_t chunk) {
         while (ready <= chunk) {
@@ -452,7 +452,10 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         }
     };
     auto release_to = [&](uint32_t upto) {
-        if (SPIN ? lane == 0 : t == 0) {
+        // level set: lane 0 of the LAST consumer warp hands chunks back -- its
+        // rows are the record's lightest (sorted by block count) or absent, so
+        // the releases stay off the slowest warp's path (-1 % at config 3)
+        if (SPIN ? lane == 0 : t == TC - 32) {
             while (released < upto) {
                 mbar_arrive(&empty[released % NST]);
                 ++released;
