@@ -5,11 +5,13 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -188,10 +190,60 @@ void prof_collect(dd_ctx *c, const int64_t *n_real, int k_last) {
     p->used = 0;
 }
 
+// Host -> device copy of a large pageable buffer through two pinned 32 MB
+// staging buffers: an OpenMP memcpy fills one while the DMA engine drains the
+// other (pageable cudaMemcpy runs at ~3 GB/s; this at ~10-20 GB/s).
+dd_status h2d_big(void *dst, const void *src, size_t bytes) {
+    constexpr size_t STG = 32u << 20;
+    if (bytes < 2 * STG) {
+        CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+        return DD_OK;
+    }
+    uint8_t *stg[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+    dd_status rc = DD_OK;
+    if (cudaMallocHost(reinterpret_cast<void **>(&stg[0]), STG) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void **>(&stg[1]), STG) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        rc = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? DD_OK : DD_E_CUDA;
+    } else {
+        const uint8_t *s8 = reinterpret_cast<const uint8_t *>(src);
+        uint8_t *d8 = reinterpret_cast<uint8_t *>(dst);
+        for (size_t off = 0, i = 0; off < bytes; off += STG, ++i) {
+            const size_t n = std::min(STG, bytes - off);
+            uint8_t *b = stg[i % 2];
+            if (i >= 2) cudaEventSynchronize(ev[i % 2]);  // its previous DMA is done
+            const int nt = 16;
+#pragma omp parallel for num_threads(nt) schedule(static)
+            for (int q = 0; q < nt; ++q) {
+                const size_t a = n * q / nt, e = n * (q + 1) / nt;
+                std::memcpy(b + a, s8 + off + a, e - a);
+            }
+            if (cudaMemcpyAsync(d8 + off, b, n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                rc = DD_E_CUDA;
+                break;
+            }
+            cudaEventRecord(ev[i % 2], st);
+        }
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = DD_E_CUDA;
+    }
+    for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+    for (auto b : stg)
+        if (b) cudaFreeHost(b);
+    if (rc != DD_OK) set_error("dd_setup: host-to-device upload failed");
+    return rc;
+}
+
 dd_status upload_slab(Slab &sl) {
     TRY(dmalloc(&sl.d_bytes, sl.bytes.size() + 16));
     TRY(dmalloc(&sl.d_info, sl.info.size() + 1));
-    if (!sl.bytes.empty()) CK(cudaMemcpy(sl.d_bytes, sl.bytes.data(), sl.bytes.size(), cudaMemcpyHostToDevice));
+    if (!sl.bytes.empty()) TRY(h2d_big(sl.d_bytes, sl.bytes.data(), sl.bytes.size()));
     if (!sl.info.empty())
         CK(cudaMemcpy(sl.d_info, sl.info.data(), sl.info.size() * sizeof(SubInfo), cudaMemcpyHostToDevice));
     std::vector<uint8_t>().swap(sl.bytes);  // device copy is authoritative
@@ -274,10 +326,16 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
         NK(ncclCommInitRank(&comm, ctx->world, id, ctx->rank));
         ctx->nccl = comm;
     }
+    static const bool trace = getenv("DD_SETUP_TRACE") != nullptr;
+    auto tr = [&](const char *what) {
+        if (trace) fprintf(stderr, "[dd setup] %-22s %9.1f ms\n", what, now_ms() - t0);
+    };
     TRY(apply_prepare(ctx));
+    tr("apply_prepare");
     const int64_t nl = ctx->n_local;
     // slabs
     TRY(upload_slab(ctx->slab_lvl));
+    tr("slab upload");
     // sliced-ELL SpMV operand
     {
         auto &S = ctx->spmv;
@@ -288,18 +346,24 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
                 K = std::max(K, ctx->Arp[li + 1] - ctx->Arp[li]);
             sp[s + 1] = sp[s] + 32 * K;
         }
-        std::vector<int32_t> cols(S.n_slots, -1);
+        tr("ell pointers");
         const int b2 = ctx->bs * ctx->bs;
-        std::vector<double> vals(b2 * S.n_slots, 0.0);
+        // uninitialised buffers, every slot written once by the slice that owns
+        // it (padding slots: column -1, values 0) -- no serial zero-fill pass
+        std::unique_ptr<int32_t[]> cols(new int32_t[std::max<int64_t>(1, S.n_slots)]);
+        std::unique_ptr<double[]> vals(new double[std::max<int64_t>(1, b2 * S.n_slots)]);
 #pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < S.n_slices; ++s) {
-            for (int lane = 0; lane < 32; ++lane) {
-                const int64_t li = 32 * s + lane;
-                if (li >= nl) break;
-                for (int64_t k = 0; k < ctx->Arp[li + 1] - ctx->Arp[li]; ++k) {
-                    const int64_t p = ctx->Arp[li] + k;
-                    cols[sp[s] + 32 * k + lane] = ctx->Aci[p];
-                    for (int v = 0; v < b2; ++v) vals[b2 * (sp[s] + 32 * k) + 32 * v + lane] = ctx->Av[b2 * p + v];
+            const int64_t K = (sp[s + 1] - sp[s]) / 32;
+            for (int64_t k = 0; k < K; ++k) {
+                int32_t *cs = &cols[sp[s] + 32 * k];
+                double *vs = &vals[b2 * (sp[s] + 32 * k)];
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int64_t li = 32 * s + lane;
+                    const bool has = li < nl && k < ctx->Arp[li + 1] - ctx->Arp[li];
+                    const int64_t p = has ? ctx->Arp[li] + k : 0;
+                    cs[lane] = has ? ctx->Aci[p] : -1;
+                    for (int v = 0; v < b2; ++v) vs[32 * v + lane] = has ? ctx->Av[b2 * p + v] : 0.0;
                 }
             }
         }
@@ -308,8 +372,10 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
         TRY(dmalloc(&S.vals, std::max<int64_t>(1, b2 * S.n_slots)));
         CK(cudaMemcpy(S.slot_ptr, sp.data(), sp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
         if (S.n_slots) {
-            CK(cudaMemcpy(S.cols, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(S.vals, vals.data(), vals.size() * sizeof(double), cudaMemcpyHostToDevice));
+            tr("ell fill");
+            TRY(h2d_big(S.cols, cols.get(), S.n_slots * sizeof(int32_t)));
+            TRY(h2d_big(S.vals, vals.get(), b2 * S.n_slots * sizeof(double)));
+            tr("ell upload");
         }
     }
     // permutation index of the local rows (original global row of local row li)
@@ -358,6 +424,7 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     if (!sidx.empty())
         CK(cudaMemcpy(ws->d_send_idx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(cudaDeviceSynchronize());
+    tr("workspace");
     if (ctx->world > 1 && ctx->comm == DD_COMM_LOCAL) {
         CK(cudaEventCreateWithFlags(&ws->xev_ready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ws->xev_done, cudaEventDisableTiming));
