@@ -37,7 +37,8 @@ def run_ranks(world, fn):
 
 
 @pytest.mark.parametrize("name,world", [("random_8sub", 2), ("random_8sub", 3), ("laplace_24^3", 2),
-                                        ("chunks_ragged_oddP", 2), ("spe10_small", 3)])
+                                        ("laplace_24^3", 4), ("chunks_ragged_oddP", 2), ("chunks_ragged_oddP", 5),
+                                        ("spe10_small", 3)])
 def test_local_world_parity(name, world):
     import torch
     gen, kw = CASES[name]
