@@ -38,6 +38,9 @@ __all__ = [
     "random_csr_grid",
     "csr_to_scipy",
     "manufactured_rhs_csr",
+    "stencil27_pattern",
+    "random_block_stencil27",
+    "random_csr_stencil27",
 ]
 
 
@@ -286,6 +289,60 @@ def random_block_grid(nx: int, ny: int, nz: int, seed: int, dominance: float = 1
     d[:, d3, d3] = absrow + dominance
     vals[dpos] = d
     return row_ptr, col_idx, vals.reshape(-1)
+
+
+def stencil27_pattern(nx: int, ny: int, nz: int):
+    """27-point pattern (all neighbours within distance 1 in each coordinate),
+    natural order, columns ascending: up to 13 strictly-lower blocks per row."""
+    n = nx * ny * nz
+    g = np.arange(n, dtype=np.int64)
+    i, j, k = g % nx, (g // nx) % ny, g // (nx * ny)
+    cols, masks = [], []
+    for dk in (-1, 0, 1):
+        for dj in (-1, 0, 1):
+            for di in (-1, 0, 1):
+                ok = (i + di >= 0) & (i + di < nx) & (j + dj >= 0) & (j + dj < ny) & (k + dk >= 0) & (k + dk < nz)
+                cols.append(g + di + nx * (dj + ny * dk))
+                masks.append(ok)
+    cols = np.stack(cols, axis=1)
+    mask = np.stack(masks, axis=1)  # offsets ascend with (dk, dj, di) -> columns ascending
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(mask.sum(axis=1), out=row_ptr[1:])
+    return row_ptr, cols[mask].astype(np.int32)
+
+
+def random_block_stencil27(nx: int, ny: int, nz: int, seed: int, dominance: float = 1.0):
+    """27-point pattern with random full 3x3 blocks, block-row diagonally dominant
+    (rows with up to 13 lower and 13 upper blocks: the general-K record path)."""
+    rng = np.random.default_rng(seed)
+    row_ptr, col_idx = stencil27_pattern(nx, ny, nz)
+    n = nx * ny * nz
+    vals = rng.uniform(-1.0, 1.0, (col_idx.shape[0], 3, 3))
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    diag = col_idx == rows
+    absrow = np.zeros((n, 3))
+    np.add.at(absrow, rows[~diag], np.abs(vals[~diag]).sum(axis=2))
+    d3 = np.arange(3)
+    dpos = np.nonzero(diag)[0]
+    d = vals[dpos]
+    absrow += np.abs(d).sum(axis=2) - np.abs(d[:, d3, d3])
+    d[:, d3, d3] = absrow + dominance
+    vals[dpos] = d
+    return row_ptr, col_idx, vals.reshape(-1)
+
+
+def random_csr_stencil27(nx: int, ny: int, nz: int, seed: int, dominance: float = 1.0):
+    """Scalar 27-point analogue of random_block_stencil27."""
+    rng = np.random.default_rng(seed)
+    row_ptr, col_idx = stencil27_pattern(nx, ny, nz)
+    n = nx * ny * nz
+    vals = rng.uniform(-1.0, 1.0, col_idx.shape[0])
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    diag = col_idx == rows
+    absrow = np.zeros(n)
+    np.add.at(absrow, rows[~diag], np.abs(vals[~diag]))
+    vals[diag] = absrow + dominance
+    return row_ptr, col_idx, vals
 
 
 def random_block_chain(n: int, seed: int, dominance: float = 1.0):

@@ -11,7 +11,8 @@ import pytest
 
 import oracle
 import paper_2508_04917_b200 as dd
-from inputs.gen import csr_to_scipy, laplacian_csr, manufactured_rhs_csr, random_csr_grid, spe10_style_csr
+from inputs.gen import (csr_to_scipy, laplacian_csr, manufactured_rhs_csr, random_csr_grid, random_csr_stencil27,
+                        spe10_style_csr)
 from tests.parity import assert_setup_bitwise
 
 pytestmark = pytest.mark.gpu
@@ -24,6 +25,7 @@ CASES = {
     "csr_random_P1": (lambda: random_csr_grid(6, 5, 4, seed=13), dict(P=1)),
     "csr_spe10_bfs_P8192": (lambda: spe10_style_csr()[:3], dict(P=8192, partitioner="bfs")),
     "csr_laplace_P16384": (lambda: laplacian_csr(64, 64, 64), dict(grid=(64, 64, 64), tiles=(32, 32, 16))),
+    "csr_stencil27_bfs": (lambda: random_csr_stencil27(24, 20, 16, seed=33), dict(P=1500, partitioner="bfs")),
 }
 
 _cache = {}
@@ -81,7 +83,7 @@ def test_csr_spmv_bitwise_and_levels(name):
     assert np.array_equal(hl, S["hmapL"]) and np.array_equal(hu, S["hmapU"])
 
 
-@pytest.mark.parametrize("name", ["csr_laplace_32^3", "csr_random_ragged", "csr_spe10_bfs_P8192"])
+@pytest.mark.parametrize("name", ["csr_laplace_32^3", "csr_random_ragged", "csr_spe10_bfs_P8192", "csr_stencil27_bfs"])
 def test_csr_bicgstab(name):
     import torch
     rp, ci, v, S, ctx = get_case(name)

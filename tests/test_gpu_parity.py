@@ -10,7 +10,7 @@ import pytest
 import oracle
 import paper_2508_04917_b200 as dd
 from inputs.gen import (apply_input, laplacian_bsr3, manufactured_rhs, random_block_grid,
-                        spe10_style_bsr3)
+                        random_block_stencil27, spe10_style_bsr3)
 from tests.parity import assert_setup_bitwise
 
 pytestmark = pytest.mark.gpu
@@ -30,6 +30,9 @@ CASES = {
     "one_subdomain": (lambda: random_block_grid(12, 12, 12, seed=7), dict(grid=(12, 12, 12), tiles=(12, 12, 12))),
     "spe10_style_cfg4": (lambda: spe10_style_bsr3()[:3], dict(grid=(60, 220, 85), tiles=(10, 20, 17))),
     "spe10_style_bfs_P2048": (lambda: spe10_style_bsr3()[:3], dict(P=2048, partitioner="bfs")),
+    # 27-point pattern: up to 13 lower / 13 upper blocks per row -> the general-K record path
+    "stencil27_geo": (lambda: random_block_stencil27(16, 12, 10, seed=31), dict(grid=(16, 12, 10), tiles=(8, 6, 5))),
+    "stencil27_bfs_ragged": (lambda: random_block_stencil27(14, 10, 9, seed=32), dict(P=333, partitioner="bfs")),
 }
 
 _cache = {}
@@ -110,7 +113,8 @@ def test_spmv_bitwise(name):
 
 @pytest.mark.parametrize("name,tol", [("cfg1_16^3", 1e-8), ("cfg2a_64^3", 1e-8), ("random_blocks", 1e-8),
                                       ("spe10_style_cfg4", 1e-8), ("spe10_style_cfg4", 1e-6),
-                                      ("chunks_ragged_oddP", 1e-8), ("spe10_style_bfs_P2048", 1e-8)])
+                                      ("chunks_ragged_oddP", 1e-8), ("spe10_style_bfs_P2048", 1e-8),
+                                      ("stencil27_geo", 1e-8), ("stencil27_bfs_ragged", 1e-8)])
 def test_bicgstab_iterations(name, tol):
     import torch
     rp, ci, v, S, ctx = get_case(name)
