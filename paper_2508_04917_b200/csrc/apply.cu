@@ -85,7 +85,7 @@ __device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, ui
 // Every load (descriptor, values, Dinv) is addressed from (t, cnt) alone, so
 // all are in flight before the first FMA; the only dependent step is the
 // gather of vec[3j..3j+2] through the descriptor's column ids.
-template <bool SPIN, class Rd>
+template <bool SPIN, bool GEN, class Rd>
 __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
@@ -94,7 +94,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
-    if (K <= 3) {
+    if (!GEN || K <= 3) {
         const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
         const uint32_t i = d.x & 0xffffu;
         const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
@@ -157,7 +157,10 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         }
         return;
     }
-    // ---- general K (> 3): descriptor of rec_dw(K) bytes, loop over k
+    // ---- general K (> 3): descriptor of rec_dw(K) bytes, loop over k. Compiled
+    // only into the GEN kernels (slabs with more than 3 blocks per row in a
+    // triangle): it needs more registers than the 7-point path.
+    if constexpr (GEN) {
     const uint32_t dw = ddi::rec_dw(K);
     const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * t);
     double a0, a1, a2;
@@ -181,27 +184,48 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         a1 = vec[3 * i + 1];
         a2 = vec[3 * i + 2];
     }
+    // blocks in groups of three: a group's counts, columns and values are all
+    // loaded before its FMAs (as in the K <= 3 path), so a row with K blocks
+    // has ceil(K/3) dependent load rounds instead of K
     uint32_t pre = 0;
-    for (uint32_t k = 0; k < K; ++k) {
-        const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
-        if ((uint32_t)t >= ck) break;
-        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k));
-        const uint32_t vb = off_val + 72u * pre + 8u * t;
-        double b[9];
+    for (uint32_t k0 = 0; k0 < K; k0 += 3) {
+        uint32_t ck[3];
 #pragma unroll
-        for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + 8u * ck * v);
-        if (SPIN) spin_until(flags, j, ep);
-        const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
-        a0 = __fma_rn(-b[0], x0, a0);
-        a0 = __fma_rn(-b[1], x1, a0);
-        a0 = __fma_rn(-b[2], x2, a0);
-        a1 = __fma_rn(-b[3], x0, a1);
-        a1 = __fma_rn(-b[4], x1, a1);
-        a1 = __fma_rn(-b[5], x2, a1);
-        a2 = __fma_rn(-b[6], x0, a2);
-        a2 = __fma_rn(-b[7], x1, a2);
-        a2 = __fma_rn(-b[8], x2, a2);
-        pre += ck;
+        for (int q = 0; q < 3; ++q) {
+            const uint32_t k = k0 + q;
+            ck[q] = k < K ? rd.template ld<uint16_t>(16u + 2u * k) : 0u;
+        }
+        if ((uint32_t)t >= ck[0]) break;  // rows sorted by block count: none further
+        uint32_t j[3];
+        double b[3][9];
+        uint32_t pq = pre;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if ((uint32_t)t < ck[q]) {
+                j[q] = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k0 + q));
+                const uint32_t vb = off_val + 72u * pq + 8u * t;
+#pragma unroll
+                for (int v = 0; v < 9; ++v) b[q][v] = rd.template ld<double>(vb + 8u * ck[q] * v);
+            }
+            pq += ck[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if ((uint32_t)t < ck[q]) {
+                if (SPIN) spin_until(flags, j[q], ep);
+                const double x0 = vec[3 * j[q]], x1 = vec[3 * j[q] + 1], x2 = vec[3 * j[q] + 2];
+                a0 = __fma_rn(-b[q][0], x0, a0);
+                a0 = __fma_rn(-b[q][1], x1, a0);
+                a0 = __fma_rn(-b[q][2], x2, a0);
+                a1 = __fma_rn(-b[q][3], x0, a1);
+                a1 = __fma_rn(-b[q][4], x1, a1);
+                a1 = __fma_rn(-b[q][5], x2, a1);
+                a2 = __fma_rn(-b[q][6], x0, a2);
+                a2 = __fma_rn(-b[q][7], x1, a2);
+                a2 = __fma_rn(-b[q][8], x2, a2);
+            }
+        }
+        pre = pq;
     }
     vec[3 * i] = a0;
     vec[3 * i + 1] = a1;
@@ -210,13 +234,14 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         __threadfence_block();
         *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
     }
+    }
 }
 
 // Scalar CSR rows: the same record walk with 1x1 blocks --
 // one value plane per k, one Dinv plane, one FMA chain per row
 // (lower: acc = r_i, fma(-l_ij, z_j, acc); upper: acc = dinv_i * z_i,
 // fma(-u_ij, x_j, acc); blocks ascending).
-template <bool SPIN, class Rd>
+template <bool SPIN, bool GEN, class Rd>
 __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
@@ -225,7 +250,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
-    if (K <= 3) {
+    if (!GEN || K <= 3) {
         const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
         const uint32_t i = d.x & 0xffffu;
         const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
@@ -260,6 +285,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
         }
         return;
     }
+    if constexpr (GEN) {
     const uint32_t dw = ddi::rec_dw(K);
     const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * t);
     double a;
@@ -271,29 +297,45 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
         a = vec[i];
     }
     uint32_t pre = 0;
-    for (uint32_t k = 0; k < K; ++k) {
-        const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
-        if ((uint32_t)t >= ck) break;
-        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k));
-        const double b = rd.template ld<double>(off_val + 8u * (pre + t));
-        if (SPIN) spin_until(flags, j, ep);
-        a = __fma_rn(-b, vec[j], a);
-        pre += ck;
+    for (uint32_t k0 = 0; k0 < K; k0 += 4) {  // groups of four, loads first (see process_record3)
+        uint32_t ck[4], j[4];
+        double b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ck[q] = k0 + q < K ? rd.template ld<uint16_t>(16u + 2u * (k0 + q)) : 0u;
+        if ((uint32_t)t >= ck[0]) break;
+        uint32_t pq = pre;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((uint32_t)t < ck[q]) {
+                j[q] = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k0 + q));
+                b[q] = rd.template ld<double>(off_val + 8u * (pq + t));
+            }
+            pq += ck[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((uint32_t)t < ck[q]) {
+                if (SPIN) spin_until(flags, j[q], ep);
+                a = __fma_rn(-b[q], vec[j[q]], a);
+            }
+        }
+        pre = pq;
     }
     vec[i] = a;
     if (SPIN) {
         __threadfence_block();
         *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
     }
+    }
 }
 
-template <int BS, bool SPIN, class Rd>
+template <int BS, bool SPIN, bool GEN, class Rd>
 __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     if constexpr (BS == 3)
-        process_record3<SPIN>(rd, h, c8, t, vec, flags, ep);
+        process_record3<SPIN, GEN>(rd, h, c8, t, vec, flags, ep);
     else
-        process_record1<SPIN>(rd, h, c8, t, vec, flags, ep);
+        process_record1<SPIN, GEN>(rd, h, c8, t, vec, flags, ep);
 }
 
 __device__ __forceinline__ RecHdr hdr_from(uint4 q) {
@@ -315,7 +357,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // Ablation: level-set sweep reading the records straight from global memory;
 // only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
 // keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
-template <int BS>
+template <int BS, bool GEN>
 __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
@@ -352,7 +394,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
             // L level 0 carries no blocks (z_i = r_i in place): no work, no barrier
             const bool skip = !(h.flags & ddi::REC_UPPER) && h.K == 0 && !last;
             if (!skip) {
-                process_record<BS, false>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
+                process_record<BS, false, GEN>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
                 __syncthreads();
             }
             ro += h.bytes;
@@ -373,7 +415,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 //   barriers count NW arrivals).
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
 //   the streaming ceiling of the ring.
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, bool GEN>
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
@@ -509,9 +551,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             const uint32_t ep_set = upper ? ep : ep - 1;
             if (mode == 1 || skip) {
             } else if (pos + h.bytes <= RING) {
-                process_record<BS, SPIN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN, GEN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
             } else {
-                process_record<BS, SPIN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN, GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
             }
             ro += h.bytes;
             if (SPIN) {
@@ -538,9 +580,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
 // ------------------------------------------------------------ host side
 using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int);
 
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, bool GEN>
 static RingFn ring_fn() {
-    return k_apply_ring<BS, RING, CH, SPIN>;
+    return k_apply_ring<BS, RING, CH, SPIN, GEN>;
 }
 
 // ring chunk = RING / 4: every chunk costs the consumers one mbarrier
@@ -548,32 +590,37 @@ static RingFn ring_fn() {
 // thread one arrive, so few large chunks win (measured at config 3: 16 KB
 // chunks 434 us, 8 KB 444 us, 4 KB 485 us); a chunk plus the largest record
 // must still fit the ring (apply_prepare checks)
-template <int BS>
-static RingFn pick_ring_bs(int ring, bool spin) {
+template <int BS, bool GEN>
+static RingFn pick_ring_bg(int ring, bool spin) {
     if (!spin) {
         switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 32768, false>();
-            case 65536: return ring_fn<BS, 65536, 16384, false>();
-            case 32768: return ring_fn<BS, 32768, 8192, false>();
-            case 16384: return ring_fn<BS, 16384, 4096, false>();
+            case 131072: return ring_fn<BS, 131072, 32768, false, GEN>();
+            case 65536: return ring_fn<BS, 65536, 16384, false, GEN>();
+            case 32768: return ring_fn<BS, 32768, 8192, false, GEN>();
+            case 16384: return ring_fn<BS, 16384, 4096, false, GEN>();
         }
     } else {
         switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 32768, true>();
-            case 65536: return ring_fn<BS, 65536, 16384, true>();
-            case 32768: return ring_fn<BS, 32768, 8192, true>();
-            case 16384: return ring_fn<BS, 16384, 4096, true>();
+            case 131072: return ring_fn<BS, 131072, 32768, true, GEN>();
+            case 65536: return ring_fn<BS, 65536, 16384, true, GEN>();
+            case 32768: return ring_fn<BS, 32768, 8192, true, GEN>();
+            case 16384: return ring_fn<BS, 16384, 4096, true, GEN>();
         }
     }
     return nullptr;
 }
 
-static RingFn pick_ring(int bs, int ring, bool spin) {
-    return bs == 1 ? pick_ring_bs<1>(ring, spin) : pick_ring_bs<3>(ring, spin);
+// gen: the slab has rows with more than 3 blocks in a triangle (general-K path)
+static RingFn pick_ring(int bs, int ring, bool spin, bool gen) {
+    if (bs == 1) return gen ? pick_ring_bg<1, true>(ring, spin) : pick_ring_bg<1, false>(ring, spin);
+    return gen ? pick_ring_bg<3, true>(ring, spin) : pick_ring_bg<3, false>(ring, spin);
 }
 
 using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *);
-static DirectFn pick_direct(int bs) { return bs == 1 ? k_apply_direct<1> : k_apply_direct<3>; }
+static DirectFn pick_direct(int bs, bool gen) {
+    if (bs == 1) return gen ? k_apply_direct<1, true> : k_apply_direct<1, false>;
+    return gen ? k_apply_direct<3, true> : k_apply_direct<3, false>;
+}
 
 static int ring_chunk(int ring) { return ring / 4; }
 
@@ -607,6 +654,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     const int smem_sm = (int)prop.sharedMemPerMultiprocessor;    // 233472 on B200
     const int nsl = ctx->sub_last - ctx->sub_first;
     const int bs = ctx->bs;
+    const bool gen = ctx->kmax > 3;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
     const int flag_bytes = ((4 * ctx->max_P + 127) / 128) * 128;  // sync-free ready flags, 4 B per row
     const int tc = bs == 1 ? TCB<1> : TCB<3>;
@@ -623,7 +671,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         // the attribute is per function and shared by every context: set the maximum
-        allow_max_smem(pick_direct(bs), smem_max);
+        allow_max_smem(pick_direct(bs, gen), smem_max);
     }
     // ---- ring variants: largest ring that fits with the vector; override via DD_RING_KB
     // Ring choice: the consumer sweep is latency-bound, so maximise resident
@@ -638,9 +686,9 @@ dd_status apply_prepare(dd_ctx *ctx) {
             const int nst = rc / ring_chunk(rc);
             const int sm = vec_bytes + rc + 16 * nst + (spin ? flag_bytes : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
-            allow_max_smem(pick_ring(bs, rc, spin), smem_max);
+            allow_max_smem(pick_ring(bs, rc, spin, gen), smem_max);
             int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin), tc + 32, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin, gen), tc + 32, sm);
             if (occ > best_occ) {
                 best_occ = occ;
                 best_ring = rc;
@@ -680,27 +728,28 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     const int nsl = ctx->sub_last - ctx->sub_first;
     if (nsl == 0) return DD_OK;
     const int bs = ctx->bs;
+    const bool gen = ctx->kmax > 3;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
     if (variant == 0) variant = DD_LEVELSET;
     static const int mode = env_int("DD_APPLY_MODE", 0);  // 1: streaming ceiling (measurement only)
     if (variant == DD_DIRECT) {
         static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
         const LaunchCfg &c = ctx->cfg_direct;
-        pick_direct(bs)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf,
+        pick_direct(bs, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf,
                                                            skip);
     } else if (variant == DD_LEVELSET) {
         const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, r, z, vec_bytes, mode, skip, 0);
     } else if (variant == DD_UNFUSED) {
         // ablation of the fusion (sec. 4.4): the L sweep and the D+U
         // sweep as two launches of the same kernel; the vector makes a round
         // trip through HBM in between (z holds L^-1 r after the first)
         const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, r, z, vec_bytes, mode, skip, 1);
         ++ctx->n_launches;
-        pick_ring(bs, c.ring, false)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                    nsl, z, z, vec_bytes, mode, skip, 2);
     } else if (variant == DD_SPINLOOP) {
         if (!(ctx->variants & DD_SPINLOOP)) {
@@ -708,7 +757,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
             return DD_E_SUBDOMAIN_TOO_LARGE;
         }
         const LaunchCfg &c = ctx->cfg_spin;
-        pick_ring(bs, c.ring, true)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
+        pick_ring(bs, c.ring, true, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
                                                                   nsl, r, z, vec_bytes, mode, skip, 0);
     } else {
         set_error("dd_apply: unknown variant");

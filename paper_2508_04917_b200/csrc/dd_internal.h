@@ -104,6 +104,7 @@ struct dd_ctx {
     int32_t sub_first = 0, sub_last = 0;  // local subdomains [first, last)
     int64_t row_first = 0, n_local = 0;   // reordered global rows
     int32_t max_P = 0;
+    int32_t kmax = 0;  // most blocks of a row in one factor triangle (> 3: general-K kernels)
     // factors of the local rows (local numbering)
     std::vector<int64_t> Lrp, Urp;
     std::vector<int32_t> Lci, Uci;

@@ -690,6 +690,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     int32_t Kmax = 0;
     for (int64_t li = 0; li < nl; ++li)
         Kmax = std::max<int32_t>(Kmax, (int32_t)std::max(ctx->Lrp[li + 1] - ctx->Lrp[li], ctx->Urp[li + 1] - ctx->Urp[li]));
+    ctx->kmax = Kmax;
     {
         const int64_t vec = (8 * bs * (int64_t)ctx->max_P + 127) / 128 * 128;
         const int64_t avail = 232448 - vec - 2 * (int64_t)ctx->max_P - 1024;
