@@ -85,7 +85,9 @@ __device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, ui
 // Every load (descriptor, values, Dinv) is addressed from (t, cnt) alone, so
 // all are in flight before the first FMA; the only dependent step is the
 // gather of vec[3j..3j+2] through the descriptor's column ids.
-template <bool SPIN, bool GEN, class Rd>
+// GEN: 0 = rows with at most 3 blocks per triangle only (7-point), 1 = general
+// K with blocks in groups of three, 2 = general K one block per step
+template <bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
@@ -94,7 +96,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
-    if (!GEN || K <= 3) {
+    if (GEN == 0 || K <= 3) {
         const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
         const uint32_t i = d.x & 0xffffu;
         const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
@@ -184,6 +186,31 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         a1 = vec[3 * i + 1];
         a2 = vec[3 * i + 2];
     }
+    if constexpr (GEN == 2) {
+        // one block per step (fewer registers; the direct variant keeps this form)
+    uint32_t pre = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t ck = rd.template ld<uint16_t>(16u + 2u * k);
+        if ((uint32_t)t >= ck) break;
+        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * t + 2u * (1u + k));
+        const uint32_t vb = off_val + 72u * pre + 8u * t;
+        double b[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + 8u * ck * v);
+        if (SPIN) spin_until(flags, j, ep);
+        const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+        a0 = __fma_rn(-b[0], x0, a0);
+        a0 = __fma_rn(-b[1], x1, a0);
+        a0 = __fma_rn(-b[2], x2, a0);
+        a1 = __fma_rn(-b[3], x0, a1);
+        a1 = __fma_rn(-b[4], x1, a1);
+        a1 = __fma_rn(-b[5], x2, a1);
+        a2 = __fma_rn(-b[6], x0, a2);
+        a2 = __fma_rn(-b[7], x1, a2);
+        a2 = __fma_rn(-b[8], x2, a2);
+        pre += ck;
+    }
+    } else {
     // blocks in groups of three: a group's counts, columns and values are all
     // loaded before its FMAs (as in the K <= 3 path), so a row with K blocks
     // has ceil(K/3) dependent load rounds instead of K
@@ -227,6 +254,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         }
         pre = pq;
     }
+    }
     vec[3 * i] = a0;
     vec[3 * i + 1] = a1;
     vec[3 * i + 2] = a2;
@@ -241,7 +269,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
 // one value plane per k, one Dinv plane, one FMA chain per row
 // (lower: acc = r_i, fma(-l_ij, z_j, acc); upper: acc = dinv_i * z_i,
 // fma(-u_ij, x_j, acc); blocks ascending).
-template <bool SPIN, bool GEN, class Rd>
+template <bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     const uint32_t w = h.w, K = h.K;
@@ -250,7 +278,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
-    if (!GEN || K <= 3) {
+    if (GEN == 0 || K <= 3) {
         const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
         const uint32_t i = d.x & 0xffffu;
         const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
@@ -329,7 +357,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     }
 }
 
-template <int BS, bool SPIN, bool GEN, class Rd>
+template <int BS, bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
     if constexpr (BS == 3)
@@ -357,7 +385,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // Ablation: level-set sweep reading the records straight from global memory;
 // only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
 // keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
-template <int BS, bool GEN>
+template <int BS, int GEN>
 __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
@@ -415,7 +443,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 //   barriers count NW arrivals).
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
 //   the streaming ceiling of the ring.
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN, bool GEN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
@@ -580,7 +608,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
 // ------------------------------------------------------------ host side
 using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int);
 
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN, bool GEN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
 static RingFn ring_fn() {
     return k_apply_ring<BS, RING, CH, SPIN, GEN>;
 }
@@ -590,7 +618,7 @@ static RingFn ring_fn() {
 // thread one arrive, so few large chunks win (measured at config 3: 16 KB
 // chunks 434 us, 8 KB 444 us, 4 KB 485 us); a chunk plus the largest record
 // must still fit the ring (apply_prepare checks)
-template <int BS, bool GEN>
+template <int BS, int GEN>
 static RingFn pick_ring_bg(int ring, bool spin) {
     if (!spin) {
         switch (ring) {
@@ -612,14 +640,17 @@ static RingFn pick_ring_bg(int ring, bool spin) {
 
 // gen: the slab has rows with more than 3 blocks in a triangle (general-K path)
 static RingFn pick_ring(int bs, int ring, bool spin, bool gen) {
-    if (bs == 1) return gen ? pick_ring_bg<1, true>(ring, spin) : pick_ring_bg<1, false>(ring, spin);
-    return gen ? pick_ring_bg<3, true>(ring, spin) : pick_ring_bg<3, false>(ring, spin);
+    if (bs == 1) return gen ? pick_ring_bg<1, 1>(ring, spin) : pick_ring_bg<1, 0>(ring, spin);
+    return gen ? pick_ring_bg<3, 1>(ring, spin) : pick_ring_bg<3, 0>(ring, spin);
 }
 
 using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *);
 static DirectFn pick_direct(int bs, bool gen) {
-    if (bs == 1) return gen ? k_apply_direct<1, true> : k_apply_direct<1, false>;
-    return gen ? k_apply_direct<3, true> : k_apply_direct<3, false>;
+    // the 3x3 direct ablation keeps the one-block-per-step general path compiled
+    // in (GEN 2): the compiler schedules its global loads better that way
+    // (458 vs 534 us at config 3)
+    if (bs == 1) return gen ? k_apply_direct<1, 1> : k_apply_direct<1, 0>;
+    return gen ? k_apply_direct<3, 1> : k_apply_direct<3, 2>;
 }
 
 static int ring_chunk(int ring) { return ring / 4; }
