@@ -69,6 +69,15 @@ struct Workspace {
     std::vector<int64_t> send_off;  // [world + 1]
     // DD_COMM_LOCAL: "my send data is ready" / "I have copied my peers' data"
     cudaEvent_t xev_ready = nullptr, xev_done = nullptr;
+    // fused halo (world > 1): the solver's applies write the rows peers need
+    // straight from shared memory (send buffer, or DD_COMM_LOCAL the peer's
+    // ghost block); xev_app: "my fused apply has written", xev_free: "my SpMV
+    // no longer reads my ghost block"
+    bool halo_fuse = false;
+    ddi::HaloOut hout;
+    int32_t *d_hptr = nullptr, *d_hrow = nullptr;
+    double **d_hdst = nullptr;
+    cudaEvent_t xev_app = nullptr, xev_free = nullptr;
     // CUDA-graph solve loop (one executable graph per solution vector)
     cudaStream_t cap = nullptr;
     cudaGraph_t graph = nullptr;
@@ -295,7 +304,10 @@ void local_leave(dd_ctx *ctx) {
     // no live peer may still be copying from this rank's buffers: its copies
     // precede its last xev_done record
     for (dd_ctx *q : G->members)
-        if (q && q != ctx && q->dev_ws && ws_of(q)->xev_done) cudaEventSynchronize(ws_of(q)->xev_done);
+        if (q && q != ctx && q->dev_ws) {
+            if (ws_of(q)->xev_done) cudaEventSynchronize(ws_of(q)->xev_done);
+            if (ws_of(q)->xev_app) cudaEventSynchronize(ws_of(q)->xev_app);  // fused writes into our ghost block
+        }
     G->members[ctx->rank] = nullptr;
     ctx->group = nullptr;
     if (--G->refs == 0) {
@@ -315,6 +327,71 @@ void local_leave(dd_ctx *ctx) {
             return DD_E_NCCL;                                                      \
         }                                                                          \
     } while (0)
+
+// Fused halo lists: for every local subdomain, the rows that
+// peers need (send_rows, ascending per peer) and where they go -- this rank's
+// NCCL send buffer, or with DD_COMM_LOCAL the consuming peer's ghost block
+// directly (peer memory: every member on one device or peer-accessible
+// devices; otherwise the unfused gather + copy is kept). DD_HALO_FUSE=0
+// disables it (A/B measurements and tests).
+dd_status halo_out_build(dd_ctx *ctx) {
+    Workspace *ws = ws_of(ctx);
+    const char *env = getenv("DD_HALO_FUSE");
+    bool fuse = !env || atoi(env) != 0;
+    if (fuse && ctx->comm == DD_COMM_LOCAL) {
+        for (dd_ctx *a : group_of(ctx)->members)
+            for (dd_ctx *b : group_of(ctx)->members) {
+                int can = 1;
+                if (a->device != b->device) cudaDeviceCanAccessPeer(&can, a->device, b->device);
+                if (!can) fuse = false;
+            }
+    }
+    ws->halo_fuse = fuse;
+    if (!fuse) return DD_OK;
+    const int nsl = ctx->sub_last - ctx->sub_first;
+    struct Ent {
+        int32_t sub, row;
+        double *dst;
+    };
+    std::vector<Ent> ents;
+    for (int q = 0; q < ctx->world; ++q) {
+        if (q == ctx->rank || q >= (int)ctx->send_rows.size()) continue;
+        const auto &rows = ctx->send_rows[q];
+        double *base;
+        if (ctx->comm == DD_COMM_LOCAL) {
+            dd_ctx *peer = group_of(ctx)->members[q];
+            base = ws_of(peer)->xg + ctx->bs * peer->recv_off[ctx->rank];
+        } else {
+            base = ws->sendbuf + ctx->bs * ws->send_off[q];
+        }
+        for (size_t p = 0; p < rows.size(); ++p) {
+            const int64_t g = ctx->row_first + rows[p];  // reordered global row
+            const int32_t s = (int32_t)(std::upper_bound(ctx->sub_ptr.begin() + ctx->sub_first,
+                                                         ctx->sub_ptr.begin() + ctx->sub_last + 1, g) -
+                                        ctx->sub_ptr.begin()) - 1;
+            ents.push_back({s - ctx->sub_first, (int32_t)(g - ctx->sub_ptr[s]), base + ctx->bs * (int64_t)p});
+        }
+    }
+    std::stable_sort(ents.begin(), ents.end(), [](const Ent &a, const Ent &b) { return a.sub < b.sub; });
+    std::vector<int32_t> ptr(nsl + 1, 0), row(ents.size());
+    std::vector<double *> dst(ents.size());
+    for (size_t e = 0; e < ents.size(); ++e) {
+        ++ptr[ents[e].sub + 1];
+        row[e] = ents[e].row;
+        dst[e] = ents[e].dst;
+    }
+    for (int s = 0; s < nsl; ++s) ptr[s + 1] += ptr[s];
+    TRY(dmalloc(&ws->d_hptr, ptr.size()));
+    TRY(dmalloc(&ws->d_hrow, std::max<size_t>(1, row.size())));
+    TRY(dmalloc(&ws->d_hdst, std::max<size_t>(1, dst.size())));
+    CK(cudaMemcpy(ws->d_hptr, ptr.data(), ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (!row.empty()) {
+        CK(cudaMemcpy(ws->d_hrow, row.data(), row.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ws->d_hdst, dst.data(), dst.size() * sizeof(double *), cudaMemcpyHostToDevice));
+    }
+    ws->hout = ddi::HaloOut{ws->d_hptr, ws->d_hrow, ws->d_hdst};
+    return DD_OK;
+}
 
 dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     const double t0 = now_ms();
@@ -428,8 +505,11 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     if (ctx->world > 1 && ctx->comm == DD_COMM_LOCAL) {
         CK(cudaEventCreateWithFlags(&ws->xev_ready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ws->xev_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ws->xev_app, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ws->xev_free, cudaEventDisableTiming));
         TRY(local_join(ctx, nccl_id));
     }
+    if (ctx->world > 1) TRY(halo_out_build(ctx));
     ctx->setup_ms[5] = now_ms() - t0;
     return DD_OK;
 }
@@ -495,13 +575,26 @@ dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaS
     return DD_OK;
 }
 
-// halo exchange of the SpMV input x (local rows) into ws->xg
-dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
+// halo exchange of the SpMV input x (local rows) into ws->xg. packed: x was
+// produced by a fused-halo apply (apply_halo), which already wrote the rows
+// peers need (NCCL: into the send buffer; DD_COMM_LOCAL: into the peers'
+// ghost blocks -- only the ordering remains)
+dd_status halo(dd_ctx *c, const double *x, cudaStream_t st, bool packed) {
     if (c->world <= 1) return DD_OK;
     Workspace *ws = ws_of(c);
+    packed = packed && ws->halo_fuse;
     const int64_t ns = ws->send_off[c->world];
-    if (ns) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
-    if (c->comm == DD_COMM_LOCAL) return local_halo(c, st);
+    if (ns && !packed) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
+    if (c->comm == DD_COMM_LOCAL) {
+        if (!packed) return local_halo(c, st);
+        // every producer has recorded xev_app after its fused apply
+        LocalGroup *G = group_of(c);
+        RENDEZVOUS(G);
+        for (int q = 0; q < c->world; ++q)
+            if (q != c->rank && c->recv_off[q + 1] > c->recv_off[q])
+                CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_app, 0));
+        return DD_OK;
+    }
     auto comm = reinterpret_cast<ncclComm_t>(c->nccl);
     NK(ncclGroupStart());
     for (int q = 0; q < c->world; ++q) {
@@ -516,9 +609,33 @@ dd_status halo(dd_ctx *c, const double *x, cudaStream_t st) {
 }
 
 dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, const ddk::RedArgs &ra,
-                    cudaStream_t st) {
-    TRY(halo(c, x, st));
+                    cudaStream_t st, bool packed = false) {
+    TRY(halo(c, x, st, packed));
     ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, ra, st);
+    // DD_COMM_LOCAL with the fused halo: peers' next fused applies write this
+    // rank's ghost block only after this SpMV has read it
+    if (c->world > 1 && c->comm == DD_COMM_LOCAL && ws_of(c)->halo_fuse) CK(cudaEventRecord(ws_of(c)->xev_free, st));
+    return DD_OK;
+}
+
+// The solver's apply r -> z with the fused halo epilogue (world > 1): the rows
+// peers read in the following SpMV leave from shared memory. DD_COMM_LOCAL:
+// the writes land in the peers' ghost blocks, so they wait until each
+// consumer's previous SpMV has read its block (xev_free), and xev_app tells
+// the consumers the rows are there.
+dd_status apply_halo(dd_ctx *c, const double *r, double *z, cudaStream_t st, const int *skip) {
+    Workspace *ws = ws_of(c);
+    const bool fuse = c->world > 1 && ws->halo_fuse;
+    const bool local = fuse && c->comm == DD_COMM_LOCAL;
+    if (local) {
+        LocalGroup *G = group_of(c);
+        RENDEZVOUS(G);
+        for (int q = 0; q < c->world; ++q)
+            if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
+                CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_free, 0));
+    }
+    TRY(apply_launch(c, DD_LEVELSET, r, z, reinterpret_cast<void *>(st), skip, fuse ? &ws->hout : nullptr));
+    if (local) CK(cudaEventRecord(ws->xev_app, st));
     return DD_OK;
 }
 
@@ -729,9 +846,12 @@ void dd_destroy(dd_ctx *c) {
             if (ws->cap) cudaStreamDestroy(ws->cap);
             for (auto e : ws->ev)
                 if (e) cudaEventDestroy(e);
-            for (auto e : {ws->xev_ready, ws->xev_done})
+            for (auto e : {ws->xev_ready, ws->xev_done, ws->xev_app, ws->xev_free})
                 if (e) cudaEventDestroy(e);
             cudaFree(ws->d_send_idx);
+            cudaFree(ws->d_hptr);
+            cudaFree(ws->d_hrow);
+            cudaFree(ws->d_hdst);
             cudaFreeHost(ws->h_sc);
             delete ws;
         }
@@ -778,14 +898,13 @@ dd_status dd_spmv(dd_ctx *c, const double *x, double *y, void *stream) {
 dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaStream_t st) {
     Workspace *ws = ws_of(c);
     const int64_t m = ws->m;
-    void *stream = reinterpret_cast<void *>(st);
     ra.k = k;
     TRY(timed(c, PK_BLAS, k, st, [&] {
         ddk::launch_update_p(c, m, k < 0 ? -1 : (k == 1), ws->r, ws->v, ws->p, ws->sc, ws->ctl, st);
         return DD_OK;
     }));
-    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->p, ws->ph, stream, ws->ctl); }));
-    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st); }));
+    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->p, ws->ph, st, ws->ctl); }));
+    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st, true); }));
     TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
     TRY(timed(c, PK_BLAS, k, st, [&] {
         ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
@@ -793,8 +912,8 @@ dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaSt
     }));
     TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
     ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
-    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_launch(c, DD_LEVELSET, ws->s, ws->sh, stream, ws->ctl); }));
-    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st); }));
+    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->s, ws->sh, st, ws->ctl); }));
+    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st, true); }));
     TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
     TRY(timed(c, PK_BLAS, k, st, [&] {
         ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);

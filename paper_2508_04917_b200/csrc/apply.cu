@@ -447,7 +447,7 @@ template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
-                 int phase) {
+                 int phase, ddi::HaloOut ho) {
     // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
@@ -550,7 +550,10 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             ensure(gbase + c);
             const uint32_t qlo = c == 0 ? 0u : (c * CH - shift) / 8u;
             const uint32_t qhi = min(nd, ((c + 1) * CH - shift) / 8u);
-            for (uint32_t q = qlo + t; q < qhi; q += TC)
+            // thread t fills the entries q = t (mod TC) -- the ones it stored
+            // to z for the previous subdomain -- so no barrier is needed
+            // between that store and this fill
+            for (uint32_t q = qlo + (t + TC - qlo % TC) % TC; q < qhi; q += TC)
                 vec[q] = *reinterpret_cast<const double *>(ring + ((abs0 + shift + 8u * q) & (RING - 1u)));
             if ((c + 1) % (NST / 2) == 0 && c + 1 < nrc) {
                 named_bar_sync(1, TC);
@@ -601,12 +604,29 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         }
         double *zs = z + BS * (int64_t)si.row0;
         for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[q];
+        // fused halo: the subdomain's rows that peers read in
+        // the next SpMV go straight from shared memory to their destination
+        // (send buffer or the peer's ghost block); the CTA then waits before
+        // the next subdomain overwrites the vector
+        if (ho.ptr && phase != 1) {
+            const int e0 = ho.ptr[s], e1 = ho.ptr[s + 1];
+            if (e1 > e0) {
+                for (int e = e0 + t; e < e1; e += TC) {
+                    const int li = ho.row[e];
+                    double *d = ho.dst[e];
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) d[c] = vec[BS * li + c];
+                }
+                named_bar_sync(1, TC);
+            }
+        }
         gbase += nch;
     }
 }
 
 // ------------------------------------------------------------ host side
-using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int);
+using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int,
+                        ddi::HaloOut);
 
 template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
 static RingFn ring_fn() {
@@ -682,7 +702,6 @@ dd_status apply_prepare(dd_ctx *ctx) {
     }
     ctx->num_sms = prop.multiProcessorCount;
     const int smem_max = (int)prop.sharedMemPerBlockOptin;       // 232448 on B200
-    const int smem_sm = (int)prop.sharedMemPerMultiprocessor;    // 233472 on B200
     const int nsl = ctx->sub_last - ctx->sub_first;
     const int bs = ctx->bs;
     const bool gen = ctx->kmax > 3;
@@ -753,7 +772,8 @@ dd_status apply_prepare(dd_ctx *ctx) {
     return cudaGetLastError() == cudaSuccess ? DD_OK : DD_E_CUDA;
 }
 
-dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip) {
+dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip,
+                       const HaloOut *halo) {
     using namespace ddk;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int nsl = ctx->sub_last - ctx->sub_first;
@@ -762,6 +782,11 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     const bool gen = ctx->kmax > 3;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
     if (variant == 0) variant = DD_LEVELSET;
+    const HaloOut ho = halo ? *halo : HaloOut{};
+    if (ho.ptr && variant == DD_DIRECT) {
+        set_error("dd_apply: the fused halo epilogue is a ring-kernel feature");
+        return DD_E_INVALID_ARG;
+    }
     static const int mode = env_int("DD_APPLY_MODE", 0);  // 1: streaming ceiling (measurement only)
     if (variant == DD_DIRECT) {
         static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
@@ -771,17 +796,17 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     } else if (variant == DD_LEVELSET) {
         const LaunchCfg &c = ctx->cfg_lvl;
         pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode, skip, 0);
+                                                                   nsl, r, z, vec_bytes, mode, skip, 0, ho);
     } else if (variant == DD_UNFUSED) {
         // ablation of the fusion (sec. 4.4): the L sweep and the D+U
         // sweep as two launches of the same kernel; the vector makes a round
         // trip through HBM in between (z holds L^-1 r after the first)
         const LaunchCfg &c = ctx->cfg_lvl;
         pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode, skip, 1);
+                                                                   nsl, r, z, vec_bytes, mode, skip, 1, ho);
         ++ctx->n_launches;
         pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, z, z, vec_bytes, mode, skip, 2);
+                                                                   nsl, z, z, vec_bytes, mode, skip, 2, ho);
     } else if (variant == DD_SPINLOOP) {
         if (!(ctx->variants & DD_SPINLOOP)) {
             set_error("dd_apply: sync-free variant unavailable (its ready flags do not fit shared memory)");
@@ -789,7 +814,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
         }
         const LaunchCfg &c = ctx->cfg_spin;
         pick_ring(bs, c.ring, true, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                  nsl, r, z, vec_bytes, mode, skip, 0);
+                                                                  nsl, r, z, vec_bytes, mode, skip, 0, ho);
     } else {
         set_error("dd_apply: unknown variant");
         return DD_E_INVALID_ARG;

@@ -81,6 +81,16 @@ struct Slab {
     SubInfo *d_info = nullptr;
 };
 
+// Halo rows written by the apply's epilogue (world > 1): for
+// local subdomain s, entries [ptr[s], ptr[s+1]) name a row of the subdomain
+// (row[e], 0-based inside it) and the address its bs values go to -- the
+// rank's NCCL send buffer, or (DD_COMM_LOCAL) the consuming peer's ghost block.
+struct HaloOut {
+    const int32_t *ptr = nullptr;  // [n_local_sub + 1]; nullptr = no halo output
+    const int32_t *row = nullptr;  // [E]
+    double *const *dst = nullptr;  // [E]
+};
+
 struct LaunchCfg {
     int grid = 0, threads = 0, smem = 0, ring = 0, consumers = 0;
 };
@@ -165,7 +175,7 @@ double now_ms();
 
 // kernels (apply.cu / spmv.cu / blas1.cu)
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream,
-                       const int *skip = nullptr);
+                       const int *skip = nullptr, const HaloOut *halo = nullptr);
 dd_status apply_prepare(dd_ctx *ctx);  // choose launch cfgs, set smem attributes
 void spmv_launch(const dd_ctx *ctx, const double *x, double *y, void *stream);
 }  // namespace ddi
