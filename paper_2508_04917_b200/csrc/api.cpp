@@ -74,6 +74,7 @@ struct Workspace {
     // ghost block); xev_app: "my fused apply has written", xev_free: "my SpMV
     // no longer reads my ghost block"
     bool halo_fuse = false;
+    bool merge_ss = false;  // world > 1: s.s reduced with (t.s, t.t), see enqueue_iteration
     ddi::HaloOut hout;
     int32_t *d_hptr = nullptr, *d_hrow = nullptr;
     double **d_hdst = nullptr;
@@ -477,8 +478,14 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     CK(cudaMalloc(&ws->partials, ddk::partials_bytes(ctx)));
     TRY(dmalloc(&ws->counter, 4));
     CK(cudaMemset(ws->counter, 0, 4 * sizeof(unsigned int)));
-    TRY(dmalloc(&ws->loc, 4));
-    TRY(dmalloc(&ws->gathered, 4 * (size_t)std::max(1, ctx->world)));
+    TRY(dmalloc(&ws->loc, 6));
+    TRY(dmalloc(&ws->gathered, 6 * (size_t)std::max(1, ctx->world)));
+    {
+        // world > 1: ||s||^2 joins the (t.s, t.t) collective -- three
+        // reduction points per iteration instead of four (DD_MERGE_SS=0: four)
+        const char *e = getenv("DD_MERGE_SS");
+        ws->merge_ss = ctx->world > 1 && (!e || atoi(e) != 0);
+    }
     CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_sc), ddk::S_COUNT * sizeof(double)));
     TRY(dmalloc(&ws->ctl, 8));
     CK(cudaMemset(ws->ctl, 0, 8 * sizeof(int)));
@@ -517,7 +524,7 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
 ddk::RedArgs red_args(dd_ctx *c) {
     Workspace *ws = ws_of(c);
     return ddk::RedArgs{reinterpret_cast<ddk::DD *>(ws->partials), ws->counter, ws->sc, ws->loc,
-                        c->world <= 1 ? 1 : 0, nullptr, nullptr, 0};
+                        c->world <= 1 ? 1 : 0, nullptr, nullptr, 0, 0};
 }
 
 // world > 1: all-gather the rank-local (s, c) pairs and finalize in rank order.
@@ -906,15 +913,28 @@ dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaSt
     TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->p, ws->ph, st, ws->ctl); }));
     TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st, true); }));
     TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
+    // world > 1 (merge_ss): the rank-local s.s waits in loc[4..5] and joins
+    // the (t.s, t.t) collective; the half-step test is then taken after the
+    // second apply and SpMV, which are wasted only in a solve's last
+    // iteration -- the iterates are unchanged (tested bitwise)
+    ddk::RedArgs ra_s = ra;
+    if (ws->merge_ss) ra_s.slot = 2;
     TRY(timed(c, PK_BLAS, k, st, [&] {
-        ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra, st);
+        ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra_s, st);
         return DD_OK;
     }));
-    TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
-    ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
+    if (!ws->merge_ss) {
+        TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
+        ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
+    }
     TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->s, ws->sh, st, ws->ctl); }));
     TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st, true); }));
-    TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
+    if (ws->merge_ss) {
+        TRY(reduce_across(c, 3, ddk::FIN_SS_OMEGA, ra, st));
+        ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
+    } else {
+        TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
+    }
     TRY(timed(c, PK_BLAS, k, st, [&] {
         ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
         return DD_OK;

@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 }
 
 // -------------------------------------------------------------------- ring
+#ifndef DD_PF_AHEAD
+#define DD_PF_AHEAD 0
+#endif
 // SPIN = false (level set, Alg. 6): every consumer thread takes one row of
 //   each record; a named barrier separates records (levels).
 // SPIN = true  (sync-free, Alg. 4 with per-row ready flags): each warp walks
@@ -491,8 +494,34 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 const uint32_t nch = (total + CH - 1) / CH;
                 const uint8_t *rsrc = reinterpret_cast<const uint8_t *>(r) + rlo;
                 const uint8_t *fsrc = slab + si.stream_off + sec_lo;
+#if DD_PF_AHEAD
+                // experiment: L2 prefetch DD_PF_AHEAD bytes ahead of the ring fill
+                // position, into the CTA's next subdomain at the end of this one
+                auto pf_sub = [&](int ss, uint32_t a, uint32_t b) {
+                    const SubInfo sj = info[ss];
+                    const int64_t jlo = (8 * BS * (int64_t)sj.row0) & ~(int64_t)15;
+                    const int64_t jhi = (8 * BS * ((int64_t)sj.row0 + sj.nrows) + 15) & ~(int64_t)15;
+                    const uint32_t jrb = (uint32_t)(jhi - jlo);
+                    const uint32_t jtot = jrb + (uint32_t)sj.stream_bytes;
+                    b = min(b, jtot);
+                    if (a >= b) return;
+                    if (a < jrb) prefetch_l2(reinterpret_cast<const uint8_t *>(r) + jlo + a, min(b, jrb) - a);
+                    if (b > jrb) {
+                        const uint32_t q = max(a, jrb);
+                        prefetch_l2(slab + sj.stream_off + (q - jrb), b - q);
+                    }
+                };
+#endif
                 for (uint32_t c = 0; c < nch; ++c, ++g) {
                     const uint32_t st = g % NST;
+#if DD_PF_AHEAD
+                    if (phase == 0) {
+                        const uint32_t a = c * CH + DD_PF_AHEAD, b = a + CH;
+                        if (a < total) pf_sub(s, a, b);
+                        if (b > total && s + (int)gridDim.x < n_sub)
+                            pf_sub(s + gridDim.x, a > total ? a - total : 0u, b - total);
+                    }
+#endif
                     if (g >= NST) mbar_wait(&empty[st], ((g / NST) - 1u) & 1u);
                     const uint32_t lo = c * CH, hi = min(total, lo + CH);
                     mbar_arrive_expect_tx(&full[st], hi - lo);

@@ -210,8 +210,8 @@ __device__ __forceinline__ void deliver(const RedArgs &ra, int op, const DD (&ou
     } else {
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-            ra.loc[2 * q] = out[q].s;
-            ra.loc[2 * q + 1] = out[q].c;
+            ra.loc[2 * (ra.slot + q)] = out[q].s;
+            ra.loc[2 * (ra.slot + q) + 1] = out[q].c;
         }
     }
 }
@@ -459,11 +459,17 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, const double *__restri
 __global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, RedArgs ra, int op) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (op != FIN_INIT && op != FIN_RESID && stopped(ra.ctl)) return;
-    double out[2] = {0.0, 0.0};
+    double out[3] = {0.0, 0.0, 0.0};
     for (int q = 0; q < nv; ++q) {
         DD acc{0.0, 0.0};
         for (int rr = 0; rr < world; ++rr) acc = dd_plus(acc, DD{gathered[rr * 2 * nv + 2 * q], gathered[rr * 2 * nv + 2 * q + 1]});
         out[q] = acc.s + acc.c;
+    }
+    if (op == FIN_SS_OMEGA) {
+        // the half-step test comes first, as in Alg. 1; omega only if it failed
+        finalize(ra.sc, FIN_SS, out + 2, ra.ctl, ra.hist, ra.k);
+        if (stopped(ra.ctl)) return;
+        op = FIN_OMEGA;
     }
     finalize(ra.sc, op, out, ra.ctl, ra.hist, ra.k);
 }

@@ -28,7 +28,9 @@ enum : int {
     S_COUNT = 16
 };
 
-enum : int { FIN_INIT = 1, FIN_ALPHA, FIN_SS, FIN_OMEGA, FIN_RHO, FIN_RESID };
+enum : int { FIN_INIT = 1, FIN_ALPHA, FIN_SS, FIN_OMEGA, FIN_RHO, FIN_RESID,
+             FIN_SS_OMEGA  // world > 1: (t.s, t.t, s.s) in one collective; FIN_SS first, then FIN_OMEGA
+};
 
 // Device-side solver control (int ctl[8]): the finalizing last blocks decide
 // convergence / breakdown (R21, R25) and every iteration kernel returns at
@@ -58,6 +60,7 @@ struct RedArgs {
     int *ctl;               // solver control (nullptr: no control, e.g. plain SpMV)
     double *hist;           // residual history [2*max_iter+1] (device)
     int k;                  // iteration the launch belongs to (< 0: ctl[C_ITER], graph mode)
+    int slot;               // world > 1: first (s, c) pair of loc[] this reduction writes
 };
 
 // CUDA-graph BiCGSTAB (f4): the iteration body runs under a conditional WHILE

@@ -151,21 +151,23 @@ def test_local_world_bad_arguments():
 
 @pytest.mark.parametrize("name,world", [("laplace_24^3", 3), ("chunks_ragged_oddP", 2), ("spe10_small", 2),
                                         ("random_8sub", 4)])
-def test_fused_halo_equals_unfused(name, world, monkeypatch):
-    """the solver's applies write the rows peers read in the next
-    SpMV straight from shared memory into the peers' ghost blocks
-    (DD_COMM_LOCAL; NCCL: into the send buffer). Same solve, bitwise, as the
-    unfused gather kernel + copy (DD_HALO_FUSE=0), with two gather launches
-    fewer per iteration and rank."""
+def test_fused_halo_and_merged_reduction_equal_plain(name, world, monkeypatch):
+    """SURVEY 8(f4), world > 1. (a) Fused halo: the solver's applies write the
+    rows peers read in the next SpMV straight from shared memory into the
+    peers' ghost blocks (DD_COMM_LOCAL; NCCL: into the send buffer) instead of
+    a gather kernel + copy (DD_HALO_FUSE=0). (b) Merged reduction: s.s joins
+    the (t.s, t.t) collective, three reduction points per iteration instead
+    of four (DD_MERGE_SS=0). Every combination gives the same solve bitwise
+    (x, residual history, iterations), with fewer launches."""
     import torch
     gen, kw = CASES[name]
     rp, ci, v = gen()
     xs, b = manufactured_rhs(rp, ci, v)
     S = oracle.setup(rp, ci, v, **kw)
     b_re = b.reshape(-1, 3)[S["new_to_old"]].ravel()
-    out = {}
-    for fuse in ("0", "1"):
-        monkeypatch.setenv("DD_HALO_FUSE", fuse)
+    def solve(knobs, tol):
+        monkeypatch.setenv("DD_HALO_FUSE", knobs[0])
+        monkeypatch.setenv("DD_MERGE_SS", knobs[1])
         key = os.urandom(128)
 
         def rank_fn(rank, bar):
@@ -177,7 +179,7 @@ def test_fused_halo_equals_unfused(name, world, monkeypatch):
                 bl = torch.from_numpy(b_re[3 * f:3 * (f + n)].copy()).cuda()
                 x = torch.zeros_like(bl)
                 l0 = ctx.stats()["launches"]
-                rep = ctx.bicgstab(bl, x, tol=1e-8, max_iter=2000, hist=True, stream=st)
+                rep = ctx.bicgstab(bl, x, tol=tol, max_iter=2000, hist=True, stream=st)
                 launches = ctx.stats()["launches"] - l0
                 st.synchronize()
                 res = (x.cpu().numpy(), rep, launches)
@@ -185,11 +187,24 @@ def test_fused_halo_equals_unfused(name, world, monkeypatch):
                 ctx.destroy()
                 return res
 
-        out[fuse] = run_ranks(world, rank_fn)
-    for q in range(world):
-        x0, rep0, l0 = out["0"][q]
-        x1, rep1, l1 = out["1"][q]
-        assert rep0["iterations"] == rep1["iterations"] and rep1["converged"] == 1
-        assert np.array_equal(x0, x1), f"rank {q}: fused halo changed the solve"
-        assert np.array_equal(rep0["resid_hist"], rep1["resid_hist"])
-        assert l1 < l0, (q, l0, l1)
+        return run_ranks(world, rank_fn)
+
+    # a tolerance met first at a half step (so the merged path's deferred
+    # half-step test and x += alpha p_hat are exercised)
+    h = solve(("0", "0"), 1e-8)[0][1]["resid_hist"]
+    j = next(j for j in range(3, len(h), 2) if h[j] < h[:j].min())
+    tol_half = h[j] * (1 + 1e-9) / h[0]
+    for tol in (1e-8, tol_half):
+        out = {knobs: solve(knobs, tol) for knobs in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1"))}
+        base = out[("0", "0")]
+        if tol == tol_half:
+            assert base[0][1]["iterations"] == (j + 1) / 2 - 0.5, (base[0][1]["iterations"], j)
+        for knobs, res in out.items():
+            for q in range(world):
+                x0, rep0, l0 = base[q]
+                x1, rep1, l1 = res[q]
+                assert rep1["converged"] == 1 and rep0["iterations"] == rep1["iterations"], (knobs, tol)
+                assert np.array_equal(x0, x1), f"rank {q}: {knobs} changed the solve"
+                assert np.array_equal(rep0["resid_hist"], rep1["resid_hist"]), (knobs, tol)
+                if knobs != ("0", "0"):
+                    assert l1 < l0, (knobs, q, l0, l1)
