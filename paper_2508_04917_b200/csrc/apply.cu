@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 
 // -------------------------------------------------------------------- ring
 #ifndef DD_PF_AHEAD
-#define DD_PF_AHEAD 0
+#define DD_PF_AHEAD -1  // L2 prefetch distance of the ring producer: -1 = half a ring, 0 = off, else bytes
 #endif
 // SPIN = false (level set, Alg. 6): every consumer thread takes one row of
 //   each record; a named barrier separates records (levels).
@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
+    constexpr uint32_t PF = DD_PF_AHEAD < 0 ? RING / 2 : (uint32_t)DD_PF_AHEAD;
     constexpr int TC = TCB<BS>;
     constexpr uint32_t NW = TC / 32;
     static_assert((RING & (RING - 1)) == 0 && (CH & (CH - 1)) == 0 && NST >= 4, "ring shape");
@@ -494,34 +495,38 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 const uint32_t nch = (total + CH - 1) / CH;
                 const uint8_t *rsrc = reinterpret_cast<const uint8_t *>(r) + rlo;
                 const uint8_t *fsrc = slab + si.stream_off + sec_lo;
-#if DD_PF_AHEAD
-                // experiment: L2 prefetch DD_PF_AHEAD bytes ahead of the ring fill
-                // position, into the CTA's next subdomain at the end of this one
+                // L2 prefetch PF bytes ahead of the ring's fill position (into the
+                // CTA's next subdomain near the end of this one): when the ring is
+                // full because the consumers are in narrow levels, HBM keeps
+                // streaming this CTA's next bytes into L2, and the ring refills
+                // from L2 once chunks free up (config 3: 425 -> 406 us at PF =
+                // half a ring, 32 KB; 410 us at 64 KB, 406 us at 128 KB). Half a
+                // ring keeps 296 x 32 KB = 9.5 MB ahead, far below L2; at 256 KB
+                // the prefetched lines are evicted before use (457 us; 512 KB:
+                // 582 us).
                 auto pf_sub = [&](int ss, uint32_t a, uint32_t b) {
                     const SubInfo sj = info[ss];
                     const int64_t jlo = (8 * BS * (int64_t)sj.row0) & ~(int64_t)15;
                     const int64_t jhi = (8 * BS * ((int64_t)sj.row0 + sj.nrows) + 15) & ~(int64_t)15;
                     const uint32_t jrb = (uint32_t)(jhi - jlo);
-                    const uint32_t jtot = jrb + (uint32_t)sj.stream_bytes;
-                    b = min(b, jtot);
+                    const uint32_t jsl = phase == 2 ? (uint32_t)sj.u_off : 0u;
+                    const uint32_t jsh = phase == 1 ? (uint32_t)sj.u_off : (uint32_t)sj.stream_bytes;
+                    b = min(b, jrb + (jsh - jsl));
                     if (a >= b) return;
                     if (a < jrb) prefetch_l2(reinterpret_cast<const uint8_t *>(r) + jlo + a, min(b, jrb) - a);
                     if (b > jrb) {
                         const uint32_t q = max(a, jrb);
-                        prefetch_l2(slab + sj.stream_off + (q - jrb), b - q);
+                        prefetch_l2(slab + sj.stream_off + jsl + (q - jrb), b - q);
                     }
                 };
-#endif
                 for (uint32_t c = 0; c < nch; ++c, ++g) {
                     const uint32_t st = g % NST;
-#if DD_PF_AHEAD
-                    if (phase == 0) {
-                        const uint32_t a = c * CH + DD_PF_AHEAD, b = a + CH;
+                    if (PF) {
+                        const uint32_t a = c * CH + PF, b = a + CH;
                         if (a < total) pf_sub(s, a, b);
                         if (b > total && s + (int)gridDim.x < n_sub)
                             pf_sub(s + gridDim.x, a > total ? a - total : 0u, b - total);
                     }
-#endif
                     if (g >= NST) mbar_wait(&empty[st], ((g / NST) - 1u) & 1u);
                     const uint32_t lo = c * CH, hi = min(total, lo + CH);
                     mbar_arrive_expect_tx(&full[st], hi - lo);
