@@ -12,6 +12,7 @@ ap.add_argument("--tiles", default="16,16,8")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--solve", type=int, default=1)
 ap.add_argument("--spe10", type=int, default=0)
+ap.add_argument("--warm", type=int, default=0, help="1: no L2 flush between reps (L2-warm)")
 a = ap.parse_args()
 grid = tuple(map(int, a.grid.split(","))); tiles = tuple(map(int, a.tiles.split(",")))
 t = time.time()
@@ -30,13 +31,18 @@ st = ctx.stats()
 def timeit(fn, reps):
     ts = []
     for i in range(reps + 3):
-        flush.zero_()
+        if not a.warm:
+            flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); fn(); e1.record(); torch.cuda.synchronize()
         if i >= 3: ts.append(e0.elapsed_time(e1))
     return float(np.median(ts)), float(np.min(ts))
 for var, name in ((1, "levelset"), (2, "spin"), (4, "direct"), (8, "unfused")):
-    med, mn = timeit(lambda: ctx.apply(r, z, var), a.reps)
+    try:
+        med, mn = timeit(lambda: ctx.apply(r, z, var), a.reps)
+    except dd.DDError as e:
+        print(f"apply {name:9s} unavailable: {e}", flush=True)
+        continue
     print(f"apply {name:9s} median {med*1e3:8.1f} us  min {mn*1e3:8.1f} us  canonical {st['apply_canonical_bytes']/med/1e6:7.1f} GB/s  slab {st['slab_bytes_levelset']/med/1e6:7.1f} GB/s  launch {ctx.launch_info(var)}", flush=True)
 y = torch.empty_like(r)
 med, mn = timeit(lambda: ctx.spmv(r, y), a.reps)
