@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 }
 
 // -------------------------------------------------------------------- ring
+#ifndef DD_CH_DIV
+#define DD_CH_DIV 4  // ring chunk = RING / DD_CH_DIV
+#endif
 #ifndef DD_PF_AHEAD
 #define DD_PF_AHEAD -1  // L2 prefetch distance of the ring producer: -1 = half a ring, 0 = off, else bytes
 #endif
@@ -711,17 +714,17 @@ template <int BS, int GEN>
 static RingFn pick_ring_bg(int ring, bool spin) {
     if (!spin) {
         switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 32768, false, GEN>();
-            case 65536: return ring_fn<BS, 65536, 16384, false, GEN>();
-            case 32768: return ring_fn<BS, 32768, 8192, false, GEN>();
-            case 16384: return ring_fn<BS, 16384, 4096, false, GEN>();
+            case 131072: return ring_fn<BS, 131072, 131072 / DD_CH_DIV, false, GEN>();
+            case 65536: return ring_fn<BS, 65536, 65536 / DD_CH_DIV, false, GEN>();
+            case 32768: return ring_fn<BS, 32768, 32768 / DD_CH_DIV, false, GEN>();
+            case 16384: return ring_fn<BS, 16384, 16384 / DD_CH_DIV, false, GEN>();
         }
     } else {
         switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 32768, true, GEN>();
-            case 65536: return ring_fn<BS, 65536, 16384, true, GEN>();
-            case 32768: return ring_fn<BS, 32768, 8192, true, GEN>();
-            case 16384: return ring_fn<BS, 16384, 4096, true, GEN>();
+            case 131072: return ring_fn<BS, 131072, 131072 / DD_CH_DIV, true, GEN>();
+            case 65536: return ring_fn<BS, 65536, 65536 / DD_CH_DIV, true, GEN>();
+            case 32768: return ring_fn<BS, 32768, 32768 / DD_CH_DIV, true, GEN>();
+            case 16384: return ring_fn<BS, 16384, 16384 / DD_CH_DIV, true, GEN>();
         }
     }
     return nullptr;
@@ -742,7 +745,7 @@ static DirectFn pick_direct(int bs, bool gen) {
     return gen ? k_apply_direct<3, 1> : k_apply_direct<3, 2>;
 }
 
-static int ring_chunk(int ring) { return ring / 4; }
+static int ring_chunk(int ring) { return ring / DD_CH_DIV; }
 
 // the dynamic shared-memory attribute is per function and shared by every
 // context: always raise it to the device maximum minus the static part
