@@ -26,6 +26,9 @@ CASES = {
     "random_P4000_split_levels": (lambda: random_block_grid(40, 20, 20, seed=8),
                                   dict(grid=(40, 20, 20), tiles=(20, 20, 10))),
     "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),
+    # odd subdomains start 8 bytes off a 16-byte boundary and their r slice
+    # (24 KB) spans two ring chunks: the vector fill with a shifted start
+    "chunks_P1001_unaligned": (lambda: random_block_grid(24, 24, 24, seed=9), dict(P=1001)),
     "P1": (lambda: random_block_grid(6, 5, 4, seed=6), dict(P=1)),
     "one_subdomain": (lambda: random_block_grid(12, 12, 12, seed=7), dict(grid=(12, 12, 12), tiles=(12, 12, 12))),
     "spe10_style_cfg4": (lambda: spe10_style_bsr3()[:3], dict(grid=(60, 220, 85), tiles=(10, 20, 17))),
