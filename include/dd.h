@@ -55,7 +55,11 @@
  *   dd_bicgstab are collective when world > 1 (halo exchange for SpMV,
  *   all-gather of double-double dot partials; NCCL, or device-to-device
  *   copies between contexts of one process, see DD_COMM_LOCAL).
- *   dd_apply never communicates.
+ *   dd_apply never communicates. Inside dd_bicgstab the apply kernel itself
+ *   writes the rows peers read in the next SpMV (NCCL: into the send
+ *   buffer; DD_COMM_LOCAL: into the consuming peer's ghost block), and an
+ *   iteration has three dot reduction points (s.s joins the (t.s, t.t)
+ *   all-gather); neither changes any iterate.
  */
 #ifndef DD_H
 #define DD_H
