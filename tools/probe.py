@@ -12,12 +12,16 @@ ap.add_argument("--tiles", default="16,16,8")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--solve", type=int, default=1)
 ap.add_argument("--spe10", type=int, default=0)
+ap.add_argument("--stencil27", type=int, default=0, help="1: random 27-point BSR3 (general-K record path)")
 ap.add_argument("--warm", type=int, default=0, help="1: no L2 flush between reps (L2-warm)")
 a = ap.parse_args()
 grid = tuple(map(int, a.grid.split(","))); tiles = tuple(map(int, a.tiles.split(",")))
 t = time.time()
 if a.spe10:
     rp, ci, v, _ = spe10_style_bsr3(*grid)
+elif a.stencil27:
+    from inputs.gen import random_block_stencil27
+    rp, ci, v = random_block_stencil27(*grid, seed=41)
 else:
     rp, ci, v = laplacian_bsr3(*grid)
 print("gen", time.time() - t, flush=True)
