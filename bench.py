@@ -202,6 +202,11 @@ def run_ours(args, cfg):
     # Alg. 5 level assignment on the device, kernel time
     levels_device_ms = ctx.levels_device()[2]
     st = ctx.stats()
+    sv, sv_ms = ctx.solver_variant()  # the apply variant dd_bicgstab uses (timed at setup)
+    VNAME = {dd.DD_LEVELSET: "levelset", dd.DD_SPINLOOP: "spin", dd.DD_DIRECT: "direct"}
+    KNAME = {dd.DD_LEVELSET: "k_apply_ring (fused L/D/U, level set)",
+             dd.DD_SPINLOOP: "k_apply_ring (fused L/D/U, sync-free)",
+             dd.DD_DIRECT: "k_apply_direct (fused L/D/U)"}
     m = 3 * ctx.n_local
     stream = torch.cuda.current_stream()
     bd = torch.empty(m + 2, dtype=torch.float64, device="cuda")
@@ -275,7 +280,8 @@ def run_ours(args, cfg):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_apply_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("workload") == cfg["workload"] and tr.get("n_gpus", 1) == world:
+        same_kernel = ("k_apply_direct" in tr.get("kernel", "")) == (sv == dd.DD_DIRECT)
+        if tr.get("workload") == cfg["workload"] and tr.get("n_gpus", 1) == world and same_kernel:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
@@ -297,13 +303,14 @@ def run_ours(args, cfg):
                   "frac_of_8TBs": round(achieved / 8000.0, 4), "frac_of_measured": round(achieved / peak, 4),
                   "slab_bytes": st["slab_bytes_levelset"],
                   "gbs_moved": round((st["slab_bytes_levelset"] + 48 * ctx.n_local) / (apply_ms * 1e-3) / 1e9, 1),
-                  "launch": ctx.launch_info()},
+                  "variant": VNAME[sv], "launch": ctx.launch_info(sv),
+                  "variants_timed_at_setup_ms": {VNAME[k]: round(t, 4) for k, t in sv_ms.items() if t > 0}},
         "spmv": {"ms": round(spmv_ms, 4), "canonical_bytes": st["spmv_canonical_bytes"],
                  "gbs_canonical": round(st["spmv_canonical_bytes"] / (spmv_ms * 1e-3) / 1e9, 1)},
         "blas1_ms_per_solve": round(prof["blas_ms"] / n_prof, 3),
         "kernel_ms_per_solve": round((prof["apply_ms"] + prof["spmv_ms"] + prof["blas_ms"]) / n_prof, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "k_apply_ring (fused L/D/U)",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": KNAME[sv],
                      "peak_kind": peak_kind},
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(b.nbytes),
                 "d2h_bytes_per_step": int(b.nbytes)},

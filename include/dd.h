@@ -270,6 +270,14 @@ dd_status dd_profile(dd_ctx *ctx, int32_t mode, double *out);
 /* Apply-kernel launch shape chosen at setup: {grid, threads, smem_bytes,
  * ring_bytes} for the given variant. */
 dd_status dd_launch_info(const dd_ctx *ctx, int32_t variant, int64_t *info);
+/* Apply variant dd_bicgstab uses, picked at dd_setup by timing every
+ * available variant once on this device (all variants give bitwise the same
+ * z, so the choice never changes a result; world > 1 keeps DD_LEVELSET, whose
+ * kernel carries the fused halo epilogue). Environment DD_SOLVER_VARIANT =
+ * levelset | spin | direct forces one. *variant (nullable) = DD_LEVELSET |
+ * DD_SPINLOOP | DD_DIRECT; ms[3] (nullable) = the measured apply times of
+ * {level set, sync-free, direct} in ms (0 = not timed / unavailable). */
+dd_status dd_solver_variant(const dd_ctx *ctx, int32_t *variant, double *ms);
 
 /* 128-byte ncclUniqueId for world > 1 (rank 0 calls it; the caller
  * broadcasts the bytes, e.g. with torch.distributed). */

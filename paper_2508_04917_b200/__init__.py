@@ -6,7 +6,7 @@ library is missing this module raises on first use.
 
 Module-level functions carry the C ABI's names (dd_setup, dd_apply, dd_spmv,
 dd_bicgstab, dd_solve_host, dd_permute, dd_unpermute, dd_get_*, dd_stats,
-dd_launch_info, dd_local_range, dd_destroy, dd_nccl_unique_id); ``Context``
+dd_launch_info, dd_solver_variant, dd_local_range, dd_destroy, dd_nccl_unique_id); ``Context``
 wraps a dd_ctx*. Device vectors are torch CUDA tensors (float64, contiguous);
 torch is used only for device memory, streams and process groups.
 """
@@ -32,7 +32,7 @@ STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP"
 EXPORTS = ["dd_setup", "dd_setup_csr", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
            "dd_get_levels", "dd_levels_device", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
-           "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_last_error"]
+           "dd_solver_variant", "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_last_error"]
 
 
 class DDError(RuntimeError):
@@ -85,7 +85,7 @@ def lib():
             "dd_bicgstab": [P, P, P, d, i32, P, P, P], "dd_solve_host": [P, P, P, d, i32, P, P],
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
             "dd_get_levels": [P, i32, P], "dd_levels_device": [P, P, P, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
-            "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_refactor": [P, P, i32, P], "dd_launch_info": [P, i32, P], "dd_nccl_unique_id": [P],
+            "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_refactor": [P, P, i32, P], "dd_launch_info": [P, i32, P], "dd_solver_variant": [P, P, P], "dd_nccl_unique_id": [P],
             "dd_last_error": [],
         }
         for name, args in sig.items():
@@ -269,6 +269,13 @@ class Context:
         return dict(n_apply=int(out[0]), apply_ms=float(out[1]), n_spmv=int(out[2]), spmv_ms=float(out[3]),
                     n_blas=int(out[4]), blas_ms=float(out[5]), launches=int(out[6]))
 
+    def solver_variant(self):
+        """(variant dd_bicgstab uses, {variant: apply ms measured at setup})."""
+        v = np.zeros(1, np.int32)
+        ms = np.zeros(3)
+        _check(lib().dd_solver_variant(self.h, _ptr(v), _ptr(ms)))
+        return int(v[0]), {DD_LEVELSET: float(ms[0]), DD_SPINLOOP: float(ms[1]), DD_DIRECT: float(ms[2])}
+
     def launch_info(self, variant=DD_LEVELSET):
         info = np.zeros(4, np.int64)
         _check(lib().dd_launch_info(self.h, variant, _ptr(info)))
@@ -384,6 +391,10 @@ def dd_refactor(ctx, vals, stream=None):
 
 def dd_profile(ctx, mode=-1):
     return ctx.profile(mode)
+
+
+def dd_solver_variant(ctx):
+    return ctx.solver_variant()
 
 
 def dd_launch_info(ctx, variant=DD_LEVELSET):

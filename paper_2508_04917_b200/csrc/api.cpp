@@ -394,6 +394,64 @@ dd_status halo_out_build(dd_ctx *ctx) {
     return DD_OK;
 }
 
+// The solver's apply variant: every variant reads the same slab and gives
+// bitwise the same z, so dd_setup times each once on this device (3 launches
+// after a warm-up, CUDA events, the workspace vectors as scratch) and
+// dd_bicgstab uses the fastest -- the level set for 7-point slabs, the
+// direct variant for 27-point slabs whose records need the largest ring.
+// world > 1 keeps the level set (its kernel carries the fused halo).
+dd_status tune_solver_variant(dd_ctx *ctx) {
+    ctx->solver_variant = DD_LEVELSET;
+    const char *e = getenv("DD_SOLVER_VARIANT");
+    const std::string want = e ? e : "auto";
+    if (want == "levelset") return DD_OK;
+    if (want == "spin" || want == "direct") {
+        const int v = want == "spin" ? DD_SPINLOOP : DD_DIRECT;
+        if (!(ctx->variants & v)) {
+            set_error("DD_SOLVER_VARIANT: variant unavailable for this slab");
+            return DD_E_INVALID_ARG;
+        }
+        ctx->solver_variant = v;
+        return DD_OK;
+    }
+    if (ctx->world > 1 || ctx->n_local == 0) return DD_OK;
+    Workspace *ws = ws_of(ctx);
+    const int64_t launches0 = ctx->n_launches;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    dd_status rc = DD_OK;
+    cudaMemsetAsync(ws->r, 0, sizeof(double) * ws->m, st);
+    const int vars[3] = {DD_LEVELSET, DD_SPINLOOP, DD_DIRECT};
+    float best = 0.f;
+    for (int q = 0; q < 3 && rc == DD_OK; ++q) {
+        if (!(ctx->variants & vars[q])) continue;
+        rc = apply_launch(ctx, vars[q], ws->r, ws->p, st);  // warm-up
+        cudaEventRecord(a, st);
+        for (int k = 0; k < 3 && rc == DD_OK; ++k) rc = apply_launch(ctx, vars[q], ws->r, ws->p, st);
+        cudaEventRecord(b, st);
+        float ms = 0.f;
+        if (rc == DD_OK && cudaEventSynchronize(b) == cudaSuccess && cudaEventElapsedTime(&ms, a, b) == cudaSuccess) {
+            ctx->variant_ms[q] = ms / 3.0;
+            if (best == 0.f || ms < best) {
+                best = ms;
+                ctx->solver_variant = vars[q];
+            }
+        }
+    }
+    ctx->n_launches = launches0;  // setup-time launches are not the caller's
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(st);
+    if (rc == DD_OK && cudaGetLastError() != cudaSuccess) {
+        set_error("dd_setup: apply variant timing failed");
+        rc = DD_E_CUDA;
+    }
+    return rc;
+}
+
 dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     const double t0 = now_ms();
     CK(cudaSetDevice(ctx->device));
@@ -517,6 +575,7 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
         TRY(local_join(ctx, nccl_id));
     }
     if (ctx->world > 1) TRY(halo_out_build(ctx));
+    TRY(tune_solver_variant(ctx));
     ctx->setup_ms[5] = now_ms() - t0;
     return DD_OK;
 }
@@ -641,7 +700,8 @@ dd_status apply_halo(dd_ctx *c, const double *r, double *z, cudaStream_t st, con
             if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
                 CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_free, 0));
     }
-    TRY(apply_launch(c, DD_LEVELSET, r, z, reinterpret_cast<void *>(st), skip, fuse ? &ws->hout : nullptr));
+    TRY(apply_launch(c, fuse ? DD_LEVELSET : c->solver_variant, r, z, reinterpret_cast<void *>(st), skip,
+                     fuse ? &ws->hout : nullptr));
     if (local) CK(cudaEventRecord(ws->xev_app, st));
     return DD_OK;
 }
@@ -1328,6 +1388,14 @@ dd_status dd_profile(dd_ctx *c, int32_t mode, double *out) {
         out[6] = (double)c->n_launches;
         out[7] = 0;
     }
+    return DD_OK;
+}
+
+dd_status dd_solver_variant(const dd_ctx *c, int32_t *variant, double *ms) {
+    if (!c) return DD_E_INVALID_ARG;
+    if (variant) *variant = c->solver_variant;
+    if (ms)
+        for (int q = 0; q < 3; ++q) ms[q] = c->variant_ms[q];
     return DD_OK;
 }
 

@@ -133,6 +133,8 @@ struct dd_ctx {
     // slabs
     ddi::Slab slab_lvl, slab_spin;
     int32_t variants = 0;
+    int32_t solver_variant = DD_LEVELSET;  // apply variant inside dd_bicgstab (timed at setup)
+    double variant_ms[3] = {0, 0, 0};      // level set, sync-free, direct
     ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct;
     // spmv
     ddi::SpmvDev spmv;

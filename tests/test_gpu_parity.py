@@ -302,3 +302,31 @@ def test_graph_solve_equals_batched_solve(name):
     x3 = torch.zeros_like(br)
     r3 = ctx.bicgstab(br, x3, tol=1e-30, max_iter=3)
     assert r3["status_name"] == "DD_E_MAXITER" and r3["iterations"] == 3
+
+
+@pytest.mark.parametrize("name", ["cfg1_16^3", "stencil27_geo"])
+def test_solver_variant_autotune_bitwise(name, monkeypatch):
+    """dd_setup times every apply variant and dd_bicgstab uses the fastest
+    (dd_solver_variant); all variants give bitwise the same z, so forcing any
+    of them (DD_SOLVER_VARIANT) gives bitwise the same solve."""
+    import torch
+    rp, ci, v, S, ctx = get_case(name)
+    var, ms = ctx.solver_variant()
+    timed = {k: t for k, t in ms.items() if t > 0}
+    assert var in timed and timed[var] == min(timed.values()), (var, ms)
+    _, b = manufactured_rhs(rp, ci, v)
+    br = torch_vec(b.reshape(-1, 3)[S["new_to_old"]].ravel())
+    sols = {}
+    for forced, code in (("levelset", dd.DD_LEVELSET), ("direct", dd.DD_DIRECT), ("spin", dd.DD_SPINLOOP)):
+        if ms[code] == 0:  # unavailable for this slab (sync-free flags do not fit)
+            continue
+        monkeypatch.setenv("DD_SOLVER_VARIANT", forced)
+        c2 = dd.dd_setup(rp, ci, v, variants=ALL, **CASES[name][1])
+        assert c2.solver_variant()[0] == code
+        x = torch.zeros_like(br)
+        rep = c2.bicgstab(br, x, tol=1e-8, hist=True)
+        sols[forced] = (x.cpu().numpy(), rep["iterations"], rep["resid_hist"])
+        c2.destroy()
+    x0, it0, h0 = sols["levelset"]
+    for forced, (x1, it1, h1) in sols.items():
+        assert it1 == it0 and np.array_equal(x1, x0) and np.array_equal(h1, h0), forced
