@@ -110,6 +110,7 @@ class ClockSampler:
 def cpu_baseline(cfg, rp, ci, v, b, full_iters, n_it=4):
     """The oracle as it stands, on this host's cores, on a bounded sample:
     the first iterations of the same solve, scaled to a full solve."""
+    import numpy as np
     import oracle
     oracle.set_threads(0)
     cores = oracle.get_threads()
@@ -125,10 +126,25 @@ def cpu_baseline(cfg, rp, ci, v, b, full_iters, n_it=4):
     per_it = ((t2 - t1) - (t1 - t0)) / n_it
     fixed = (t1 - t0) - per_it
     est_ms = 1e3 * (fixed + per_it * full_iters)
+    # the oracle's apply alone: median of 3 on all cores and on
+    # one thread (OpenMP over subdomains only; bitwise the same output)
+    from inputs.gen import apply_input
+    r = apply_input(S["n"])
+    apply_ms = {}
+    for label, nt in (("all_cores", 0), ("1_thread", 1)):
+        oracle.set_threads(nt)
+        ts = []
+        for _ in range(3):
+            a = time.perf_counter()
+            oracle.apply(S, r)
+            ts.append(1e3 * (time.perf_counter() - a))
+        apply_ms[label] = round(float(np.median(ts)), 2)
+    oracle.set_threads(0)
     return {"value": round(est_ms, 3), "unit": "ms", "cores": cores, "kind": "oracle",
             "sample": f"oracle BiCGSTAB on the same {cfg['workload']} system: 1 and {1 + n_it} iterations timed "
                       f"({(t2 - t0):.1f} s), per-iteration cost {1e3 * per_it:.1f} ms scaled to {full_iters} "
                       f"iterations; oracle setup {setup_s:.1f} s not included",
+            "apply_ms": apply_ms,
             "higher_is_better": False}
 
 
