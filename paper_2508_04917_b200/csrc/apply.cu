@@ -90,12 +90,22 @@ struct RingRd {  // ring variant, record wraps the ring end
     }
 };
 
-// Sync-free variant: flags[i] holds the epoch of the last sweep that finished
-// row i (L sweeps publish ep - 1, U sweeps ep; epochs only grow).
-__device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, uint32_t ep) {
-    while (*reinterpret_cast<const volatile uint32_t *>(flags + j) < ep) {
+// Sync-free variant: per-row ready bits in shared memory, one bitset for the
+// L sweep and one for the U sweep of the current subdomain (cleared while
+// the next subdomain's r slice is loaded). 1 bit per row and sweep keeps the
+// flags at 512 B for P 2048, so two sync-free CTAs fit on an SM beside their
+// 48 KB vectors and 64 KB rings (4-byte epochs needed 8 KB and forced one).
+struct SpinFlags {
+    uint32_t *L, *U;
+};
+__device__ __forceinline__ void spin_bit(const uint32_t *bits, uint32_t j) {
+    while (!((*reinterpret_cast<const volatile uint32_t *>(bits + (j >> 5)) >> (j & 31u)) & 1u)) {
     }
     __threadfence_block();
+}
+__device__ __forceinline__ void set_bit(uint32_t *bits, uint32_t i) {
+    __threadfence_block();
+    atomicOr(bits + (i >> 5), 1u << (i & 31u));
 }
 
 // Process one record: thread t owns the t-th row of the record (t < w).
@@ -106,7 +116,7 @@ __device__ __forceinline__ void spin_until(const uint32_t *flags, uint32_t j, ui
 // K with blocks in groups of three, 2 = general K one block per step
 template <bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
-                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+                                                double *__restrict__ vec, SpinFlags F) {
     const uint32_t w = h.w, K = h.K;
     if (t >= (int)w) return;
     const bool upper = (h.flags & ddi::REC_UPPER) != 0;
@@ -148,7 +158,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
             double D[9];
 #pragma unroll
             for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
-            if (SPIN) spin_until(flags, i, ep - 1);  // own L result
+            if (SPIN) spin_bit(F.L, i);  // own L result
             const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
             a0 = D[0] * z0;
             a0 = __fma_rn(D[1], z1, a0);
@@ -170,13 +180,13 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
             {
                 const bool ok = (uint32_t)t < cnt[k];
                 const uint32_t j = ok ? col[k] : i;
-                if (SPIN && ok) spin_until(flags, j, ep);
+                if (SPIN && ok) spin_bit(upper ? F.U : F.L, j);
                 const double y0 = vec[3 * j], y1 = vec[3 * j + 1], y2 = vec[3 * j + 2];
                 const double x0 = ok ? y0 : 0.0, x1 = ok ? y1 : 0.0, x2 = ok ? y2 : 0.0;
 #else
             if ((uint32_t)t < cnt[k]) {
                 const uint32_t j = col[k];
-                if (SPIN) spin_until(flags, j, ep);
+                if (SPIN) spin_bit(upper ? F.U : F.L, j);
                 const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
 #endif
                 a0 = __fma_rn(-b[k][0], x0, a0);
@@ -193,10 +203,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         vec[3 * i] = a0;
         vec[3 * i + 1] = a1;
         vec[3 * i + 2] = a2;
-        if (SPIN) {
-            __threadfence_block();
-            *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
-        }
+        if (SPIN) set_bit(upper ? F.U : F.L, i);
         return;
     }
     // ---- general K (> 3): descriptor of rec_dw(K) bytes, loop over k. Compiled
@@ -210,7 +217,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         double D[9];
 #pragma unroll
         for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
-        if (SPIN) spin_until(flags, i, ep - 1);  // own L result
+        if (SPIN) spin_bit(F.L, i);  // own L result
         const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
         a0 = D[0] * z0;
         a0 = __fma_rn(D[1], z1, a0);
@@ -237,7 +244,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         double b[9];
 #pragma unroll
         for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + 8u * ck * v);
-        if (SPIN) spin_until(flags, j, ep);
+        if (SPIN) spin_bit(upper ? F.U : F.L, j);
         const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
         a0 = __fma_rn(-b[0], x0, a0);
         a0 = __fma_rn(-b[1], x1, a0);
@@ -285,7 +292,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         for (int q = 0; q < 3; ++q) {
             {
                 const bool ok = (uint32_t)t < ck[q];
-                if (SPIN && ok) spin_until(flags, j[q], ep);
+                if (SPIN && ok) spin_bit(upper ? F.U : F.L, j[q]);
                 const double y0 = vec[3 * j[q]], y1 = vec[3 * j[q] + 1], y2 = vec[3 * j[q] + 2];
                 const double x0 = ok ? y0 : 0.0, x1 = ok ? y1 : 0.0, x2 = ok ? y2 : 0.0;
 #else
@@ -302,7 +309,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             if ((uint32_t)t < ck[q]) {
-                if (SPIN) spin_until(flags, j[q], ep);
+                if (SPIN) spin_bit(upper ? F.U : F.L, j[q]);
                 const double x0 = vec[3 * j[q]], x1 = vec[3 * j[q] + 1], x2 = vec[3 * j[q] + 2];
 #endif
                 a0 = __fma_rn(-b[q][0], x0, a0);
@@ -322,10 +329,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     vec[3 * i] = a0;
     vec[3 * i + 1] = a1;
     vec[3 * i + 2] = a2;
-    if (SPIN) {
-        __threadfence_block();
-        *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
-    }
+    if (SPIN) set_bit(upper ? F.U : F.L, i);
     }
 }
 
@@ -335,7 +339,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
 // fma(-u_ij, x_j, acc); blocks ascending).
 template <bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
-                                                double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+                                                double *__restrict__ vec, SpinFlags F) {
     const uint32_t w = h.w, K = h.K;
     if (t >= (int)w) return;
     const bool upper = (h.flags & ddi::REC_UPPER) != 0;
@@ -357,7 +361,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
         double a;
         if (upper) {
             const double D = rd.template ld<double>(off_dinv + 8u * t);
-            if (SPIN) spin_until(flags, i, ep - 1);
+            if (SPIN) spin_bit(F.L, i);
             a = D * vec[i];
         } else {
             a = vec[i];
@@ -366,15 +370,12 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
         for (int k = 0; k < 3; ++k) {
             if ((uint32_t)t < cnt[k]) {
                 const uint32_t j = col[k];
-                if (SPIN) spin_until(flags, j, ep);
+                if (SPIN) spin_bit(upper ? F.U : F.L, j);
                 a = __fma_rn(-b[k], vec[j], a);
             }
         }
         vec[i] = a;
-        if (SPIN) {
-            __threadfence_block();
-            *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
-        }
+        if (SPIN) set_bit(upper ? F.U : F.L, i);
         return;
     }
     if constexpr (GEN) {
@@ -383,7 +384,7 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     double a;
     if (upper) {
         const double D = rd.template ld<double>(off_dinv + 8u * t);
-        if (SPIN) spin_until(flags, i, ep - 1);
+        if (SPIN) spin_bit(F.L, i);
         a = D * vec[i];
     } else {
         a = vec[i];
@@ -407,27 +408,24 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             if ((uint32_t)t < ck[q]) {
-                if (SPIN) spin_until(flags, j[q], ep);
+                if (SPIN) spin_bit(upper ? F.U : F.L, j[q]);
                 a = __fma_rn(-b[q], vec[j[q]], a);
             }
         }
         pre = pq;
     }
     vec[i] = a;
-    if (SPIN) {
-        __threadfence_block();
-        *reinterpret_cast<volatile uint32_t *>(flags + i) = ep;
-    }
+    if (SPIN) set_bit(upper ? F.U : F.L, i);
     }
 }
 
 template <int BS, bool SPIN, int GEN, class Rd>
 __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
-                                               double *__restrict__ vec, uint32_t *flags, uint32_t ep) {
+                                               double *__restrict__ vec, SpinFlags F) {
     if constexpr (BS == 3)
-        process_record3<SPIN, GEN>(rd, h, c8, t, vec, flags, ep);
+        process_record3<SPIN, GEN>(rd, h, c8, t, vec, F);
     else
-        process_record1<SPIN, GEN>(rd, h, c8, t, vec, flags, ep);
+        process_record1<SPIN, GEN>(rd, h, c8, t, vec, F);
 }
 
 __device__ __forceinline__ RecHdr hdr_from(uint4 q) {
@@ -486,7 +484,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
             // L level 0 carries no blocks (z_i = r_i in place): no work, no barrier
             const bool skip = !(h.flags & ddi::REC_UPPER) && h.K == 0 && !last;
             if (!skip) {
-                process_record<BS, false, GEN>(GlobalRd{p}, h, c8, t, vec, nullptr, 0);
+                process_record<BS, false, GEN>(GlobalRd{p}, h, c8, t, vec, SpinFlags{nullptr, nullptr});
                 __syncthreads();
             }
             ro += h.bytes;
@@ -530,7 +528,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     uint8_t *ring = smem + vec_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + RING);
     uint64_t *empty = full + NST;
-    uint32_t *flags = reinterpret_cast<uint32_t *>(empty + NST);
+    // sync-free ready bits: L bitset then U bitset, fw words each
+    const uint32_t fw = ((uint32_t)vec_bytes / (8u * BS) + 31u) / 32u;
+    const SpinFlags F{reinterpret_cast<uint32_t *>(empty + NST), reinterpret_cast<uint32_t *>(empty + NST) + fw};
     const int tid = threadIdx.x;
 
     if (tid == TC) {
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         fence_mbar_init();
     }
     if (SPIN) {
-        for (int q = tid; q < vec_bytes / (8 * BS); q += TC + 32) flags[q] = 0;
+        for (uint32_t q = tid; q < 2 * fw; q += TC + 32) F.L[q] = 0u;
     }
     __syncthreads();
 
@@ -615,7 +615,6 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     uint32_t gbase = 0;     // chunk index at which the current subdomain starts
     uint32_t ready = 0;     // chunks this thread has seen full
     uint32_t released = 0;  // chunks handed back (SPIN: each warp's lane 0; else t == TC - 32)
-    uint32_t ep = 0;
     auto ensure = [&](uint32_t chunk) {
         while (ready <= chunk) {
             mbar_wait(&full[ready % NST], (ready / NST) & 1u);
@@ -661,9 +660,12 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 release_to(gbase + c + 1);
             }
         }
+        // sync-free: clear the ready bits of the previous subdomain (every
+        // thread passed its final barrier, nobody reads them until the next)
+        if (SPIN)
+            for (uint32_t q = t; q < 2 * fw; q += TC) F.L[q] = 0u;
         named_bar_sync(1, TC);
         release_to(gbase + rb / CH);
-        ep += 2;  // sync-free: L rows publish ep - 1, U rows ep
         // ---- records
         uint32_t ro = rb;
         while (true) {
@@ -680,12 +682,11 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             // L level 0 carries no blocks (z_i = r_i in place): the level set
             // skips it (no work, no barrier); the sync-free sweep publishes flags
             const bool skip = !SPIN && !upper && h.K == 0 && !last;
-            const uint32_t ep_set = upper ? ep : ep - 1;
             if (mode == 1 || skip) {
             } else if (pos + h.bytes <= RING) {
-                process_record<BS, SPIN, GEN>(LinRd{ring + pos}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN, GEN>(LinRd{ring + pos}, h, c8, t, vec, F);
             } else {
-                process_record<BS, SPIN, GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, flags, ep_set);
+                process_record<BS, SPIN, GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, F);
             }
             ro += h.bytes;
             if (SPIN) {
@@ -807,7 +808,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     const int bs = ctx->bs;
     const bool gen = ctx->kmax > 3;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
-    const int flag_bytes = ((4 * ctx->max_P + 127) / 128) * 128;  // sync-free ready flags, 4 B per row
+    const int flag_bytes = ((8 * ((ctx->max_P + 31) / 32)) + 15) / 16 * 16;  // sync-free ready bits: 2 per row
     const int tc = bs == 1 ? TCB<1> : TCB<3>;
     // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
     {
@@ -831,20 +832,27 @@ dd_status apply_prepare(dd_ctx *ctx) {
     auto choose = [&](LaunchCfg &c, bool spin, int64_t max_rec) -> dd_status {
         const int want = env_int("DD_RING_KB", 0) * 1024;
         const int cands[4] = {131072, 65536, 32768, 16384};
-        int best_ring = 0, best_occ = 0;
-        for (int rc : cands) {
+        int occs[4] = {0, 0, 0, 0}, max_occ = 0;
+        for (int k = 0; k < 4; ++k) {
+            const int rc = cands[k];
             if (want && rc != want) continue;
             const int nst = rc / ring_chunk(rc);
             const int sm = vec_bytes + rc + 16 * nst + (spin ? flag_bytes : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
             allow_max_smem(pick_ring(bs, rc, spin, gen), smem_max);
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, spin, gen), tc + 32, sm);
-            if (occ > best_occ) {
-                best_occ = occ;
-                best_ring = rc;
-            }
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs[k], pick_ring(bs, rc, spin, gen), tc + 32, sm);
+            max_occ = std::max(max_occ, occs[k]);
         }
+        // CTAs per SM worth having: no more than the subdomains can fill
+        // (128 subdomains on 148 SMs run one CTA per SM whatever the ring), then
+        // the largest ring at that occupancy
+        const int need = std::max(1, std::min(max_occ, (nsl + ctx->num_sms - 1) / ctx->num_sms));
+        int best_ring = 0, best_occ = 0;
+        for (int k = 0; k < 4; ++k)
+            if (occs[k] >= need && !best_ring) {
+                best_ring = cands[k];
+                best_occ = occs[k];
+            }
         if (!best_ring) {
             set_error("no ring size fits the subdomain vector and the largest record");
             return DD_E_SUBDOMAIN_TOO_LARGE;
@@ -864,7 +872,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
         dd_status st = choose(ctx->cfg_lvl, false, ctx->slab_lvl.max_rec_bytes);
         if (st != DD_OK) return st;
     }
-    // the sync-free variant also needs 4 B of ready flags per row; when it
+    // the sync-free variant also needs 2 ready bits per row; when they
     // does not fit it is dropped (dd_apply_variant then reports the error)
     if (choose(ctx->cfg_spin, true, ctx->slab_lvl.max_rec_bytes) != DD_OK) {
         ctx->variants &= ~DD_SPINLOOP;

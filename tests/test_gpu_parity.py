@@ -71,8 +71,9 @@ def test_apply_parity(name, variant):
     r = apply_input(S["n"], seed=2)
     z_ref = oracle.apply(S, r)
     z = torch.full((3 * S["n"],), float("nan"), dtype=torch.float64, device="cuda")
-    if variant == dd.DD_SPINLOOP and S["sub_ptr"].size and max(np.diff(S["sub_ptr"])) > 6000:
-        # 24 B/row vector + 4 B/row flags + ring do not fit 227 KB: clean error, no fallback
+    if variant == dd.DD_SPINLOOP and ctx.launch_info(dd.DD_SPINLOOP)["grid"] == 0:
+        # vector + ready bits + a ring holding the largest record do not fit
+        # 227 KB: a clean error, no fallback
         with pytest.raises(dd.DDError) as e:
             ctx.apply(torch_vec(r), z, variant)
         assert e.value.name == "DD_E_SUBDOMAIN_TOO_LARGE"
