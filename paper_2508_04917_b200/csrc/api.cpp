@@ -415,9 +415,12 @@ dd_status tune_solver_variant(dd_ctx *ctx) {
         return DD_OK;
     }
     if (ctx->world > 1 || ctx->n_local == 0) return DD_OK;
-    // under a profiler or sanitizer (they inject through this variable) kernel
-    // times are serialised replays: keep the level set rather than trust them
-    if (getenv("CUDA_INJECTION64_PATH")) return DD_OK;
+    // under Nsight Compute or compute-sanitizer (recognised by the variables
+    // their injection sets) kernel times are serialised replays: keep the
+    // level set rather than trust them
+    for (const char *v : {"NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NVIDIA_PROCESS_INJECTION_CRASH_REPORTING",
+                          "NVTX_INJECTION64_PATH", "CUDA_INJECTION64_PATH"})
+        if (getenv(v)) return DD_OK;
     Workspace *ws = ws_of(ctx);
     const int64_t launches0 = ctx->n_launches;
     cudaStream_t st;
