@@ -7,6 +7,9 @@ import numpy as np, torch
 import paper_2508_04917_b200 as dd
 from inputs.gen import random_block_grid, laplacian_csr, apply_input, manufactured_rhs, random_block_stencil27
 
+_held = []
+
+
 def one(rp, ci, v, kw, csr=False):
     ctx = (dd.dd_setup_csr if csr else dd.dd_setup)(rp, ci, v, variants=7, **kw)
     bs = 1 if csr else 3
@@ -22,7 +25,10 @@ def one(rp, ci, v, kw, csr=False):
     x = torch.zeros_like(r)
     rep = ctx.bicgstab(r, x, tol=1e-8, max_iter=200)
     torch.cuda.synchronize()
-    ctx.destroy()
+    if os.environ.get("SAN_KEEP", "0") == "1":
+        _held.append((ctx, r, z, x))
+    else:
+        ctx.destroy()
     return rep["iterations"]
 
 print(one(*random_block_grid(12, 10, 8, seed=3), dict(grid=(12, 10, 8), tiles=(6, 5, 4))))
