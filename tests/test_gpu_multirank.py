@@ -15,7 +15,7 @@ import pytest
 import oracle
 import paper_2508_04917_b200 as dd
 from inputs.gen import (apply_input, bsr_to_scipy, laplacian_bsr3, manufactured_rhs, random_block_grid,
-                        spe10_style_bsr3)
+                        random_block_stencil27, spe10_style_bsr3)
 
 pytestmark = pytest.mark.gpu
 
@@ -25,6 +25,8 @@ CASES = {
     "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),
     "spe10_small": (lambda: spe10_style_bsr3(20, 40, 20, upper_ness_from=10)[:3],
                     dict(grid=(20, 40, 20), tiles=(10, 20, 10))),
+    # 27-point rows: the general-K apply kernels, edge and corner halo rows
+    "stencil27": (lambda: random_block_stencil27(12, 12, 12, seed=33), dict(grid=(12, 12, 12), tiles=(6, 6, 4))),
 }
 
 
@@ -38,7 +40,7 @@ def run_ranks(world, fn):
 
 @pytest.mark.parametrize("name,world", [("random_8sub", 2), ("random_8sub", 3), ("laplace_24^3", 2),
                                         ("laplace_24^3", 4), ("chunks_ragged_oddP", 2), ("chunks_ragged_oddP", 5),
-                                        ("spe10_small", 3)])
+                                        ("spe10_small", 3), ("stencil27", 3)])
 def test_local_world_parity(name, world):
     import torch
     gen, kw = CASES[name]
@@ -150,7 +152,7 @@ def test_local_world_bad_arguments():
 
 
 @pytest.mark.parametrize("name,world", [("laplace_24^3", 3), ("chunks_ragged_oddP", 2), ("spe10_small", 2),
-                                        ("random_8sub", 4)])
+                                        ("random_8sub", 4), ("stencil27", 2)])
 def test_fused_halo_and_merged_reduction_equal_plain(name, world, monkeypatch):
     """SURVEY 8(f4), world > 1. (a) Fused halo: the solver's applies write the
     rows peers read in the next SpMV straight from shared memory into the
