@@ -577,8 +577,8 @@ void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg,
     const auto &S = ctx->spmv;
     const int grid = ctx->num_sms * 8;           // plain: grid-stride
     const int grid1 = spmv_fused_grid(ctx);      // fused dots: one warp per slice (fixed per context)
-    static const int mb0 = env_i("DD_SPMV_MINB_0", 1), mb1 = env_i("DD_SPMV_MINB_1", 5),
-                     mb2 = env_i("DD_SPMV_MINB_2", 5);
+    static const int mb0 = env_i("DD_SPMV_MINB_0", 1), mb1 = env_i("DD_SPMV_MINB_1", 1),
+                     mb2 = env_i("DD_SPMV_MINB_2", 1);
     switch (mode) {
         case SPMV_PLAIN: spmv_go<SPMV_PLAIN>(ctx->bs, mb0, grid, st, ctx->n_local, S, x, xg, y, aux, ra); break;
         case SPMV_SIGMA: spmv_go<SPMV_SIGMA>(ctx->bs, mb1, grid1, st, ctx->n_local, S, x, xg, y, aux, ra); break;
