@@ -107,6 +107,40 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def host_info():
+    """CPU model, affinity and OpenMP threads of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = os.cpu_count()
+    return {"cpu_model": model, "affinity_cpus": aff, "omp_num_threads_env": os.environ.get("OMP_NUM_THREADS")}
+
+
+def oracle_solve_estimate(S, br, full_iters, n_it):
+    """ONE timing model for both oracle legs (cpu_baseline and --impl
+    reference): time a 1-iteration and a (1 + n_it)-iteration oracle solve of
+    the same system, split fixed cost (init, true residual) from the
+    per-iteration cost, and scale to the full iteration count."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.bicgstab(S, br, tol=1e-300, max_iter=1, hist=False)
+    t1 = time.perf_counter()
+    oracle.bicgstab(S, br, tol=1e-300, max_iter=1 + n_it, hist=False)
+    t2 = time.perf_counter()
+    per_it = ((t2 - t1) - (t1 - t0)) / n_it
+    fixed = (t1 - t0) - per_it
+    return 1e3 * (fixed + per_it * full_iters), 1e3 * per_it, t2 - t0
+
+
 def cpu_baseline(cfg, rp, ci, v, b, full_iters, n_it=4):
     """The oracle as it stands, on this host's cores, on a bounded sample:
     the first iterations of the same solve, scaled to a full solve."""
@@ -118,14 +152,9 @@ def cpu_baseline(cfg, rp, ci, v, b, full_iters, n_it=4):
     S = oracle.setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"])
     setup_s = time.perf_counter() - t0
     br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
-    t0 = time.perf_counter()
-    oracle.bicgstab(S, br, tol=1e-300, max_iter=1, hist=False)
-    t1 = time.perf_counter()
-    oracle.bicgstab(S, br, tol=1e-300, max_iter=1 + n_it, hist=False)
-    t2 = time.perf_counter()
-    per_it = ((t2 - t1) - (t1 - t0)) / n_it
-    fixed = (t1 - t0) - per_it
-    est_ms = 1e3 * (fixed + per_it * full_iters)
+    est_ms, per_it_ms, wall = oracle_solve_estimate(S, br, full_iters, n_it)
+    per_it = per_it_ms / 1e3
+    t2, t0 = wall, 0.0
     # the oracle's apply alone: median of 3 on all cores and on
     # one thread (OpenMP over subdomains only; bitwise the same output)
     from inputs.gen import apply_input
@@ -144,7 +173,7 @@ def cpu_baseline(cfg, rp, ci, v, b, full_iters, n_it=4):
             "sample": f"oracle BiCGSTAB on the same {cfg['workload']} system: 1 and {1 + n_it} iterations timed "
                       f"({(t2 - t0):.1f} s), per-iteration cost {1e3 * per_it:.1f} ms scaled to {full_iters} "
                       f"iterations; oracle setup {setup_s:.1f} s not included",
-            "apply_ms": apply_ms,
+            "apply_ms": apply_ms, "host": host_info(),
             "higher_is_better": False}
 
 
@@ -162,21 +191,20 @@ def run_reference(args, cfg):
     n_it = 2
     vals, walls = [], []
     for step in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle.bicgstab(S, br, tol=1e-300, max_iter=n_it, hist=False)
-        w = time.perf_counter() - t0
+        est_ms, _, w = oracle_solve_estimate(S, br, full, n_it)
         if step >= args.warmup:
             walls.append(w)
-            vals.append(1e3 * w / n_it * full)
+            vals.append(est_ms)
     value = float(np.mean(vals))
     line = {"metric": METRIC, "value": round(value, 3), "unit": "ms", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(walls)), 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg["workload"], "tol": cfg["tol"]},
             "cpu_baseline": {"value": round(value, 3), "unit": "ms", "cores": oracle.get_threads(), "kind": "oracle",
-                             "sample": f"each step: the first {n_it} oracle BiCGSTAB iterations of the "
-                                       f"{cfg['workload']} solve, scaled to the oracle's full {full}-iteration "
-                                       f"solve (tests/golden/oracle_bicgstab.json)"},
+                             "sample": f"each step: a 1- and a {1 + n_it}-iteration oracle BiCGSTAB solve of the "
+                                       f"{cfg['workload']} system (fixed and per-iteration cost separated, the "
+                                       f"same model as cpu_baseline), scaled to the oracle's full {full}-iteration "
+                                       f"solve (tests/golden/oracle_bicgstab.json)", "host": host_info()},
             "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -197,13 +225,20 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rp, ci, v, b = make_inputs(cfg)
     nccl_id = None
+    comm_info = None
     if world > 1:
-        obj = [dd.dd_nccl_unique_id() if rank == 0 else None]
+        # the group key: an ncclUniqueId (comm nccl) or 128 random bytes naming
+        # the peer-memory group (comm ipc); rank 0 draws it, torch broadcasts
+        obj = [(dd.dd_nccl_unique_id() if args.comm == "nccl" else dd.comm_key()) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+        one = torch.ones(1, device="cuda")
+        dist.all_reduce(one)
+        comm_info = {"transport": args.comm, "nranks": int(one.item()), "nranks_ok": int(one.item()) == world,
+                     "devices": torch.cuda.device_count()}
     t0 = time.perf_counter()
     ctx = dd.dd_setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"], device=local, rank=rank, world=world,
-                      nccl_id=nccl_id, enable_refactor=True)
+                      nccl_id=nccl_id, enable_refactor=True, comm=args.comm if world > 1 else "nccl")
     setup_ms = 1e3 * (time.perf_counter() - t0)
     # GPU numeric re-factorisation of the same pattern, values already on the device
     vd = torch.from_numpy(v).cuda()
@@ -286,11 +321,21 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
-    # roofline of the dominant kernel (fused apply), measured inside the timed solves
+    # roofline of the dominant kernel (fused apply), measured inside the timed
+    # solves; world > 1: the slowest rank's apply moves all ranks' bytes
     apply_ms = prof["apply_ms"] / max(1, prof["n_apply"])
     spmv_ms = prof["spmv_ms"] / max(1, prof["n_spmv"])
     peak, peak_kind = measured_peak()
     canon = st["apply_canonical_bytes"]
+    if world > 1:
+        t = torch.tensor([apply_ms, spmv_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        apply_ms, spmv_ms = float(t[0]), float(t[1])
+        t = torch.tensor([canon, st["spmv_canonical_bytes"]], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        canon = int(t[0])
+        st["spmv_canonical_bytes"] = int(t[1])
+        peak = peak * world  # every rank's HBM
     achieved = canon / (apply_ms * 1e-3) / 1e9
     traffic = None
     try:
@@ -326,13 +371,18 @@ def run_ours(args, cfg):
         "blas1_ms_per_solve": round(prof["blas_ms"] / n_prof, 3),
         "kernel_ms_per_solve": round((prof["apply_ms"] + prof["spmv_ms"] + prof["blas_ms"]) / n_prof, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": KNAME[sv],
-                     "peak_kind": peak_kind},
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": "stored ncu --set full capture of this kernel on this workload "
+                                       "(profiles/ncu_apply_traffic.json), not measured in this run"
+                                       if traffic is not None else None,
+                     "kernel": KNAME[sv], "peak_kind": peak_kind},
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(b.nbytes),
                 "d2h_bytes_per_step": int(b.nbytes)},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if comm_info:
+        out["comm"] = comm_info
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(cfg, rp, ci, v, b, golden_iterations(cfg) or r0["iterations"])
@@ -354,11 +404,33 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="ipc", choices=["ipc", "nccl"],
+                    help="world > 1 transport: peer memory over NVLink (ipc) or NCCL")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     return run_ours(args, cfg)
+
+
+def self_launch(args):
+    """--gpus N without torchrun: launch N ranks (one per GPU) the way the
+    driver does; fail loudly if fewer than N devices exist."""
+    import socket
+
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, {n} visible\n")
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -124,21 +124,40 @@ typedef struct {
     int32_t n_threads;        /* host setup threads, 0 = all                   */
     int32_t enable_refactor;  /* 1: keep the symbolic maps dd_refactor needs    */
     int32_t partitioner;      /* without grid: DD_PART_CHUNKS or DD_PART_BFS    */
-    int32_t comm;             /* world > 1: DD_COMM_NCCL (default) or DD_COMM_LOCAL */
+    int32_t comm;             /* world > 1: DD_COMM_NCCL (default), DD_COMM_IPC or DD_COMM_LOCAL */
 } dd_opts;
 
 /* Exchange transports for world > 1 (the SpMV halo and the dot partials):
  *   DD_COMM_NCCL   one process per GPU; nccl_unique_id is an ncclUniqueId.
- *   DD_COMM_LOCAL  the ranks are contexts of ONE process (one per GPU, or
- *                  several sharing a GPU), each created and driven by its own
- *                  host thread (dd_setup, dd_spmv, dd_bicgstab, dd_solve_host
- *                  and dd_destroy are collective over the group);
- *                  nccl_unique_id is any 128-byte key the ranks share. Data
- *                  moves by device-to-device (peer) copies ordered with CUDA
- *                  events and one host rendezvous per exchange; a rendezvous
- *                  that waits > 120 s fails with DD_E_NCCL. */
+ *                  Grouped ncclSend/ncclRecv for the halo, ncclAllGather for
+ *                  the dot partials; asynchronous NCCL errors are polled
+ *                  while the host waits (the communicator is aborted and the
+ *                  call fails with DD_E_NCCL).
+ *   DD_COMM_IPC    one process per GPU on one node (the 8-GPU NVSwitch box):
+ *                  peer-memory transport. Every rank owns a device mailbox
+ *                  (ghost block, dot slots, flags) that every peer maps with
+ *                  CUDA IPC handles; the apply kernel's epilogue stores the
+ *                  halo rows straight into the consumer's ghost block (NVLink
+ *                  stores), one-thread kernels publish / wait on monotone
+ *                  counters (release / acquire, system scope). No host step
+ *                  per exchange, so the whole solve is one CUDA graph at
+ *                  world > 1 too. nccl_unique_id is any 128-byte key the ranks
+ *                  share (it names the host rendezvous used during dd_setup,
+ *                  dd_refactor and dd_destroy: POSIX shared memory).
+ *   DD_COMM_LOCAL  the same peer-memory transport with the ranks as contexts
+ *                  of ONE process (one per GPU, or several sharing a GPU),
+ *                  each created and driven by its own host thread; mailboxes
+ *                  are shared as plain device pointers (devices must be peer-
+ *                  accessible). nccl_unique_id is any 128-byte key.
+ * With either peer transport dd_setup, dd_spmv, dd_bicgstab, dd_solve_host,
+ * dd_refactor and dd_destroy are collective. A device-side wait that sees no
+ * progress for DD_PEER_TIMEOUT_S seconds (default 120) stops the solve and the
+ * call returns DD_E_NCCL; a host rendezvous that waits longer than that fails
+ * the same way. Setup and refactor status is agreed over the ranks (every rank
+ * returns the same status). */
 #define DD_COMM_NCCL 0
 #define DD_COMM_LOCAL 1
+#define DD_COMM_IPC 2
 
 /* Borrowed scalar CSR matrix (the paper's CSR half, P:110,
  * P:279-305): the same pipeline with 1x1 blocks. vals[nnz]; vectors passed

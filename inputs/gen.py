@@ -291,6 +291,43 @@ def random_block_grid(nx: int, ny: int, nz: int, seed: int, dominance: float = 1
     return row_ptr, col_idx, vals.reshape(-1)
 
 
+def half_coupled_bsr3(n_sub: int, P: int, seed: int, dominance: float = 1.0, h: int = 0):
+    """n_sub chunks of P block rows; inside each chunk, row i >= h (default P // 2)
+    couples to row i - h (both directions) and nothing else, so the first h
+    rows of a chunk form one wide level without lower blocks (a long run of
+    block-free level-0 records in the factor stream) followed by one level
+    with one lower block per row. Random full 3x3 blocks, block-row dominant.
+    Used with contiguous chunk partitions of P rows (the ring-release tests)."""
+    rng = np.random.default_rng(seed)
+    n = n_sub * P
+    h = h or P // 2
+    rows, cols = [], []
+    for c in range(n_sub):
+        for i in range(P):
+            g = c * P + i
+            nb = [g]
+            if i >= h:
+                nb.append(g - h)
+            if i < P - h and i + h < P:
+                nb.append(g + h)
+            for j in sorted(nb):
+                rows.append(g)
+                cols.append(j)
+    rows = np.array(rows)
+    col_idx = np.array(cols, dtype=np.int32)
+    row_ptr = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))]).astype(np.int64)
+    vals = rng.uniform(-1.0, 1.0, (col_idx.shape[0], 3, 3))
+    diag = col_idx == rows
+    absrow = np.zeros((n, 3))
+    np.add.at(absrow, rows[~diag], np.abs(vals[~diag]).sum(axis=2))
+    d3 = np.arange(3)
+    dv = vals[diag]
+    absrow += np.abs(dv).sum(axis=2) - np.abs(dv[:, d3, d3])
+    dv[:, d3, d3] = absrow + dominance
+    vals[diag] = dv
+    return row_ptr, col_idx, vals.reshape(-1)
+
+
 def stencil27_pattern(nx: int, ny: int, nz: int):
     """27-point pattern (all neighbours within distance 1 in each coordinate),
     natural order, columns ascending: up to 13 strictly-lower blocks per row."""

@@ -25,7 +25,7 @@ if os.environ.get("DD_LIB"):
 
 DD_LEVELSET, DD_SPINLOOP, DD_DIRECT, DD_UNFUSED = 1, 2, 4, 8
 DD_PART_CHUNKS, DD_PART_BFS = 0, 1
-DD_COMM_NCCL, DD_COMM_LOCAL = 0, 1
+DD_COMM_NCCL, DD_COMM_LOCAL, DD_COMM_IPC = 0, 1, 2
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",
           "DD_E_SINGULAR_PIVOT", "DD_E_SUBDOMAIN_TOO_LARGE", "DD_E_GRID_NOT_DIVISIBLE", "DD_E_CUDA",
           "DD_E_NCCL", "DD_E_OOM", "DD_E_BREAKDOWN", "DD_E_MAXITER", "DD_E_NO_DEVICE"]
@@ -117,13 +117,35 @@ def _stream(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
-def _dev_vec(t, n, name):
+def _dev_vec(t, n, name, align16=False):
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor")
     if t.numel() < n:
         raise ValueError(f"{name}: needs {n} elements, has {t.numel()}")
+    if align16 and t.data_ptr() % 16:
+        # the ring kernels stream r with 16-byte bulk copies (dd.h); a view at
+        # an odd element offset is only 8-byte aligned
+        raise ValueError(f"{name}: data pointer must be 16-byte aligned (view at an odd element offset?)")
     return t.data_ptr()
+
+
+def _host_vec(a, n, name, writable=False):
+    """A C-contiguous float64 numpy array of at least n elements (the C side
+    reads or writes exactly n)."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+        raise TypeError(f"{name}: expected a C-contiguous float64 numpy array")
+    if writable and not a.flags.writeable:
+        raise ValueError(f"{name}: array is read-only")
+    if a.size < n:
+        raise ValueError(f"{name}: needs {n} elements, has {a.size}")
+    return a.ctypes.data
+
+
+def comm_key() -> bytes:
+    """A fresh 128-byte key naming a peer-transport group (comm="ipc" / "local");
+    rank 0 draws it and the caller broadcasts it."""
+    return os.urandom(128)
 
 
 def dd_nccl_unique_id() -> bytes:
@@ -135,9 +157,10 @@ def dd_nccl_unique_id() -> bytes:
 class Context:
     """A dd_ctx*. Build with dd_setup(...)."""
 
-    def __init__(self, handle, N, keep, bs=3):
+    def __init__(self, handle, N, keep, bs=3, nnzb=0):
         self.h = handle
         self.N = N
+        self.nnzb = nnzb
         self.bs = bs  # unknowns per row: 3 (BSR3) or 1 (scalar CSR)
         self._keep = keep
         first, nl = C.c_int64(), C.c_int64()
@@ -156,7 +179,8 @@ class Context:
     # --- compute
     def apply(self, r, z, variant=DD_LEVELSET, stream=None):
         m = self.bs * self.n_local
-        _check(lib().dd_apply_variant(self.h, variant, _dev_vec(r, m, "r"), _dev_vec(z, m, "z"), _stream(stream)))
+        _check(lib().dd_apply_variant(self.h, variant, _dev_vec(r, m, "r", align16=True), _dev_vec(z, m, "z"),
+                                      _stream(stream)))
 
     def spmv(self, x, y, stream=None):
         m = self.bs * self.n_local
@@ -178,29 +202,32 @@ class Context:
         return out
 
     def solve_host(self, b_host: np.ndarray, x_host: np.ndarray, tol=1e-8, max_iter=1000, stream=None):
-        assert b_host.dtype == np.float64 and x_host.dtype == np.float64
+        n = self.bs * self.N
         rep = Report()
-        st = lib().dd_solve_host(self.h, _ptr(b_host), _ptr(x_host), tol, max_iter, C.byref(rep), _stream(stream))
+        st = lib().dd_solve_host(self.h, _host_vec(b_host, n, "b_host"), _host_vec(x_host, n, "x_host", True), tol,
+                                 max_iter, C.byref(rep), _stream(stream))
         if st not in (0, 11, 12):
             _check(st)
         return rep.as_dict()
 
     def permute(self, v_orig_host: np.ndarray, v_reord_dev, stream=None):
-        _check(lib().dd_permute(self.h, _ptr(np.ascontiguousarray(v_orig_host, np.float64)),
+        v = np.ascontiguousarray(v_orig_host, np.float64)
+        _check(lib().dd_permute(self.h, _host_vec(v, self.bs * self.N, "v_orig_host"),
                                 _dev_vec(v_reord_dev, self.bs * self.n_local, "v"), _stream(stream)))
 
     def unpermute(self, v_reord_dev, v_orig_host: np.ndarray, stream=None):
-        _check(lib().dd_unpermute(self.h, _dev_vec(v_reord_dev, self.bs * self.n_local, "v"), _ptr(v_orig_host),
-                                  _stream(stream)))
+        _check(lib().dd_unpermute(self.h, _dev_vec(v_reord_dev, self.bs * self.n_local, "v"),
+                                  _host_vec(v_orig_host, self.bs * self.N, "v_orig_host", True), _stream(stream)))
 
     def refactor(self, vals, stream=None):
         """New block values (original block order, same pattern): host numpy or
         CUDA float64 tensor."""
+        n = 9 * self.nnzb  # dd_refactor reads 9 * nnzb values (BSR3 only)
         if isinstance(vals, np.ndarray):
             vals = np.ascontiguousarray(vals, np.float64)
-            _check(lib().dd_refactor(self.h, _ptr(vals), 0, _stream(stream)))
+            _check(lib().dd_refactor(self.h, _host_vec(vals, n, "vals"), 0, _stream(stream)))
         else:
-            _check(lib().dd_refactor(self.h, _dev_vec(vals, 0, "vals"), 1, _stream(stream)))
+            _check(lib().dd_refactor(self.h, _dev_vec(vals, n, "vals"), 1, _stream(stream)))
 
     # --- introspection
     def partition(self):
@@ -285,14 +312,20 @@ class Context:
 def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=DD_LEVELSET, device=0, rank=0,
              world=1, nccl_id: bytes | None = None, pivot_floor=0.0, host_only=False, n_threads=0,
              enable_refactor=False, partitioner="chunks", comm="nccl", csr=False) -> Context:
-    """world > 1: comm="nccl" (one process per GPU, nccl_id from dd_nccl_unique_id)
-    or comm="local" (ranks are contexts of this process, each created and driven
+    """world > 1: comm="nccl" (one process per GPU, nccl_id from dd_nccl_unique_id),
+    comm="ipc" (one process per GPU on one node, peer-memory transport through
+    CUDA IPC; nccl_id is any 128-byte key the ranks share, e.g. comm_key()) or
+    comm="local" (ranks are contexts of this process, each created and driven
     from its own thread; nccl_id is any 128-byte key the ranks share).
     csr=True: a scalar CSR matrix (vals[nnz]) through dd_setup_csr."""
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
     n = row_ptr.shape[0] - 1
+    b2 = 1 if csr else 9
+    if n < 0 or col_idx.shape[0] != row_ptr[-1] or vals.shape[0] != b2 * col_idx.shape[0]:
+        raise ValueError(f"dd_setup: inconsistent arrays (row_ptr[-1] = {row_ptr[-1] if n >= 0 else None}, "
+                         f"col_idx {col_idx.shape[0]}, vals {vals.shape[0]}, expected {b2} values per block)")
     A = BSR3(n, col_idx.shape[0], _ptr(row_ptr), _ptr(col_idx), _ptr(vals))
     o = Opts()
     g = None
@@ -309,10 +342,10 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     o.n_threads = n_threads
     o.enable_refactor = int(bool(enable_refactor))
     o.partitioner = {"chunks": DD_PART_CHUNKS, "bfs": DD_PART_BFS}[partitioner]
-    o.comm = {"nccl": DD_COMM_NCCL, "local": DD_COMM_LOCAL}[comm]
+    o.comm = {"nccl": DD_COMM_NCCL, "local": DD_COMM_LOCAL, "ipc": DD_COMM_IPC}[comm]
     h = C.c_void_p()
     _check((lib().dd_setup_csr if csr else lib().dd_setup)(C.byref(A), C.byref(o), C.byref(h)))
-    return Context(h, n, keep=(g, idbuf), bs=1 if csr else 3)
+    return Context(h, n, keep=(g, idbuf), bs=1 if csr else 3, nnzb=int(col_idx.shape[0]))
 
 
 def dd_setup_csr(row_ptr, col_idx, vals, **kw) -> Context:

@@ -1,205 +1,26 @@
-// api.cpp -- the C ABI of include/dd.h: context lifetime, device upload,
-// apply / SpMV entry points, the BiCGSTAB driver (Alg. 1, right
-// preconditioning R20) and the NCCL plumbing for world > 1 (sec. 8e).
+// api.cpp -- the C ABI of include/dd.h: context lifetime and setup (host
+// setup -> status agreed over ranks -> device upload -> transport connect),
+// the apply / SpMV entry points and the introspection calls. The BiCGSTAB
+// driver is in solver.cpp, the transports in comm.cpp, dd_refactor in
+// refactor_api.cpp.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
-#include <cstdio>
-#include <chrono>
 #include <cmath>
-#include <condition_variable>
+#include <cstdint>
+#include <cstdio>
 #include <cstring>
-#include <map>
 #include <memory>
-#include <mutex>
 #include <string>
 #include <vector>
 
-#include "dd_internal.h"
-#include "krylov.cuh"
+#include "api_internal.h"
 #include "levels.cuh"
-#include "refactor.cuh"
-
-namespace ddi {
-const char *last_error_c();
-}
 
 using namespace ddi;
 
-#define CK(x)                                                                                   \
-    do {                                                                                        \
-        cudaError_t e_ = (x);                                                                   \
-        if (e_ != cudaSuccess) {                                                                \
-            set_error(std::string(#x) + ": " + cudaGetErrorString(e_));                         \
-            return e_ == cudaErrorMemoryAllocation ? DD_E_OOM : DD_E_CUDA;                      \
-        }                                                                                       \
-    } while (0)
-
-#define NK(x)                                                                                   \
-    do {                                                                                        \
-        ncclResult_t r_ = (x);                                                                  \
-        if (r_ != ncclSuccess) {                                                                \
-            set_error(std::string(#x) + ": " + ncclGetErrorString(r_));                         \
-            return DD_E_NCCL;                                                                   \
-        }                                                                                       \
-    } while (0)
-
 namespace {
-
-struct Workspace {
-    int64_t m = 0;  // bs * n_local
-    double *r = nullptr, *rh = nullptr, *p = nullptr, *v = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr,
-           *t = nullptr, *bd = nullptr, *xd = nullptr;
-    double *sc = nullptr;        // device scalars [S_COUNT]
-    void *partials = nullptr;    // DD [grid * 2]
-    unsigned int *counter = nullptr;
-    double *loc = nullptr;       // [4] rank-local (s, c) pairs
-    double *gathered = nullptr;  // [world * 4]
-    double *h_sc = nullptr;      // pinned [S_COUNT]
-    int *ctl = nullptr;          // device solver control [8]
-    int *h_ctl = nullptr;        // pinned [16]: two snapshots
-    double *d_hist = nullptr;    // device residual history
-    int64_t hist_cap = 0;
-    double *h_tol = nullptr;     // pinned scalar (tolerance upload)
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    double *xg = nullptr;        // ghost rows of the SpMV input [bs * n_ghost]
-    double *sendbuf = nullptr;   // [bs * total send rows]
-    int32_t *d_send_idx = nullptr;
-    std::vector<int64_t> send_off;  // [world + 1]
-    // DD_COMM_LOCAL: "my send data is ready" / "I have copied my peers' data"
-    cudaEvent_t xev_ready = nullptr, xev_done = nullptr;
-    // fused halo (world > 1): the solver's applies write the rows peers need
-    // straight from shared memory (send buffer, or DD_COMM_LOCAL the peer's
-    // ghost block); xev_app: "my fused apply has written", xev_free: "my SpMV
-    // no longer reads my ghost block"
-    bool halo_fuse = false;
-    bool merge_ss = false;  // world > 1: s.s reduced with (t.s, t.t), see enqueue_iteration
-    ddi::HaloOut hout;
-    int32_t *d_hptr = nullptr, *d_hrow = nullptr;
-    double **d_hdst = nullptr;
-    cudaEvent_t xev_app = nullptr, xev_free = nullptr;
-    // CUDA-graph solve loop (one executable graph per solution vector)
-    cudaStream_t cap = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t gexec = nullptr;
-    double *gx = nullptr, *ghist = nullptr;  // the captured body's x and history buffers
-    int64_t g_launches = 0;
-    int *h_max = nullptr;  // pinned
-};
-
-// ---------------------------------------------------------------- DD_COMM_LOCAL
-// Ranks that are contexts of one process. Each exchange: every rank records
-// xev_ready after producing its outgoing data; rendezvous; every rank makes
-// its stream wait on the producers' events and copies device-to-device;
-// records xev_done; rendezvous; every producer's stream waits on its
-// consumers' xev_done before it can overwrite the outgoing buffer. All waits
-// name events recorded before the rendezvous, so the GPU work of all ranks is
-// enqueued before anything waits on it (no cycles).
-struct LocalGroup {
-    int world = 0;
-    std::vector<dd_ctx *> members;
-    std::mutex m;
-    std::condition_variable cv;
-    int arrived = 0, refs = 0;
-    uint64_t gen = 0;
-    bool barrier() {
-        std::unique_lock<std::mutex> lk(m);
-        const uint64_t g = gen;
-        if (++arrived == world) {
-            arrived = 0;
-            ++gen;
-            cv.notify_all();
-            return true;
-        }
-        return cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; });
-    }
-};
-
-std::mutex g_groups_m;
-std::map<std::string, LocalGroup *> g_groups;
-
-LocalGroup *group_of(const dd_ctx *c) { return reinterpret_cast<LocalGroup *>(c->group); }
-
-template <class T>
-dd_status dmalloc(T **p, size_t count) {
-    *p = nullptr;
-    if (count == 0) return DD_OK;
-    CK(cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T)));
-    return DD_OK;
-}
-
-#define TRY(x)                        \
-    do {                              \
-        dd_status s_ = (x);           \
-        if (s_ != DD_OK) return s_;   \
-    } while (0)
-
-Workspace *ws_of(dd_ctx *c) { return reinterpret_cast<Workspace *>(c->dev_ws); }
-
-// Optional per-kernel timing inside dd_bicgstab (dd_profile): CUDA events on
-// the solver's stream around every apply / SpMV / BLAS-1 launch, harvested at
-// the solver's own synchronisation points (no extra host syncs).
-enum { PK_APPLY = 0, PK_SPMV = 1, PK_BLAS = 2 };
-struct Prof {
-    bool on = false;
-    std::vector<cudaEvent_t> pool;
-    size_t used = 0;
-    struct Pend {
-        int kind, iter;
-        cudaEvent_t a, b;
-    };
-    std::vector<Pend> pend;
-    double ms[3] = {0, 0, 0};
-    int64_t n[3] = {0, 0, 0};
-};
-
-Prof *prof_of(dd_ctx *c) {
-    if (!c->prof) c->prof = new Prof();
-    return reinterpret_cast<Prof *>(c->prof);
-}
-
-cudaEvent_t prof_ev(Prof *p) {
-    if (p->used == p->pool.size()) {
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        p->pool.push_back(e);
-    }
-    return p->pool[p->used++];
-}
-
-template <class F>
-dd_status timed(dd_ctx *c, int kind, int iter, cudaStream_t st, F &&launch) {
-    Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
-    if (!p || !p->on) return launch();
-    cudaEvent_t a = prof_ev(p), b = prof_ev(p);
-    cudaEventRecord(a, st);
-    dd_status r = launch();
-    cudaEventRecord(b, st);
-    p->pend.push_back({kind, iter, a, b});
-    return r;
-}
-
-// Harvest after the stream is idle. Launches enqueued past the stopping point
-// return at entry, so only the first n_real[kind] launches of each kind (and,
-// for BLAS-1, those of iterations <= k_last) are counted.
-void prof_collect(dd_ctx *c, const int64_t *n_real, int k_last) {
-    Prof *p = c->prof ? reinterpret_cast<Prof *>(c->prof) : nullptr;
-    if (!p) return;
-    int64_t seen[3] = {0, 0, 0};
-    for (auto &q : p->pend) {
-        const bool real = q.kind == PK_BLAS ? q.iter <= k_last : seen[q.kind] < n_real[q.kind];
-        ++seen[q.kind];
-        float ms = 0.f;
-        if (real && cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
-            p->ms[q.kind] += ms;
-            p->n[q.kind] += 1;
-        }
-    }
-    p->pend.clear();
-    p->used = 0;
-}
-
 // Host -> device copy of a large pageable buffer through two pinned 32 MB
 // staging buffers: an OpenMP memcpy fills one while the DMA engine drains the
 // other (pageable cudaMemcpy runs at ~3 GB/s; this at ~10-20 GB/s).
@@ -257,140 +78,6 @@ dd_status upload_slab(Slab &sl) {
     if (!sl.info.empty())
         CK(cudaMemcpy(sl.d_info, sl.info.data(), sl.info.size() * sizeof(SubInfo), cudaMemcpyHostToDevice));
     std::vector<uint8_t>().swap(sl.bytes);  // device copy is authoritative
-    return DD_OK;
-}
-
-// DD_COMM_LOCAL: join the group named by the 128-byte key; returns once
-// every rank has joined (its workspace is then visible to the peers).
-dd_status local_join(dd_ctx *ctx, const void *key) {
-    LocalGroup *G;
-    {
-        std::lock_guard<std::mutex> lk(g_groups_m);
-        const std::string k(reinterpret_cast<const char *>(key), 128);
-        auto it = g_groups.find(k);
-        if (it == g_groups.end()) {
-            G = new LocalGroup();
-            G->world = ctx->world;
-            G->members.assign(ctx->world, nullptr);
-            g_groups[k] = G;
-        } else {
-            G = it->second;
-        }
-        if (G->world != ctx->world || G->members[ctx->rank]) {
-            set_error("dd_setup: DD_COMM_LOCAL group key reused with another world size or rank");
-            return DD_E_INVALID_ARG;
-        }
-        G->members[ctx->rank] = ctx;
-        ++G->refs;
-        ctx->group = G;
-    }
-    if (!G->barrier()) {
-        set_error("dd_setup: DD_COMM_LOCAL rendezvous timed out (every rank must call dd_setup from its own thread)");
-        return DD_E_NCCL;
-    }
-    // peer access between distinct devices (copies also work without it)
-    for (dd_ctx *q : G->members)
-        if (q->device != ctx->device) {
-            int can = 0;
-            cudaDeviceCanAccessPeer(&can, ctx->device, q->device);
-            if (can && cudaDeviceEnablePeerAccess(q->device, 0) != cudaSuccess) cudaGetLastError();
-        }
-    return DD_OK;
-}
-
-void local_leave(dd_ctx *ctx) {
-    LocalGroup *G = group_of(ctx);
-    if (!G) return;
-    std::lock_guard<std::mutex> lk(g_groups_m);
-    // no live peer may still be copying from this rank's buffers: its copies
-    // precede its last xev_done record
-    for (dd_ctx *q : G->members)
-        if (q && q != ctx && q->dev_ws) {
-            if (ws_of(q)->xev_done) cudaEventSynchronize(ws_of(q)->xev_done);
-            if (ws_of(q)->xev_app) cudaEventSynchronize(ws_of(q)->xev_app);  // fused writes into our ghost block
-        }
-    G->members[ctx->rank] = nullptr;
-    ctx->group = nullptr;
-    if (--G->refs == 0) {
-        for (auto it = g_groups.begin(); it != g_groups.end(); ++it)
-            if (it->second == G) {
-                g_groups.erase(it);
-                break;
-            }
-        delete G;
-    }
-}
-
-#define RENDEZVOUS(G)                                                              \
-    do {                                                                           \
-        if (!(G)->barrier()) {                                                     \
-            set_error("DD_COMM_LOCAL rendezvous timed out (a rank stopped calling)"); \
-            return DD_E_NCCL;                                                      \
-        }                                                                          \
-    } while (0)
-
-// Fused halo lists: for every local subdomain, the rows that
-// peers need (send_rows, ascending per peer) and where they go -- this rank's
-// NCCL send buffer, or with DD_COMM_LOCAL the consuming peer's ghost block
-// directly (peer memory: every member on one device or peer-accessible
-// devices; otherwise the unfused gather + copy is kept). DD_HALO_FUSE=0
-// disables it (A/B measurements and tests).
-dd_status halo_out_build(dd_ctx *ctx) {
-    Workspace *ws = ws_of(ctx);
-    const char *env = getenv("DD_HALO_FUSE");
-    bool fuse = !env || atoi(env) != 0;
-    if (fuse && ctx->comm == DD_COMM_LOCAL) {
-        for (dd_ctx *a : group_of(ctx)->members)
-            for (dd_ctx *b : group_of(ctx)->members) {
-                int can = 1;
-                if (a->device != b->device) cudaDeviceCanAccessPeer(&can, a->device, b->device);
-                if (!can) fuse = false;
-            }
-    }
-    ws->halo_fuse = fuse;
-    if (!fuse) return DD_OK;
-    const int nsl = ctx->sub_last - ctx->sub_first;
-    struct Ent {
-        int32_t sub, row;
-        double *dst;
-    };
-    std::vector<Ent> ents;
-    for (int q = 0; q < ctx->world; ++q) {
-        if (q == ctx->rank || q >= (int)ctx->send_rows.size()) continue;
-        const auto &rows = ctx->send_rows[q];
-        double *base;
-        if (ctx->comm == DD_COMM_LOCAL) {
-            dd_ctx *peer = group_of(ctx)->members[q];
-            base = ws_of(peer)->xg + ctx->bs * peer->recv_off[ctx->rank];
-        } else {
-            base = ws->sendbuf + ctx->bs * ws->send_off[q];
-        }
-        for (size_t p = 0; p < rows.size(); ++p) {
-            const int64_t g = ctx->row_first + rows[p];  // reordered global row
-            const int32_t s = (int32_t)(std::upper_bound(ctx->sub_ptr.begin() + ctx->sub_first,
-                                                         ctx->sub_ptr.begin() + ctx->sub_last + 1, g) -
-                                        ctx->sub_ptr.begin()) - 1;
-            ents.push_back({s - ctx->sub_first, (int32_t)(g - ctx->sub_ptr[s]), base + ctx->bs * (int64_t)p});
-        }
-    }
-    std::stable_sort(ents.begin(), ents.end(), [](const Ent &a, const Ent &b) { return a.sub < b.sub; });
-    std::vector<int32_t> ptr(nsl + 1, 0), row(ents.size());
-    std::vector<double *> dst(ents.size());
-    for (size_t e = 0; e < ents.size(); ++e) {
-        ++ptr[ents[e].sub + 1];
-        row[e] = ents[e].row;
-        dst[e] = ents[e].dst;
-    }
-    for (int s = 0; s < nsl; ++s) ptr[s + 1] += ptr[s];
-    TRY(dmalloc(&ws->d_hptr, ptr.size()));
-    TRY(dmalloc(&ws->d_hrow, std::max<size_t>(1, row.size())));
-    TRY(dmalloc(&ws->d_hdst, std::max<size_t>(1, dst.size())));
-    CK(cudaMemcpy(ws->d_hptr, ptr.data(), ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    if (!row.empty()) {
-        CK(cudaMemcpy(ws->d_hrow, row.data(), row.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(ws->d_hdst, dst.data(), dst.size() * sizeof(double *), cudaMemcpyHostToDevice));
-    }
-    ws->hout = ddi::HaloOut{ws->d_hptr, ws->d_hrow, ws->d_hdst};
     return DD_OK;
 }
 
@@ -458,16 +145,12 @@ dd_status tune_solver_variant(dd_ctx *ctx) {
     return rc;
 }
 
-dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
+
+// Device part of dd_setup (rank-local, no collective): launch shapes, slab
+// and SpMV operand upload, the solver workspace and the transport buffers.
+dd_status device_setup(dd_ctx *ctx) {
     const double t0 = now_ms();
     CK(cudaSetDevice(ctx->device));
-    if (ctx->world > 1 && ctx->comm == DD_COMM_NCCL) {
-        ncclComm_t comm;
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_id, sizeof id);
-        NK(ncclCommInitRank(&comm, ctx->world, id, ctx->rank));
-        ctx->nccl = comm;
-    }
     static const bool trace = getenv("DD_SETUP_TRACE") != nullptr;
     auto tr = [&](const char *what) {
         if (trace) fprintf(stderr, "[dd setup] %-22s %9.1f ms\n", what, now_ms() - t0);
@@ -543,7 +226,6 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     TRY(dmalloc(&ws->counter, 4));
     CK(cudaMemset(ws->counter, 0, 4 * sizeof(unsigned int)));
     TRY(dmalloc(&ws->loc, 6));
-    TRY(dmalloc(&ws->gathered, 6 * (size_t)std::max(1, ctx->world)));
     {
         // world > 1: ||s||^2 joins the (t.s, t.t) collective -- three
         // reduction points per iteration instead of four (DD_MERGE_SS=0: four)
@@ -558,245 +240,21 @@ dd_status device_setup(dd_ctx *ctx, const void *nccl_id) {
     CK(cudaMallocHost(reinterpret_cast<void **>(&ws->h_max), sizeof(int)));
     CK(cudaEventCreateWithFlags(&ws->ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ws->ev[1], cudaEventDisableTiming));
-    // halo buffers
-    const int64_t ng = (int64_t)ctx->ghost_rows.size();
-    TRY(dmalloc(&ws->xg, std::max<int64_t>(1, ctx->bs * ng)));
-    ws->send_off.assign(ctx->world + 1, 0);
-    std::vector<int32_t> sidx;
-    for (int q = 0; q < ctx->world; ++q) {
-        if (q < (int)ctx->send_rows.size()) sidx.insert(sidx.end(), ctx->send_rows[q].begin(), ctx->send_rows[q].end());
-        ws->send_off[q + 1] = (int64_t)sidx.size();
-    }
-    TRY(dmalloc(&ws->sendbuf, std::max<size_t>(1, ctx->bs * sidx.size())));
-    TRY(dmalloc(&ws->d_send_idx, std::max<size_t>(1, sidx.size())));
-    if (!sidx.empty())
-        CK(cudaMemcpy(ws->d_send_idx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // halo buffers / peer mailbox
+    TRY(comm_alloc(ctx));
     CK(cudaDeviceSynchronize());
     tr("workspace");
-    if (ctx->world > 1 && ctx->comm == DD_COMM_LOCAL) {
-        CK(cudaEventCreateWithFlags(&ws->xev_ready, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ws->xev_done, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ws->xev_app, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ws->xev_free, cudaEventDisableTiming));
-        TRY(local_join(ctx, nccl_id));
-    }
-    if (ctx->world > 1) TRY(halo_out_build(ctx));
-    TRY(tune_solver_variant(ctx));
     ctx->setup_ms[5] = now_ms() - t0;
     return DD_OK;
 }
 
+}  // namespace
+
+namespace ddi {
 ddk::RedArgs red_args(dd_ctx *c) {
     Workspace *ws = ws_of(c);
     return ddk::RedArgs{reinterpret_cast<ddk::DD *>(ws->partials), ws->counter, ws->sc, ws->loc,
                         c->world <= 1 ? 1 : 0, nullptr, nullptr, 0, 0};
-}
-
-// world > 1: all-gather the rank-local (s, c) pairs and finalize in rank order.
-// DD_COMM_LOCAL all-gather of the ranks' loc[0 .. 2nv) into gathered[q * 2nv]
-dd_status local_allgather(dd_ctx *c, int nv, cudaStream_t st) {
-    LocalGroup *G = group_of(c);
-    Workspace *ws = ws_of(c);
-    const size_t bytes = 2 * (size_t)nv * sizeof(double);
-    CK(cudaEventRecord(ws->xev_ready, st));
-    RENDEZVOUS(G);
-    for (int q = 0; q < c->world; ++q) {
-        Workspace *pw = ws_of(G->members[q]);
-        if (q != c->rank) CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
-        CK(cudaMemcpyAsync(ws->gathered + 2 * (size_t)nv * q, pw->loc, bytes, cudaMemcpyDefault, st));
-    }
-    CK(cudaEventRecord(ws->xev_done, st));
-    RENDEZVOUS(G);
-    for (int q = 0; q < c->world; ++q)
-        if (q != c->rank) CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_done, 0));
-    return DD_OK;
-}
-
-// DD_COMM_LOCAL halo: copy every peer's send segment for this rank into xg
-dd_status local_halo(dd_ctx *c, cudaStream_t st) {
-    LocalGroup *G = group_of(c);
-    Workspace *ws = ws_of(c);
-    CK(cudaEventRecord(ws->xev_ready, st));
-    RENDEZVOUS(G);
-    for (int q = 0; q < c->world; ++q) {
-        if (q == c->rank) continue;
-        const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
-        if (!rn) continue;
-        Workspace *pw = ws_of(G->members[q]);
-        CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
-        CK(cudaMemcpyAsync(ws->xg + c->bs * ro, pw->sendbuf + c->bs * pw->send_off[c->rank], c->bs * rn * sizeof(double),
-                           cudaMemcpyDefault, st));
-    }
-    CK(cudaEventRecord(ws->xev_done, st));
-    RENDEZVOUS(G);
-    for (int q = 0; q < c->world; ++q)
-        if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
-            CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_done, 0));
-    return DD_OK;
-}
-
-dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaStream_t st) {
-    if (c->world <= 1) return DD_OK;
-    Workspace *ws = ws_of(c);
-    if (c->comm == DD_COMM_LOCAL)
-        TRY(local_allgather(c, nv, st));
-    else
-        NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, reinterpret_cast<ncclComm_t>(c->nccl), st));
-    ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ra, op, st);
-    ++c->n_launches;
-    return DD_OK;
-}
-
-// halo exchange of the SpMV input x (local rows) into ws->xg. packed: x was
-// produced by a fused-halo apply (apply_halo), which already wrote the rows
-// peers need (NCCL: into the send buffer; DD_COMM_LOCAL: into the peers'
-// ghost blocks -- only the ordering remains)
-dd_status halo(dd_ctx *c, const double *x, cudaStream_t st, bool packed) {
-    if (c->world <= 1) return DD_OK;
-    Workspace *ws = ws_of(c);
-    packed = packed && ws->halo_fuse;
-    const int64_t ns = ws->send_off[c->world];
-    if (ns && !packed) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
-    if (c->comm == DD_COMM_LOCAL) {
-        if (!packed) return local_halo(c, st);
-        // every producer has recorded xev_app after its fused apply
-        LocalGroup *G = group_of(c);
-        RENDEZVOUS(G);
-        for (int q = 0; q < c->world; ++q)
-            if (q != c->rank && c->recv_off[q + 1] > c->recv_off[q])
-                CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_app, 0));
-        return DD_OK;
-    }
-    auto comm = reinterpret_cast<ncclComm_t>(c->nccl);
-    NK(ncclGroupStart());
-    for (int q = 0; q < c->world; ++q) {
-        if (q == c->rank) continue;
-        const int64_t so = ws->send_off[q], sn = ws->send_off[q + 1] - so;
-        const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
-        if (sn) NK(ncclSend(ws->sendbuf + c->bs * so, c->bs * sn, ncclDouble, q, comm, st));
-        if (rn) NK(ncclRecv(ws->xg + c->bs * ro, c->bs * rn, ncclDouble, q, comm, st));
-    }
-    NK(ncclGroupEnd());
-    return DD_OK;
-}
-
-dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, const ddk::RedArgs &ra,
-                    cudaStream_t st, bool packed = false) {
-    TRY(halo(c, x, st, packed));
-    ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, ra, st);
-    // DD_COMM_LOCAL with the fused halo: peers' next fused applies write this
-    // rank's ghost block only after this SpMV has read it
-    if (c->world > 1 && c->comm == DD_COMM_LOCAL && ws_of(c)->halo_fuse) CK(cudaEventRecord(ws_of(c)->xev_free, st));
-    return DD_OK;
-}
-
-// The solver's apply r -> z with the fused halo epilogue (world > 1): the rows
-// peers read in the following SpMV leave from shared memory. DD_COMM_LOCAL:
-// the writes land in the peers' ghost blocks, so they wait until each
-// consumer's previous SpMV has read its block (xev_free), and xev_app tells
-// the consumers the rows are there.
-dd_status apply_halo(dd_ctx *c, const double *r, double *z, cudaStream_t st, const int *skip) {
-    Workspace *ws = ws_of(c);
-    const bool fuse = c->world > 1 && ws->halo_fuse;
-    const bool local = fuse && c->comm == DD_COMM_LOCAL;
-    if (local) {
-        LocalGroup *G = group_of(c);
-        RENDEZVOUS(G);
-        for (int q = 0; q < c->world; ++q)
-            if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
-                CK(cudaStreamWaitEvent(st, ws_of(G->members[q])->xev_free, 0));
-    }
-    TRY(apply_launch(c, fuse ? DD_LEVELSET : c->solver_variant, r, z, reinterpret_cast<void *>(st), skip,
-                     fuse ? &ws->hout : nullptr));
-    if (local) CK(cudaEventRecord(ws->xev_app, st));
-    return DD_OK;
-}
-
-dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
-    Workspace *ws = ws_of(c);
-    CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return DD_OK;
-}
-
-// device copies of the refactor maps (allocated at the first dd_refactor)
-struct RfState {
-    int32_t *SubLev = nullptr, *LevPtr = nullptr, *LevRows = nullptr, *Wcol = nullptr, *UpdQ = nullptr,
-            *UpdT = nullptr, *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
-    int64_t *Wrp = nullptr, *Wdiag = nullptr, *Uptr = nullptr, *Lrp = nullptr, *Urp = nullptr, *Loff = nullptr,
-            *Uoff = nullptr, *Doff = nullptr, *Wsrc = nullptr, *Esrc = nullptr;
-    double *W = nullptr, *Dinv = nullptr, *stage = nullptr;
-    unsigned long long *bad = nullptr;
-    unsigned long long *h_bad = nullptr;
-};
-
-template <class T>
-dd_status upload_vec(T **d, const std::vector<T> &h) {
-    TRY(dmalloc(d, std::max<size_t>(1, h.size())));
-    if (!h.empty()) CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
-    return DD_OK;
-}
-
-dd_status refactor_init(dd_ctx *c) {
-    if (c->rf) return DD_OK;
-    auto *rf = new RfState();
-    c->rf = rf;
-    TRY(upload_vec(&rf->SubLev, c->SubLev));
-    TRY(upload_vec(&rf->LevPtr, c->LevPtr));
-    TRY(upload_vec(&rf->LevRows, c->LevRows));
-    TRY(upload_vec(&rf->Wcol, c->Wcol));
-    TRY(upload_vec(&rf->UpdQ, c->UpdQ));
-    TRY(upload_vec(&rf->UpdT, c->UpdT));
-    TRY(upload_vec(&rf->Lst, c->SlabLst));
-    TRY(upload_vec(&rf->Ust, c->SlabUst));
-    TRY(upload_vec(&rf->Dst, c->SlabDst));
-    TRY(upload_vec(&rf->Wrp, c->Wrp));
-    TRY(upload_vec(&rf->Wdiag, c->Wdiag));
-    TRY(upload_vec(&rf->Uptr, c->Uptr));
-    TRY(upload_vec(&rf->Lrp, c->Lrp));
-    TRY(upload_vec(&rf->Urp, c->Urp));
-    TRY(upload_vec(&rf->Loff, c->SlabLoff));
-    TRY(upload_vec(&rf->Uoff, c->SlabUoff));
-    TRY(upload_vec(&rf->Doff, c->SlabDoff));
-    TRY(upload_vec(&rf->Wsrc, c->Wsrc));
-    // sliced-ELL slot -> original block index (-1 = padding), same layout as device_setup
-    {
-        const int64_t nl = c->n_local;
-        const auto &S = c->spmv;
-        std::vector<int64_t> es(S.n_slots, -1);
-        int64_t base = 0;
-        for (int64_t s = 0; s < S.n_slices; ++s) {
-            int64_t K = 0;
-            for (int64_t li = 32 * s; li < std::min(nl, 32 * s + 32); ++li) K = std::max(K, c->Arp[li + 1] - c->Arp[li]);
-            for (int lane = 0; lane < 32; ++lane) {
-                const int64_t li = 32 * s + lane;
-                if (li >= nl) break;
-                for (int64_t k = 0; k < c->Arp[li + 1] - c->Arp[li]; ++k) es[base + 32 * k + lane] = c->Asrc[c->Arp[li] + k];
-            }
-            base += 32 * K;
-        }
-        TRY(upload_vec(&rf->Esrc, es));
-    }
-    TRY(dmalloc(&rf->W, 9 * std::max<size_t>(1, c->Wsrc.size())));
-    TRY(dmalloc(&rf->Dinv, 9 * std::max<int64_t>(1, c->n_local)));
-    TRY(dmalloc(&rf->stage, 9 * std::max<int64_t>(1, c->nnzb_A)));
-    TRY(dmalloc(&rf->bad, 1));
-    CK(cudaMallocHost(reinterpret_cast<void **>(&rf->h_bad), sizeof(unsigned long long)));
-    return DD_OK;
-}
-
-void refactor_free(dd_ctx *c) {
-    auto *rf = reinterpret_cast<RfState *>(c->rf);
-    if (!rf) return;
-    for (void *p : {(void *)rf->SubLev, (void *)rf->LevPtr, (void *)rf->LevRows, (void *)rf->Wcol, (void *)rf->UpdQ,
-                    (void *)rf->UpdT, (void *)rf->Lst, (void *)rf->Ust, (void *)rf->Dst, (void *)rf->Wrp,
-                    (void *)rf->Wdiag, (void *)rf->Uptr, (void *)rf->Lrp, (void *)rf->Urp, (void *)rf->Loff,
-                    (void *)rf->Uoff, (void *)rf->Doff, (void *)rf->Wsrc, (void *)rf->Esrc, (void *)rf->W,
-                    (void *)rf->Dinv, (void *)rf->stage, (void *)rf->bad})
-        cudaFree(p);
-    cudaFreeHost(rf->h_bad);
-    delete rf;
-    c->rf = nullptr;
 }
 
 bool usable(dd_ctx *c) {
@@ -811,7 +269,15 @@ bool usable(dd_ctx *c) {
     return true;
 }
 
-}  // namespace
+dd_status spmv_mode(dd_ctx *c, int mode, const double *x, double *y, const double *aux, const ddk::RedArgs &ra,
+                    cudaStream_t st, bool packed, const int *skip) {
+    TRY(halo(c, x, st, packed, skip));
+    ddk::launch_spmv(mode, c, x, ws_of(c)->xg, y, aux, ra, st);
+    TRY(halo_consumed(c, st, skip));
+    return DD_OK;
+}
+
+}  // namespace ddi
 
 extern "C" {
 
@@ -820,7 +286,11 @@ const char *dd_last_error(void) { return last_error_c(); }
 dd_status dd_nccl_unique_id(void *out128) {
     if (!out128) return DD_E_INVALID_ARG;
     ncclUniqueId id;
-    NK(ncclGetUniqueId(&id));
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        return DD_E_NCCL;
+    }
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     std::memcpy(out128, &id, sizeof id);
     return DD_OK;
@@ -858,7 +328,7 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out, 
     ctx->world = std::max(1, o->world);
     ctx->host_only = o->host_only != 0;
     ctx->comm = o->comm;
-    if (ctx->comm != DD_COMM_NCCL && ctx->comm != DD_COMM_LOCAL) {
+    if (ctx->comm != DD_COMM_NCCL && ctx->comm != DD_COMM_LOCAL && ctx->comm != DD_COMM_IPC) {
         set_error("dd_setup: unknown comm");
         delete ctx;
         return DD_E_INVALID_ARG;
@@ -876,8 +346,17 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out, 
             return DD_E_NO_DEVICE;
         }
     }
+    // world > 1: the status is agreed over the ranks after every step that
+    // can fail on one rank only (a singular pivot in its subdomains, a
+    // launch shape that does not fit), so no rank is left waiting in a
+    // collective its peers never reach
     dd_status st = host_setup(ctx, A, o);
-    if (st == DD_OK && !ctx->host_only) st = device_setup(ctx, o->nccl_unique_id);
+    if (!ctx->host_only) {
+        st = comm_begin(ctx, o->nccl_unique_id, st);
+        if (st == DD_OK) st = comm_agree(ctx, device_setup(ctx));
+        if (st == DD_OK) st = comm_connect(ctx);
+        if (st == DD_OK) st = tune_solver_variant(ctx);
+    }
     if (st != DD_OK) {
         const std::string msg = last_error_c();
         dd_destroy(ctx);
@@ -893,7 +372,7 @@ void dd_destroy(dd_ctx *c) {
     if (!c->host_only) {
         cudaSetDevice(c->device);
         cudaDeviceSynchronize();
-        local_leave(c);
+        comm_end(c);  // peer transports: every rank idle before the mailboxes go
         for (Slab *sl : {&c->slab_lvl, &c->slab_spin}) {
             cudaFree(sl->d_bytes);
             cudaFree(sl->d_info);
@@ -905,8 +384,17 @@ void dd_destroy(dd_ctx *c) {
         cudaFree(c->d_stage);
         if (Workspace *ws = ws_of(c)) {
             for (double *q : {ws->r, ws->rh, ws->p, ws->v, ws->ph, ws->s, ws->sh, ws->t, ws->bd, ws->xd, ws->sc,
-                              ws->loc, ws->gathered, ws->xg, ws->sendbuf})
+                              ws->loc, ws->gathered, ws->sendbuf})
                 cudaFree(q);
+            if (!ws->box) cudaFree(ws->xg);
+            cudaFree(ws->box);
+            cudaFree(ws->d_boxes);
+            cudaFree(ws->seq);
+            cudaFree(ws->perr);
+            cudaFree(ws->d_send_to);
+            cudaFree(ws->d_recv_from);
+            cudaFree(ws->d_put_rows);
+            cudaFree(ws->d_put_dst);
             cudaFree(ws->partials);
             cudaFree(ws->counter);
             cudaFree(ws->ctl);
@@ -919,8 +407,6 @@ void dd_destroy(dd_ctx *c) {
             if (ws->cap) cudaStreamDestroy(ws->cap);
             for (auto e : ws->ev)
                 if (e) cudaEventDestroy(e);
-            for (auto e : {ws->xev_ready, ws->xev_done, ws->xev_app, ws->xev_free})
-                if (e) cudaEventDestroy(e);
             cudaFree(ws->d_send_idx);
             cudaFree(ws->d_hptr);
             cudaFree(ws->d_hrow);
@@ -928,12 +414,8 @@ void dd_destroy(dd_ctx *c) {
             cudaFreeHost(ws->h_sc);
             delete ws;
         }
-        if (c->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(c->nccl));
         refactor_free(c);
-        if (c->prof) {
-            for (auto e : reinterpret_cast<Prof *>(c->prof)->pool) cudaEventDestroy(e);
-            delete reinterpret_cast<Prof *>(c->prof);
-        }
+        prof_free(c);
     }
     delete c;
 }
@@ -951,6 +433,13 @@ dd_status dd_apply_variant(dd_ctx *c, int32_t variant, const double *r, double *
         set_error("dd_apply: NULL vector");
         return DD_E_INVALID_ARG;
     }
+    // the ring kernels stream r (and, unfused, z) with 16-byte bulk copies
+    const bool ring = variant != DD_DIRECT;
+    if (ring && (((uintptr_t)r & 15) || (variant == DD_UNFUSED && ((uintptr_t)z & 15)))) {
+        set_error("dd_apply: vectors must be 16-byte aligned (dd.h)");
+        return DD_E_INVALID_ARG;
+    }
+    DEVICE_GUARD(c);
     return apply_launch(c, variant, r, z, stream);
 }
 
@@ -960,246 +449,16 @@ dd_status dd_apply(dd_ctx *c, const double *r, double *z, void *stream) {
 
 dd_status dd_spmv(dd_ctx *c, const double *x, double *y, void *stream) {
     if (!usable(c)) return DD_E_INVALID_ARG;
+    DEVICE_GUARD(c);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, y, nullptr, red_args(c), st));
     CK(cudaGetLastError());
     return DD_OK;
 }
 
-// One Alg. 1 iteration (both half steps). k > 0: the host's iteration index;
-// k < 0: graph mode, the kernels read it from ctl[C_ITER].
-dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaStream_t st) {
-    Workspace *ws = ws_of(c);
-    const int64_t m = ws->m;
-    ra.k = k;
-    TRY(timed(c, PK_BLAS, k, st, [&] {
-        ddk::launch_update_p(c, m, k < 0 ? -1 : (k == 1), ws->r, ws->v, ws->p, ws->sc, ws->ctl, st);
-        return DD_OK;
-    }));
-    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->p, ws->ph, st, ws->ctl); }));
-    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_SIGMA, ws->ph, ws->v, ws->rh, ra, st, true); }));
-    TRY(reduce_across(c, 1, ddk::FIN_ALPHA, ra, st));
-    // world > 1 (merge_ss): the rank-local s.s waits in loc[4..5] and joins
-    // the (t.s, t.t) collective; the half-step test is then taken after the
-    // second apply and SpMV, which are wasted only in a solve's last
-    // iteration -- the iterates are unchanged (tested bitwise)
-    ddk::RedArgs ra_s = ra;
-    if (ws->merge_ss) ra_s.slot = 2;
-    TRY(timed(c, PK_BLAS, k, st, [&] {
-        ddk::launch_update_s(c, m, ws->r, ws->v, ws->s, ra_s, st);
-        return DD_OK;
-    }));
-    if (!ws->merge_ss) {
-        TRY(reduce_across(c, 1, ddk::FIN_SS, ra, st));
-        ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
-    }
-    TRY(timed(c, PK_APPLY, k, st, [&] { return apply_halo(c, ws->s, ws->sh, st, ws->ctl); }));
-    TRY(timed(c, PK_SPMV, k, st, [&] { return spmv_mode(c, ddk::SPMV_TS_TT, ws->sh, ws->t, ws->s, ra, st, true); }));
-    if (ws->merge_ss) {
-        TRY(reduce_across(c, 3, ddk::FIN_SS_OMEGA, ra, st));
-        ddk::launch_update_x_half(c, m, ws->ph, x, ws->sc, ws->ctl, st);
-    } else {
-        TRY(reduce_across(c, 2, ddk::FIN_OMEGA, ra, st));
-    }
-    TRY(timed(c, PK_BLAS, k, st, [&] {
-        ddk::launch_update_xr(c, m, ws->ph, ws->sh, ws->s, ws->t, ws->rh, x, ws->r, ra, st);
-        return DD_OK;
-    }));
-    TRY(reduce_across(c, 2, ddk::FIN_RHO, ra, st));
-    return DD_OK;
-}
-
-// CUDA-graph solve loop: the iteration body captured once per
-// solution vector under a conditional WHILE node, so a whole solve is one
-// graph launch -- no host round trip per iteration or batch. Used for
-// world == 1 when per-kernel profiling is off (DD_GRAPH=0 disables it).
-dd_status graph_solve(dd_ctx *c, const ddk::RedArgs &ra, double *x, int32_t max_iter, cudaStream_t st,
-                      int64_t *launches_per_iter) {
-    Workspace *ws = ws_of(c);
-    if (!ws->gexec || ws->gx != x || ws->ghist != ws->d_hist) {
-        if (ws->gexec) cudaGraphExecDestroy(ws->gexec);
-        if (ws->graph) cudaGraphDestroy(ws->graph);
-        ws->gexec = nullptr;
-        ws->graph = nullptr;
-        if (!ws->cap) CK(cudaStreamCreateWithFlags(&ws->cap, cudaStreamNonBlocking));
-        CK(cudaGraphCreate(&ws->graph, 0));
-        cudaGraphConditionalHandle h;
-        CK(cudaGraphConditionalHandleCreate(&h, ws->graph, 1, cudaGraphCondAssignDefault));
-        cudaGraphNodeParams p = {};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = h;
-        p.conditional.type = cudaGraphCondTypeWhile;
-        p.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, ws->graph, nullptr, 0, &p));
-        cudaGraph_t body = p.conditional.phGraph_out[0];
-        const int64_t n0 = c->n_launches;
-        CK(cudaStreamBeginCaptureToGraph(ws->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        ddk::launch_iter_head(ws->ctl, ws->cap);
-        dd_status e = enqueue_iteration(c, ra, -1, x, ws->cap);
-        ddk::launch_iter_tail(ws->ctl, h, ws->cap);
-        cudaGraph_t out = nullptr;
-        const cudaError_t ce = cudaStreamEndCapture(ws->cap, &out);
-        if (e != DD_OK) return e;
-        if (ce != cudaSuccess) {
-            set_error(std::string("dd_bicgstab: graph capture failed: ") + cudaGetErrorString(ce));
-            return DD_E_CUDA;
-        }
-        ws->g_launches = c->n_launches - n0;
-        c->n_launches = n0;
-        CK(cudaGraphInstantiate(&ws->gexec, ws->graph, 0));
-        ws->gx = x;
-        ws->ghist = ws->d_hist;
-    }
-    *ws->h_max = max_iter;
-    CK(cudaMemcpyAsync(ws->ctl + ddk::C_MAX, ws->h_max, sizeof(int), cudaMemcpyHostToDevice, st));
-    CK(cudaGraphLaunch(ws->gexec, st));
-    *launches_per_iter = ws->g_launches;
-    return DD_OK;
-}
-
-dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t max_iter, double *hist,
-                      dd_report *rep, void *stream) {
-    if (!usable(c)) return DD_E_INVALID_ARG;
-    if (!(tol > 0) || max_iter < 1) {
-        set_error("dd_bicgstab: tol must be > 0 and max_iter >= 1");
-        return DD_E_INVALID_ARG;
-    }
-    const double t0 = now_ms();
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    Workspace *ws = ws_of(c);
-    const int64_t m = ws->m;
-    if (ws->hist_cap < 2 * (int64_t)max_iter + 1) {
-        cudaFree(ws->d_hist);
-        ws->d_hist = nullptr;
-        ws->hist_cap = 0;
-        TRY(dmalloc(&ws->d_hist, 2 * (size_t)max_iter + 1));
-        ws->hist_cap = 2 * (int64_t)max_iter + 1;
-    }
-    CK(cudaMemsetAsync(ws->ctl, 0, 8 * sizeof(int), st));
-    *ws->h_tol = tol;
-    CK(cudaMemcpyAsync(ws->sc + ddk::S_TOL, ws->h_tol, sizeof(double), cudaMemcpyHostToDevice, st));
-    ddk::RedArgs ra = red_args(c);
-    ra.ctl = ws->ctl;
-    ra.hist = ws->d_hist;
-    ra.k = 0;
-    const ddk::RedArgs ra_plain = red_args(c);
-
-    // r = b - A x0; rh = r; rho_1 = ||r0||^2; thr = tol ||r0|| (FIN_INIT)
-    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, ra_plain, st));
-    ddk::launch_init_r(c, m, b, ws->t, ws->r, ws->rh, ra, st);
-    TRY(reduce_across(c, 1, ddk::FIN_INIT, ra, st));
-
-    // Alg. 1 iterations, enqueued in batches; every kernel returns at entry
-    // once the device-side control has stopped. The host looks at the control
-    // word one batch behind, so the GPU never idles on a half-step decision;
-    // every rank waits on the same batch, so all ranks stop together.
-    constexpr int BATCH = 2;
-    int k_enq = 0, j = 0;
-    static const bool graphs_env = !getenv("DD_GRAPH") || atoi(getenv("DD_GRAPH")) != 0;
-    // world == 1 only: NCCL calls are capturable, but that path is not exercised on this pool
-    const bool use_graph = graphs_env && c->world <= 1 && !(c->prof && reinterpret_cast<Prof *>(c->prof)->on);
-    int64_t g_per_iter = 0;
-    if (use_graph) TRY(graph_solve(c, ra, x, max_iter, st, &g_per_iter));
-    for (bool stop = use_graph; !stop; ++j) {
-        for (int q = 0; q < BATCH && k_enq < max_iter; ++q) {
-            const int k = ++k_enq;
-            ra.k = k;
-            TRY(enqueue_iteration(c, ra, k, x, st));
-        }
-        int *snap = ws->h_ctl + 8 * (j % 2);
-        CK(cudaMemcpyAsync(snap, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(ws->ev[j % 2], st));
-        if (j >= 1) {
-            CK(cudaEventSynchronize(ws->ev[(j - 1) % 2]));
-            if (ws->h_ctl[8 * ((j - 1) % 2) + ddk::C_STATE] != ddk::ST_RUN) stop = true;
-        }
-        if (k_enq >= max_iter) stop = true;
-    }
-    CK(cudaMemcpyAsync(ws->h_ctl, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const int state = ws->h_ctl[ddk::C_STATE], kf = ws->h_ctl[ddk::C_K], nh = ws->h_ctl[ddk::C_NH];
-    if (use_graph) c->n_launches += g_per_iter * std::max(1, ws->h_ctl[ddk::C_ITER]) + 2 * std::max(1, ws->h_ctl[ddk::C_ITER]);
-    std::vector<double> hv(std::max(1, nh));
-    CK(cudaMemcpy(hv.data(), ws->d_hist, sizeof(double) * std::max(1, nh), cudaMemcpyDeviceToHost));
-    if (hist) std::memcpy(hist, hv.data(), sizeof(double) * nh);
-    double iters = 0.0;
-    int64_t napp = 0;
-    int status = DD_OK, brk = 0;
-    double rel = 1.0;
-    const double n0 = hv[0];
-    auto last_full = [&]() { return n0 > 0 ? hv[std::max(0, (nh - 1) & ~1)] / n0 : 0.0; };
-    switch (state) {
-        case ddk::ST_DONE_HALF: iters = kf - 0.5; napp = 2 * kf - 1; rel = hv[2 * kf - 1] / n0; break;
-        case ddk::ST_DONE_FULL: iters = kf; napp = 2 * kf; rel = hv[2 * kf] / n0; break;
-        case ddk::ST_ZERO: iters = 0; napp = 0; rel = 0.0; break;
-        case ddk::ST_BRK_RHO: status = DD_E_BREAKDOWN; brk = 1; iters = kf; napp = 2 * kf; rel = last_full(); break;
-        case ddk::ST_BRK_SIGMA: status = DD_E_BREAKDOWN; brk = 2; iters = kf - 1; napp = 2 * kf - 1; rel = last_full(); break;
-        case ddk::ST_BRK_TAU: status = DD_E_BREAKDOWN; brk = 3; iters = kf - 0.5; napp = 2 * kf; rel = last_full(); break;
-        default: status = DD_E_MAXITER; iters = max_iter; napp = 2 * (int64_t)max_iter; rel = last_full(); break;
-    }
-    {
-        const int64_t n_real[3] = {napp, napp, 0};
-        prof_collect(c, n_real, (int)std::ceil(iters));
-    }
-    // true residual ||b - A x|| / ||b||
-    TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, ra_plain, st));
-    ddk::launch_resid(c, m, b, ws->t, ra_plain, st);
-    TRY(reduce_across(c, 2, ddk::FIN_RESID, ra_plain, st));
-    TRY(read_scalars(c, st));
-    CK(cudaGetLastError());
-    const double *sc = ws->h_sc;
-    if (rep) {
-        rep->iterations = iters;
-        rep->n_applies = (int32_t)napp;
-        rep->converged = status == DD_OK;
-        rep->breakdown = brk;
-        rep->status = status;
-        rep->rel_resid = rel;
-        rep->true_rel_resid = sc[ddk::S_RES_BB] > 0 ? std::sqrt(sc[ddk::S_RES_TT]) / std::sqrt(sc[ddk::S_RES_BB]) : 0.0;
-        rep->solve_ms = now_ms() - t0;
-    }
-    return (dd_status)status;
-}
-
-dd_status dd_refactor(dd_ctx *c, const double *vals, int32_t on_device, void *stream) {
-    if (!usable(c) || !vals) return DD_E_INVALID_ARG;
-    if (!c->refactor) {
-        set_error("dd_refactor: context was set up without enable_refactor");
-        return DD_E_INVALID_ARG;
-    }
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    TRY(refactor_init(c));
-    auto *rf = reinterpret_cast<RfState *>(c->rf);
-    const double *src = vals;
-    if (!on_device) {
-        CK(cudaMemcpyAsync(rf->stage, vals, 9 * c->nnzb_A * sizeof(double), cudaMemcpyHostToDevice, st));
-        src = rf->stage;
-    }
-    const int grid = c->num_sms * 8;
-    ddk::launch_gather_blocks((int64_t)c->Wsrc.size(), rf->Wsrc, src, rf->W, 0, grid, st);
-    ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
-    *rf->h_bad = ~0ull;
-    CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    ddk::RfArgs a{rf->SubLev, rf->LevPtr, rf->LevRows, rf->Wrp, rf->Wdiag, rf->Uptr, rf->Lrp, rf->Urp,
-                  rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes, rf->Loff, rf->Uoff, rf->Doff,
-                  rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad, c->row_first};
-    const int nsl = c->sub_last - c->sub_first;
-    if (nsl > 0) ddk::launch_refactor(nsl, a, st);
-    c->n_launches += 3;
-    CK(cudaMemcpyAsync(rf->h_bad, rf->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    CK(cudaGetLastError());
-    if (*rf->h_bad != ~0ull) {
-        set_error("dd_refactor: singular pivot block (|det| < pivot_floor) at reordered row " +
-                  std::to_string(*rf->h_bad));
-        return DD_E_SINGULAR_PIVOT;
-    }
-    return DD_OK;
-}
-
 dd_status dd_permute(dd_ctx *c, const double *v_orig_host, double *v_reord_dev, void *stream) {
     if (!usable(c) || !v_orig_host || !v_reord_dev) return DD_E_INVALID_ARG;
+    DEVICE_GUARD(c);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     CK(cudaMemcpyAsync(c->d_stage, v_orig_host, c->bs * c->N * sizeof(double), cudaMemcpyHostToDevice, st));
     ddk::launch_gather3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), c->d_stage,
@@ -1210,6 +469,7 @@ dd_status dd_permute(dd_ctx *c, const double *v_orig_host, double *v_reord_dev, 
 
 dd_status dd_unpermute(dd_ctx *c, const double *v_reord_dev, double *v_orig_host, void *stream) {
     if (!usable(c) || !v_orig_host || !v_reord_dev) return DD_E_INVALID_ARG;
+    DEVICE_GUARD(c);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (c->world <= 1) {
         ddk::launch_scatter3(c, c->n_local, reinterpret_cast<const int32_t *>(c->d_new_to_old_local), v_reord_dev,
@@ -1227,19 +487,6 @@ dd_status dd_unpermute(dd_ctx *c, const double *v_reord_dev, double *v_orig_host
         }
     }
     return DD_OK;
-}
-
-dd_status dd_solve_host(dd_ctx *c, const double *b_host, double *x_host, double tol, int32_t max_iter,
-                        dd_report *rep, void *stream) {
-    if (!usable(c)) return DD_E_INVALID_ARG;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    Workspace *ws = ws_of(c);
-    TRY(dd_permute(c, b_host, ws->bd, stream));
-    CK(cudaMemsetAsync(ws->xd, 0, ws->m * sizeof(double), st));
-    dd_status s = dd_bicgstab(c, ws->bd, ws->xd, tol, max_iter, nullptr, rep, stream);
-    if (s != DD_OK && s != DD_E_BREAKDOWN && s != DD_E_MAXITER) return s;
-    TRY(dd_unpermute(c, ws->xd, x_host, stream));
-    return s;
 }
 
 dd_status dd_get_partition(const dd_ctx *c, int32_t *labels, int32_t *new_to_old) {
@@ -1371,29 +618,6 @@ dd_status dd_stats(const dd_ctx *c, int64_t *stats, double *setup_ms) {
     }
     if (setup_ms)
         for (int q = 0; q < 6; ++q) setup_ms[q] = c->setup_ms[q];
-    return DD_OK;
-}
-
-dd_status dd_profile(dd_ctx *c, int32_t mode, double *out) {
-    if (!c) return DD_E_INVALID_ARG;
-    Prof *p = prof_of(c);
-    if (mode == 1) {
-        p->on = true;
-        for (int q = 0; q < 3; ++q) {
-            p->ms[q] = 0;
-            p->n[q] = 0;
-        }
-    } else if (mode == 0) {
-        p->on = false;
-    }
-    if (out) {
-        for (int q = 0; q < 3; ++q) {
-            out[2 * q] = (double)p->n[q];
-            out[2 * q + 1] = p->ms[q];
-        }
-        out[6] = (double)c->n_launches;
-        out[7] = 0;
-    }
     return DD_OK;
 }
 

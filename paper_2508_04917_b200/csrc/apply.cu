@@ -688,13 +688,17 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             } else {
                 process_record<BS, SPIN, GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, F);
             }
+            const uint32_t ro0 = ro;
             ro += h.bytes;
             if (SPIN) {
                 // lanes diverge in the flag waits: reconverge before lane 0 hands
                 // chunks back (rows of one record never depend on each other, so
                 // this cannot deadlock)
                 __syncwarp();
-            } else if (!skip) {
+            } else if (!skip || ro0 / CH != ro / CH) {
+                // a skipped record needs no barrier for the sweep, but when it
+                // ends in a later chunk than it started, the chunk handed back
+                // below may hold headers a lagging warp has not read yet
                 named_bar_sync(1, TC);
             }
             if (last) {
@@ -719,6 +723,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
 #pragma unroll
                     for (int c = 0; c < BS; ++c) d[c] = vec[BS * li + c];
                 }
+                // peer transports publish the rows with a flag after this
+                // kernel: the NVLink stores must be performed system-wide first
+                __threadfence_system();
                 named_bar_sync(1, TC);
             }
         }

@@ -148,8 +148,8 @@ struct dd_ctx {
     double *d_sendbuf = nullptr;
     void *dev_ws = nullptr;              // BiCGSTAB workspace (api.cpp)
     void *nccl = nullptr;                // ncclComm_t
-    int comm = 0;                        // DD_COMM_NCCL / DD_COMM_LOCAL
-    void *group = nullptr;               // LocalGroup (DD_COMM_LOCAL)
+    int comm = 0;                        // DD_COMM_NCCL / DD_COMM_LOCAL / DD_COMM_IPC
+    void *rdv = nullptr;                 // host rendezvous of the peer transports (comm.cpp)
     double *h_pinned = nullptr;          // small pinned scalars
     int num_sms = 148;
     // --- refactor (dd_refactor) symbolic maps, built when opts.enable_refactor

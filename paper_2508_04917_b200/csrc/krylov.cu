@@ -16,6 +16,7 @@
 
 #include "dd_internal.h"
 #include "krylov.cuh"
+#include "peer.cuh"
 
 // Split dot reduction for the fused-dot SpMV modes (default): warps write
 // per-slice Dot2 partials and a small second kernel combines them, instead of
@@ -503,14 +504,15 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, const double *__restri
     if (grid_reduce<2>(v, ra.partials, ra.counter, out)) deliver<2>(ra, FIN_RESID, out);
 }
 
-// multi-rank: combine the gathered per-rank values (in rank order) and finalize
-__global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, RedArgs ra, int op) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (op != FIN_INIT && op != FIN_RESID && stopped(ra.ctl)) return;
+// multi-rank: combine the gathered per-rank values (in rank order) and
+// finalize; rank rr's pairs at gathered[rr * stride ..]
+__device__ void combine_finalize(int world, int nv, const volatile double *gathered, int stride, const RedArgs &ra,
+                                 int op) {
     double out[3] = {0.0, 0.0, 0.0};
     for (int q = 0; q < nv; ++q) {
         DD acc{0.0, 0.0};
-        for (int rr = 0; rr < world; ++rr) acc = dd_plus(acc, DD{gathered[rr * 2 * nv + 2 * q], gathered[rr * 2 * nv + 2 * q + 1]});
+        for (int rr = 0; rr < world; ++rr)
+            acc = dd_plus(acc, DD{gathered[rr * stride + 2 * q], gathered[rr * stride + 2 * q + 1]});
         out[q] = acc.s + acc.c;
     }
     if (op == FIN_SS_OMEGA) {
@@ -520,6 +522,41 @@ __global__ void k_finalize_gathered(int world, int nv, const double *__restrict_
         op = FIN_OMEGA;
     }
     finalize(ra.sc, op, out, ra.ctl, ra.hist, ra.k);
+}
+
+__global__ void k_finalize_gathered(int world, int nv, const double *__restrict__ gathered, RedArgs ra, int op) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (op != FIN_INIT && op != FIN_RESID && stopped(ra.ctl)) return;
+    combine_finalize(world, nv, gathered, 2 * nv, ra, op);
+}
+
+// peer transport (DD_COMM_LOCAL / DD_COMM_IPC, peer.cuh): publish this rank's
+// pairs into every rank's gathered slot (double-buffered by the parity of the
+// DOT count: a peer can be at most one all-gather ahead, because the next one
+// needs this rank's partial), release the count, wait for every peer, then
+// the same rank-order combine. Skipped by the same rule on every rank.
+__global__ void k_peer_allgather_finalize(PeerDev d, int nv, const double *__restrict__ loc, RedArgs ra, int op) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (op != FIN_INIT && op != FIN_RESID && stopped(ra.ctl)) return;
+    if (*reinterpret_cast<volatile int *>(d.err)) return;
+    const unsigned long long s = ++d.seq[PCH_DOT];
+    const int par = (int)(s & 1ull);
+    double v[6];
+    for (int e = 0; e < 2 * nv; ++e) v[e] = loc[e];
+    for (int q = 0; q < d.world; ++q) {
+        double *g = peer_gath(d, q) + (par * d.world + d.rank) * 6;
+        for (int e = 0; e < 2 * nv; ++e) g[e] = v[e];
+    }
+    __threadfence_system();
+    for (int q = 0; q < d.world; ++q)
+        if (q != d.rank) peer_st_release(peer_flags(d, q) + PCH_DOT * d.world + d.rank, s);
+    const unsigned long long target = ++d.seq[PCH_COUNT + PCH_DOT];
+    for (int q = 0; q < d.world; ++q)
+        if (q != d.rank && !peer_spin(d, PCH_DOT, q, target)) {
+            if (ra.ctl) ra.ctl[C_STATE] = ST_COMM;
+            return;
+        }
+    combine_finalize(d.world, nv, peer_gath(d, d.rank) + par * d.world * 6, 6, ra, op);
 }
 
 // permutation helpers: out[3 li + c] = in[3 idx[li] + c] and the reverse
@@ -643,6 +680,10 @@ void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, cons
 }
 void launch_finalize_gathered(int world, int nv, const double *gathered, const RedArgs &ra, int op, cudaStream_t st) {
     k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, ra, op);
+}
+void launch_peer_allgather_finalize(const PeerDev &d, int nv, const double *loc, const RedArgs &ra, int op,
+                                    cudaStream_t st) {
+    k_peer_allgather_finalize<<<1, 32, 0, st>>>(d, nv, loc, ra, op);
 }
 void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out, cudaStream_t st) {
     ++ctx->n_launches;

@@ -45,7 +45,8 @@ enum : int {
     ST_ZERO = 4,       // ||r0|| == 0
     ST_BRK_RHO = 5,
     ST_BRK_SIGMA = 6,
-    ST_BRK_TAU = 7
+    ST_BRK_TAU = 7,
+    ST_COMM = 8        // a peer-transport wait timed out (DD_E_NCCL)
 };
 enum : int { SPMV_PLAIN = 0, SPMV_SIGMA = 1, SPMV_TS_TT = 2 };
 

@@ -1,0 +1,145 @@
+// refactor_api.cpp -- dd_refactor: numeric re-factorisation of
+// the same pattern on the GPU (k_refactor, refactor.cu), the device copies of
+// the symbolic maps built at dd_setup, and the pivot status agreed over ranks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "api_internal.h"
+#include "refactor.cuh"
+
+using namespace ddi;
+
+namespace {
+dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStream_t st);
+
+// device copies of the refactor maps (allocated at the first dd_refactor)
+struct RfState {
+    int32_t *SubLev = nullptr, *LevPtr = nullptr, *LevRows = nullptr, *Wcol = nullptr, *UpdQ = nullptr,
+            *UpdT = nullptr, *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
+    int64_t *Wrp = nullptr, *Wdiag = nullptr, *Uptr = nullptr, *Lrp = nullptr, *Urp = nullptr, *Loff = nullptr,
+            *Uoff = nullptr, *Doff = nullptr, *Wsrc = nullptr, *Esrc = nullptr;
+    double *W = nullptr, *Dinv = nullptr, *stage = nullptr;
+    unsigned long long *bad = nullptr;
+    unsigned long long *h_bad = nullptr;
+};
+
+dd_status refactor_init(dd_ctx *c) {
+    if (c->rf) return DD_OK;
+    auto *rf = new RfState();
+    c->rf = rf;
+    TRY(upload_vec(&rf->SubLev, c->SubLev));
+    TRY(upload_vec(&rf->LevPtr, c->LevPtr));
+    TRY(upload_vec(&rf->LevRows, c->LevRows));
+    TRY(upload_vec(&rf->Wcol, c->Wcol));
+    TRY(upload_vec(&rf->UpdQ, c->UpdQ));
+    TRY(upload_vec(&rf->UpdT, c->UpdT));
+    TRY(upload_vec(&rf->Lst, c->SlabLst));
+    TRY(upload_vec(&rf->Ust, c->SlabUst));
+    TRY(upload_vec(&rf->Dst, c->SlabDst));
+    TRY(upload_vec(&rf->Wrp, c->Wrp));
+    TRY(upload_vec(&rf->Wdiag, c->Wdiag));
+    TRY(upload_vec(&rf->Uptr, c->Uptr));
+    TRY(upload_vec(&rf->Lrp, c->Lrp));
+    TRY(upload_vec(&rf->Urp, c->Urp));
+    TRY(upload_vec(&rf->Loff, c->SlabLoff));
+    TRY(upload_vec(&rf->Uoff, c->SlabUoff));
+    TRY(upload_vec(&rf->Doff, c->SlabDoff));
+    TRY(upload_vec(&rf->Wsrc, c->Wsrc));
+    // sliced-ELL slot -> original block index (-1 = padding), same layout as device_setup
+    {
+        const int64_t nl = c->n_local;
+        const auto &S = c->spmv;
+        std::vector<int64_t> es(S.n_slots, -1);
+        int64_t base = 0;
+        for (int64_t s = 0; s < S.n_slices; ++s) {
+            int64_t K = 0;
+            for (int64_t li = 32 * s; li < std::min(nl, 32 * s + 32); ++li) K = std::max(K, c->Arp[li + 1] - c->Arp[li]);
+            for (int lane = 0; lane < 32; ++lane) {
+                const int64_t li = 32 * s + lane;
+                if (li >= nl) break;
+                for (int64_t k = 0; k < c->Arp[li + 1] - c->Arp[li]; ++k) es[base + 32 * k + lane] = c->Asrc[c->Arp[li] + k];
+            }
+            base += 32 * K;
+        }
+        TRY(upload_vec(&rf->Esrc, es));
+    }
+    TRY(dmalloc(&rf->W, 9 * std::max<size_t>(1, c->Wsrc.size())));
+    TRY(dmalloc(&rf->Dinv, 9 * std::max<int64_t>(1, c->n_local)));
+    TRY(dmalloc(&rf->stage, 9 * std::max<int64_t>(1, c->nnzb_A)));
+    TRY(dmalloc(&rf->bad, 1));
+    CK(cudaMallocHost(reinterpret_cast<void **>(&rf->h_bad), sizeof(unsigned long long)));
+    return DD_OK;
+}
+
+}  // namespace
+
+namespace ddi {
+void refactor_free(dd_ctx *c) {
+    auto *rf = reinterpret_cast<RfState *>(c->rf);
+    if (!rf) return;
+    for (void *p : {(void *)rf->SubLev, (void *)rf->LevPtr, (void *)rf->LevRows, (void *)rf->Wcol, (void *)rf->UpdQ,
+                    (void *)rf->UpdT, (void *)rf->Lst, (void *)rf->Ust, (void *)rf->Dst, (void *)rf->Wrp,
+                    (void *)rf->Wdiag, (void *)rf->Uptr, (void *)rf->Lrp, (void *)rf->Urp, (void *)rf->Loff,
+                    (void *)rf->Uoff, (void *)rf->Doff, (void *)rf->Wsrc, (void *)rf->Esrc, (void *)rf->W,
+                    (void *)rf->Dinv, (void *)rf->stage, (void *)rf->bad})
+        cudaFree(p);
+    cudaFreeHost(rf->h_bad);
+    delete rf;
+    c->rf = nullptr;
+}
+}  // namespace ddi
+
+extern "C" {
+
+dd_status dd_refactor(dd_ctx *c, const double *vals, int32_t on_device, void *stream) {
+    if (!usable(c)) return DD_E_INVALID_ARG;
+    DEVICE_GUARD(c);
+    // collective when world > 1: every rank returns the status agreed over
+    // the ranks (a singular pivot on one rank fails all of them)
+    return comm_agree(c, refactor_run(c, vals, on_device, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"
+
+namespace {
+dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStream_t st) {
+    if (!vals) {
+        set_error("dd_refactor: NULL values");
+        return DD_E_INVALID_ARG;
+    }
+    if (!c->refactor) {
+        set_error("dd_refactor: context was set up without enable_refactor");
+        return DD_E_INVALID_ARG;
+    }
+    TRY(refactor_init(c));
+    auto *rf = reinterpret_cast<RfState *>(c->rf);
+    const double *src = vals;
+    if (!on_device) {
+        CK(cudaMemcpyAsync(rf->stage, vals, 9 * c->nnzb_A * sizeof(double), cudaMemcpyHostToDevice, st));
+        src = rf->stage;
+    }
+    const int grid = c->num_sms * 8;
+    ddk::launch_gather_blocks((int64_t)c->Wsrc.size(), rf->Wsrc, src, rf->W, 0, grid, st);
+    ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
+    *rf->h_bad = ~0ull;
+    CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    ddk::RfArgs a{rf->SubLev, rf->LevPtr, rf->LevRows, rf->Wrp, rf->Wdiag, rf->Uptr, rf->Lrp, rf->Urp,
+                  rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes, rf->Loff, rf->Uoff, rf->Doff,
+                  rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad, c->row_first};
+    const int nsl = c->sub_last - c->sub_first;
+    if (nsl > 0) ddk::launch_refactor(nsl, a, st);
+    c->n_launches += 3;
+    CK(cudaMemcpyAsync(rf->h_bad, rf->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (*rf->h_bad != ~0ull) {
+        set_error("dd_refactor: singular pivot block (|det| < pivot_floor) at reordered row " +
+                  std::to_string(*rf->h_bad));
+        return DD_E_SINGULAR_PIVOT;
+    }
+    return DD_OK;
+}
+}  // namespace

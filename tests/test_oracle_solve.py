@@ -222,3 +222,39 @@ def test_o12_spe10_style_converges():
     br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
     x, rep = oracle.bicgstab(S, br, tol=1e-8, max_iter=2000)
     assert rep["status"] == 0 and rep["true_rel_resid"] <= 1e-7
+
+
+def test_o12_breakdown_sigma_closed_form():
+    """R25 sigma test pinned by exact arithmetic: A = [[1, 2], [0, -1]] (x I3),
+    P = 1 -> M = blockdiag(A_ii) = diag(1, -1), b = 1: p_hat = M^-1 r0 =
+    (1, -1), v = A p_hat = (-1, 1), sigma = r0.v = 0 exactly -> breakdown at
+    k = 1 before any update (iterations 0, one apply), x = x0."""
+    rp, ci, a = kron_blocks(np.array([[1.0, 2.0], [0.0, -1.0]]))
+    S = oracle.setup(rp, ci, a, P=1)
+    b = np.ones(6)
+    x, rep = oracle.bicgstab(S, b.reshape(-1, 3)[S["new_to_old"]].ravel(), tol=1e-8)
+    assert rep["status"] == 1 and rep["iterations"] == 0.0 and rep["n_applies"] == 1
+    assert np.array_equal(x, np.zeros(6))
+    assert rep["resid_hist"].tolist() == [math.sqrt(6.0)]
+
+
+def test_o12_breakdown_rho_initial():
+    """R25 rho test: ||r0||^2 = rho_1 < 1e-30 with r0 != 0 (b of 1e-17 on 6
+    entries: rho_1 = 6e-34) -> breakdown before the first apply."""
+    rp, ci, a = kron_blocks(np.array([[4.0, 1.0], [1.0, 4.0]]))
+    S = oracle.setup(rp, ci, a, P=2)
+    x, rep = oracle.bicgstab(S, np.full(6, 1e-17), tol=1e-8)
+    assert rep["status"] == 1 and rep["iterations"] == 0.0 and rep["n_applies"] == 0
+    assert np.array_equal(x, np.zeros(6))
+
+
+def test_o12_breakdown_tau_exact_preconditioner():
+    """R25 tau test: one subdomain with a full block pattern makes ILU0 exact
+    (M = A), so s = r0 - alpha A M^-1 r0 is pure rounding; with tol far below
+    it the half-step test fails and tau = ||A M^-1 s||^2 < 1e-30 -> breakdown
+    at iteration 1/2 (two applies), x unchanged."""
+    from tests.breakdown_cases import find_case
+    c = find_case("tau_k1", 3)
+    assert c is not None and c["P"] == c["S"]["n"]  # one subdomain, exact ILU0
+    assert np.array_equal(c["x"], np.zeros_like(c["x"]))
+    assert len(c["rep"]["resid_hist"]) == 2 and c["rep"]["resid_hist"][1] < 1e-14 * c["rep"]["resid_hist"][0]
