@@ -58,6 +58,8 @@ def lib():
             "orc_levels_lower": (None, [i64, P, P, P]),
             "orc_levels_upper": (None, [i64, P, P, P]),
             "orc_apply": (None, [i64, i32, P, P, P, P, P, P, P, P]),
+            "orc_lower": (None, [i64, i32, P, P, P, P, P, P]),
+            "orc_apply_ilu0": (None, [i64, i32, P, P, P, P, P, P, P]),
             "orc_spmv": (None, [i64, P, P, P, P, P]),
             "orc_dot": (dbl, [i64, P, P]),
             "orc_bicgstab": (C.c_int, [i64, P, P, P, i32, P, P, P, P, P, P, P, P, dbl, i32,
@@ -205,6 +207,24 @@ def apply(S, r):
     f = lib().orc_s_apply if S.get("bs", 3) == 1 else lib().orc_apply
     f(S["n"], S["n_sub"], _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]),
       _p(S["lu"]), _p(S["dinv"]), _p(S["uunit"]), _p(r), _p(z))
+    return z
+
+
+def lower(S, r):
+    """z = L^-1 r per subdomain (unit L): the Table 3 lower solve (BSR3)."""
+    r = _c(r, np.float64)
+    z = np.empty_like(r)
+    lib().orc_lower(S["n"], S["n_sub"], _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]), _p(S["lu"]), _p(r), _p(z))
+    return z
+
+
+def apply_ilu0(S, r):
+    """ILU0 apply with the non-unit upper factor (scaling after each row's
+    off-diagonal updates), BSR3."""
+    r = _c(r, np.float64)
+    z = np.empty_like(r)
+    lib().orc_apply_ilu0(S["n"], S["n_sub"], _p(S["sub_ptr"]), _p(S["rp_d"]), _p(S["ci_d"]), _p(S["lu"]),
+                         _p(S["dinv"]), _p(r), _p(z))
     return z
 
 

@@ -323,6 +323,61 @@ void orc_apply(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *
     }
 }
 
+/* Lower solve alone (Table 3 analogue): z = L^-1 r per subdomain,
+ * unit L (sec. 4.3), the forward sweep of orc_apply written out again. */
+void orc_lower(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp, const int32_t *ci,
+               const double *lu, const double *r, double *z) {
+    (void)n;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t s = 0; s < n_sub; s++) {
+        for (int64_t i = sub_ptr[s]; i < sub_ptr[s + 1]; i++) {
+            for (int c = 0; c < 3; c++) {
+                double acc = r[3 * i + c];
+                for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < i; p++) {
+                    const double *B = lu + 9 * p;
+                    const double *zj = z + 3 * (int64_t)ci[p];
+                    for (int d = 0; d < 3; d++) acc = fma(-B[3 * c + d], zj[d], acc);
+                }
+                z[3 * i + c] = acc;
+            }
+        }
+    }
+}
+
+/* ILU0 apply with the NON-unit upper factor ("unlike ILU0
+ * where scaling follows each row's off-diagonal updates"): forward unit-lower
+ * sweep as in orc_apply; backward sweep rows descending with U = the ILU0
+ * upper blocks themselves (lu, j > i, not scaled by Dinv_i):
+ *   acc_c = z_ic; for U blocks ascending, for d: acc_c = fma(-U[c][d], x_jd, acc_c);
+ *   x_ic = D[c][0] acc_0; x_ic = fma(D[c][1], acc_1, x_ic); x_ic = fma(D[c][2], acc_2, x_ic)
+ * with D = Dinv_i = U_ii^-1. Mathematically equal to orc_apply (U = D^-1 U_unit). */
+void orc_apply_ilu0(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp, const int32_t *ci,
+                    const double *lu, const double *dinv, const double *r, double *z) {
+    orc_lower(n, n_sub, sub_ptr, rp, ci, lu, r, z);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t s = 0; s < n_sub; s++) {
+        for (int64_t i = sub_ptr[s + 1] - 1; i >= sub_ptr[s]; i--) {
+            double acc[3];
+            for (int c = 0; c < 3; c++) {
+                acc[c] = z[3 * i + c];
+                for (int64_t p = rp[i]; p < rp[i + 1]; p++) {
+                    if (ci[p] <= i) continue;
+                    const double *B = lu + 9 * p;
+                    const double *xj = z + 3 * (int64_t)ci[p];
+                    for (int d = 0; d < 3; d++) acc[c] = fma(-B[3 * c + d], xj[d], acc[c]);
+                }
+            }
+            const double *D = dinv + 9 * i;
+            for (int c = 0; c < 3; c++) {
+                double t = D[3 * c + 0] * acc[0];
+                t = fma(D[3 * c + 1], acc[1], t);
+                t = fma(D[3 * c + 2], acc[2], t);
+                z[3 * i + c] = t;
+            }
+        }
+    }
+}
+
 /* ------------------------------------------------------------------ SpMV */
 void orc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
               const double *x, double *y) {

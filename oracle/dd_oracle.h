@@ -93,6 +93,12 @@ void orc_levels_upper(int64_t n, const int64_t *rp, const int32_t *ci, int32_t *
 void orc_apply(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp,
                const int32_t *ci, const double *lu, const double *dinv, const double *uunit,
                const double *r, double *z);
+/* Table 3 analogue: the forward unit-lower sweep alone, z = L^-1 r. */
+void orc_lower(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp, const int32_t *ci,
+               const double *lu, const double *r, double *z);
+/* ILU0 with the non-unit U (scaling after each row's updates). */
+void orc_apply_ilu0(int64_t n, int32_t n_sub, const int64_t *sub_ptr, const int64_t *rp, const int32_t *ci,
+                    const double *lu, const double *dinv, const double *r, double *z);
 
 /* Block SpMV y = A x (the bsrxmv of P:185; Alg. 1's A-products). */
 void orc_spmv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,

@@ -258,3 +258,36 @@ def test_o12_breakdown_tau_exact_preconditioner():
     assert c is not None and c["P"] == c["S"]["n"]  # one subdomain, exact ILU0
     assert np.array_equal(c["x"], np.zeros_like(c["x"]))
     assert len(c["rep"]["resid_hist"]) == 2 and c["rep"]["resid_hist"][1] < 1e-14 * c["rep"]["resid_hist"][0]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_o9b_lower_vs_scipy_triangular(seed):
+    """Table 3 analogue: orc_lower is the unit-lower solve L z = r of the
+    subdomain factors -- pinned against scipy's sparse triangular solve."""
+    import scipy.sparse.linalg as sla
+    rp, ci, v = random_block_grid(8, 6, 4, seed=seed)
+    S = oracle.setup(rp, ci, v, grid=(8, 6, 4), tiles=(4, 3, 2))
+    r = apply_input(S["n"], seed=seed)
+    F = split_factors(S["rp_d"], S["ci_d"], S["lu"])
+    z_ref = sla.spsolve_triangular(F["L"].tocsr(), r, lower=True, unit_diagonal=True)
+    z = oracle.lower(S, r)
+    assert np.allclose(z, z_ref, rtol=1e-12, atol=1e-12 * np.abs(z_ref).max())
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_o9c_apply_ilu0_nonunit(seed):
+    """Non-unit ILU0 apply: the dense brute force
+    (L U)^-1 r of the subdomain factors with U = the ILU0 upper triangle
+    incl. its diagonal blocks, and equal to the ILDU0 apply to rounding."""
+    rp, ci, v = random_block_grid(6, 5, 4, seed=seed)
+    S = oracle.setup(rp, ci, v, grid=(6, 5, 4), tiles=(3, 5, 2))
+    r = apply_input(S["n"], seed=seed)
+    F = split_factors(S["rp_d"], S["ci_d"], S["lu"])
+    M = (F["L"] @ F["U"]).toarray()
+    z_ref = np.linalg.solve(M, r)
+    z = oracle.apply_ilu0(S, r)
+    assert np.allclose(z, z_ref, rtol=1e-11, atol=1e-11 * np.abs(z_ref).max())
+    z_ildu = oracle.apply(S, r)
+    assert np.abs(z - z_ildu).max() <= 1e-12 * np.abs(z_ildu).max()
+    # a different rounding path: not bitwise the ILDU0 result in general
+    assert not np.array_equal(z, z_ildu)
