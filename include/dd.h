@@ -107,6 +107,20 @@ typedef struct {
 #define DD_DIRECT 4    /* ablation: level-set kernel reading factors straight from HBM  */
 #define DD_UNFUSED 8   /* ablation of the L->D->U fusion (sec. 4.4): the L sweep and the
                           D+U sweep as two launches, z makes an HBM round trip between */
+/* Paper ablations (BSR3 only; Tables 3-4). Edge-centric variants
+ * spread a record's blocks over the threads and accumulate with atomicAdd
+ * (P:640-644): their results differ from the oracle in the last bits and the
+ * solver's iteration count may vary (R19). */
+#define DD_EDGE 16          /* dag_ec_ILDU0_fused: edge-centric atomics, vector in shared
+                               memory, factors through the TMA ring (level set)          */
+#define DD_EDGE_GLOBAL 32   /* dag_ec_no_lds: edge-centric, vector in GLOBAL memory
+                               (global atomics), factors from global             */
+#define DD_ILU0 64          /* ILU0 with the non-unit U: each row scaled by U_ii^-1 after its
+                               off-diagonal updates; request it in dd_opts.variants
+                               (builds a second slab); deterministic, not bitwise ILDU0  */
+#define DD_DIRECT_GLOBAL 128 /* vertex-centric level set with the vector in global memory */
+#define DD_LOWER 256        /* modifier OR-ed into a variant for dd_apply_variant: the lower
+                               sweep alone, z = L^-1 r (Table 3's lower-solve analogue)  */
 
 typedef struct {
     int32_t subdomain_rows;   /* P when grid == NULL: contiguous chunks (R26)   */
@@ -212,7 +226,10 @@ dd_status dd_refactor(dd_ctx *ctx, const double *vals, int32_t vals_on_device, v
 dd_status dd_local_range(const dd_ctx *ctx, int64_t *first_block_row, int64_t *n_block_rows);
 
 /* z = M^-1 r (this rank's subdomains; no communication). variant = one of
- * DD_LEVELSET / DD_SPINLOOP / DD_DIRECT built at setup; 0 = DD_LEVELSET. */
+ * DD_LEVELSET / DD_SPINLOOP / DD_DIRECT / DD_UNFUSED / DD_EDGE /
+ * DD_EDGE_GLOBAL / DD_DIRECT_GLOBAL / DD_ILU0, optionally | DD_LOWER;
+ * 0 = DD_LEVELSET. r (and z for DD_UNFUSED) must be 16-byte aligned for the
+ * ring variants (DD_E_INVALID_ARG otherwise). */
 dd_status dd_apply(dd_ctx *ctx, const double *r, double *z, void *stream);
 dd_status dd_apply_variant(dd_ctx *ctx, int32_t variant, const double *r, double *z,
                            void *stream);

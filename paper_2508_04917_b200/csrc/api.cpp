@@ -92,8 +92,14 @@ dd_status tune_solver_variant(dd_ctx *ctx) {
     const char *e = getenv("DD_SOLVER_VARIANT");
     const std::string want = e ? e : "auto";
     if (want == "levelset") return DD_OK;
-    if (want == "spin" || want == "direct") {
-        const int v = want == "spin" ? DD_SPINLOOP : DD_DIRECT;
+    // the deterministic variants, and (ablation solves, R19) the paper's others
+    static const std::pair<const char *, int> names[] = {
+        {"spin", DD_SPINLOOP}, {"direct", DD_DIRECT}, {"edge", DD_EDGE}, {"edge_global", DD_EDGE_GLOBAL},
+        {"direct_global", DD_DIRECT_GLOBAL}, {"ilu0", DD_ILU0}, {"unfused", DD_UNFUSED}};
+    int v = 0;
+    for (auto &nv : names)
+        if (want == nv.first) v = nv.second;
+    if (v) {
         if (!(ctx->variants & v)) {
             set_error("DD_SOLVER_VARIANT: variant unavailable for this slab");
             return DD_E_INVALID_ARG;
@@ -160,6 +166,7 @@ dd_status device_setup(dd_ctx *ctx) {
     const int64_t nl = ctx->n_local;
     // slabs
     TRY(upload_slab(ctx->slab_lvl));
+    if (!ctx->slab_ilu.info.empty()) TRY(upload_slab(ctx->slab_ilu));
     tr("slab upload");
     // sliced-ELL SpMV operand
     {
@@ -373,7 +380,7 @@ void dd_destroy(dd_ctx *c) {
         cudaSetDevice(c->device);
         cudaDeviceSynchronize();
         comm_end(c);  // peer transports: every rank idle before the mailboxes go
-        for (Slab *sl : {&c->slab_lvl, &c->slab_spin}) {
+        for (Slab *sl : {&c->slab_lvl, &c->slab_spin, &c->slab_ilu}) {
             cudaFree(sl->d_bytes);
             cudaFree(sl->d_info);
         }
@@ -631,7 +638,12 @@ dd_status dd_solver_variant(const dd_ctx *c, int32_t *variant, double *ms) {
 
 dd_status dd_launch_info(const dd_ctx *c, int32_t variant, int64_t *info) {
     if (!c || !info) return DD_E_INVALID_ARG;
-    const LaunchCfg *l = variant == DD_SPINLOOP ? &c->cfg_spin : variant == DD_DIRECT ? &c->cfg_direct : &c->cfg_lvl;
+    const LaunchCfg *l = variant == DD_SPINLOOP ? &c->cfg_spin
+                         : (variant == DD_DIRECT || variant == DD_EDGE_GLOBAL || variant == DD_DIRECT_GLOBAL)
+                             ? &c->cfg_direct
+                         : variant == DD_EDGE ? &c->cfg_ec
+                         : variant == DD_ILU0 ? &c->cfg_nu
+                                              : &c->cfg_lvl;
     info[0] = l->grid;
     info[1] = l->threads;
     info[2] = l->smem;

@@ -114,7 +114,11 @@ __device__ __forceinline__ void set_bit(uint32_t *bits, uint32_t i) {
 // gather of vec[3j..3j+2] through the descriptor's column ids.
 // GEN: 0 = rows with at most 3 blocks per triangle only (7-point), 1 = general
 // K with blocks in groups of three, 2 = general K one block per step
-template <bool SPIN, int GEN, class Rd>
+// NU (ILU0 ablation, DD_ILU0): the U records hold the non-unit upper blocks
+// U_ij and the row's D = U_ii^-1 is applied AFTER its off-diagonal updates
+// ("unlike ILU0 where scaling follows each row's off-diagonal updates",
+// P:823): acc = z_i - sum U_ij x_j, x_i = D acc (orc_apply_ilu0's order).
+template <bool SPIN, int GEN, class Rd, bool NU = false>
 __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, SpinFlags F) {
     const uint32_t w = h.w, K = h.K;
@@ -154,21 +158,27 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         }
 #endif
         double a0, a1, a2;
+        double D[9];
         if (upper) {
-            double D[9];
 #pragma unroll
             for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
             if (SPIN) spin_bit(F.L, i);  // own L result
             const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
-            a0 = D[0] * z0;
-            a0 = __fma_rn(D[1], z1, a0);
-            a0 = __fma_rn(D[2], z2, a0);
-            a1 = D[3] * z0;
-            a1 = __fma_rn(D[4], z1, a1);
-            a1 = __fma_rn(D[5], z2, a1);
-            a2 = D[6] * z0;
-            a2 = __fma_rn(D[7], z1, a2);
-            a2 = __fma_rn(D[8], z2, a2);
+            if (NU) {
+                a0 = z0;
+                a1 = z1;
+                a2 = z2;
+            } else {
+                a0 = D[0] * z0;
+                a0 = __fma_rn(D[1], z1, a0);
+                a0 = __fma_rn(D[2], z2, a0);
+                a1 = D[3] * z0;
+                a1 = __fma_rn(D[4], z1, a1);
+                a1 = __fma_rn(D[5], z2, a1);
+                a2 = D[6] * z0;
+                a2 = __fma_rn(D[7], z1, a2);
+                a2 = __fma_rn(D[8], z2, a2);
+            }
         } else {
             a0 = vec[3 * i];
             a1 = vec[3 * i + 1];
@@ -200,6 +210,18 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
                 a2 = __fma_rn(-b[k][8], x2, a2);
             }
         }
+        if (NU && upper) {
+            const double q0 = a0, q1 = a1, q2 = a2;
+            a0 = D[0] * q0;
+            a0 = __fma_rn(D[1], q1, a0);
+            a0 = __fma_rn(D[2], q2, a0);
+            a1 = D[3] * q0;
+            a1 = __fma_rn(D[4], q1, a1);
+            a1 = __fma_rn(D[5], q2, a1);
+            a2 = D[6] * q0;
+            a2 = __fma_rn(D[7], q1, a2);
+            a2 = __fma_rn(D[8], q2, a2);
+        }
         vec[3 * i] = a0;
         vec[3 * i + 1] = a1;
         vec[3 * i + 2] = a2;
@@ -213,8 +235,14 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     const uint32_t dw = ddi::rec_dw(K);
     const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * t);
     double a0, a1, a2;
-    if (upper) {
-        double D[9];
+    double D[9];
+    if (upper && NU) {
+#pragma unroll
+        for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+        a0 = vec[3 * i];
+        a1 = vec[3 * i + 1];
+        a2 = vec[3 * i + 2];
+    } else if (upper) {
 #pragma unroll
         for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
         if (SPIN) spin_bit(F.L, i);  // own L result
@@ -326,6 +354,18 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         pre = pq;
     }
     }
+    if (NU && upper) {
+        const double q0 = a0, q1 = a1, q2 = a2;
+        a0 = D[0] * q0;
+        a0 = __fma_rn(D[1], q1, a0);
+        a0 = __fma_rn(D[2], q2, a0);
+        a1 = D[3] * q0;
+        a1 = __fma_rn(D[4], q1, a1);
+        a1 = __fma_rn(D[5], q2, a1);
+        a2 = D[6] * q0;
+        a2 = __fma_rn(D[7], q1, a2);
+        a2 = __fma_rn(D[8], q2, a2);
+    }
     vec[3 * i] = a0;
     vec[3 * i + 1] = a1;
     vec[3 * i + 2] = a2;
@@ -419,13 +459,90 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     }
 }
 
-template <int BS, bool SPIN, int GEN, class Rd>
+template <int BS, bool SPIN, int GEN, class Rd, bool NU = false>
 __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                double *__restrict__ vec, SpinFlags F) {
     if constexpr (BS == 3)
-        process_record3<SPIN, GEN>(rd, h, c8, t, vec, F);
+        process_record3<SPIN, GEN, Rd, NU>(rd, h, c8, t, vec, F);
     else
         process_record1<SPIN, GEN>(rd, h, c8, t, vec, F);
+}
+
+// Edge-centric record (dag_ec_*, Table 3/4 ablation, BSR3): the
+// record's nnz blocks are spread over the TC consumer threads (block e of
+// the jagged planes: k = the plane it falls in, row slot t = e - prefix_k),
+// each thread forms p = B x_j with its own FMA chain and subtracts it from
+// vec[i] with a shared-memory (or global) atomicAdd -- the order of the
+// atomics is not fixed, so results differ from the oracle in the last bits
+// (R19) and BiCGSTAB iteration counts may vary. An L record needs
+// no other step (vec[i] holds r_i, lower levels are final); a U record first
+// scales its rows, y_i = D_i z_i (one thread per row), then a barrier, then
+// the edges. bar() synchronises the consumer threads.
+template <int GEN, class Rd, class Bar>
+__device__ __forceinline__ void process_record_ec(const Rd &rd, const RecHdr &h, const uint4 &c8, int t, int TC,
+                                                  double *vec, Bar &&bar) {
+    const uint32_t w = h.w, K = h.K, nnz = h.nnz;
+    const bool upper = (h.flags & ddi::REC_UPPER) != 0;
+    const uint32_t off_desc = ddi::rec_off_desc(K);
+    const uint32_t dw = ddi::rec_dw(K);
+    if (upper) {
+        const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
+        for (uint32_t r = t; r < w; r += TC) {
+            const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * r);
+            double D[9];
+#pragma unroll
+            for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + r));
+            const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
+            double a0 = D[0] * z0;
+            a0 = __fma_rn(D[1], z1, a0);
+            a0 = __fma_rn(D[2], z2, a0);
+            double a1 = D[3] * z0;
+            a1 = __fma_rn(D[4], z1, a1);
+            a1 = __fma_rn(D[5], z2, a1);
+            double a2 = D[6] * z0;
+            a2 = __fma_rn(D[7], z1, a2);
+            a2 = __fma_rn(D[8], z2, a2);
+            vec[3 * i] = a0;
+            vec[3 * i + 1] = a1;
+            vec[3 * i + 2] = a2;
+        }
+        bar();
+    }
+    for (uint32_t e = t; e < nnz; e += TC) {
+        // plane k of edge e (rows sorted by block count: planes shrink)
+        uint32_t k = 0, pre = 0, ck = 0;
+        if (GEN == 0 || K <= 3) {
+            const uint32_t c0 = c8.x & 0xffffu, c1 = K > 1 ? (c8.x >> 16) : 0u, c2 = K > 2 ? (c8.y & 0xffffu) : 0u;
+            if (e >= c0 + c1) {
+                k = 2, pre = c0 + c1, ck = c2;
+            } else if (e >= c0) {
+                k = 1, pre = c0, ck = c1;
+            } else {
+                k = 0, pre = 0, ck = c0;
+            }
+        } else {
+            for (;; ++k) {
+                ck = rd.template ld<uint16_t>(16u + 2u * k);
+                if (e < pre + ck) break;
+                pre += ck;
+            }
+        }
+        const uint32_t r = e - pre;
+        const uint32_t i = rd.template ld<uint16_t>(off_desc + dw * r);
+        const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * r + 2u * (1u + k));
+        const uint32_t vb = h.off_val + 72u * pre + 8u * r, st = 8u * ck;
+        double b[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + st * v);
+        const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double p = b[3 * c] * x0;
+            p = __fma_rn(b[3 * c + 1], x1, p);
+            p = __fma_rn(b[3 * c + 2], x2, p);
+            atomicAdd(vec + 3 * i + c, -p);
+        }
+    }
 }
 
 __device__ __forceinline__ RecHdr hdr_from(uint4 q) {
@@ -447,20 +564,26 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // Ablation: level-set sweep reading the records straight from global memory;
 // only the vector lives in shared memory (so more CTAs fit per SM). Thread 0
 // keeps a bulk L2 prefetch pf_bytes ahead of the record being processed.
-template <int BS, int GEN>
+// MODE 0: vertex-centric ILDU0 (Alg. 6); 1: edge-centric with atomics
+// (process_record_ec); 2: vertex-centric ILU0 with the non-unit U (NU).
+// VECG: the vector lives in GLOBAL memory (z itself, initialised from r):
+// with MODE 1 the paper's dag_ec_no_lds (Table 3), global atomics.
+// phase 1: the lower sweep alone (z = L^-1 r, Table 3's lower solve).
+enum : int { AM_VC = 0, AM_EC = 1, AM_NU = 2 };
+template <int BS, int GEN, int MODE = AM_VC, bool VECG = false>
 __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
-                                                     uint32_t pf_bytes, const int *skip) {
+                                                     uint32_t pf_bytes, const int *skip, int phase) {
     // inside dd_bicgstab: skip (uniformly) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     extern __shared__ __align__(128) uint8_t smem[];
-    double *vec = reinterpret_cast<double *>(smem);
     const int t = threadIdx.x;
     for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
         const SubInfo si = info[s];
         const uint8_t *base = slab + si.stream_off;
-        const uint32_t sz = (uint32_t)si.stream_bytes;
+        const uint32_t sz = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
+        double *vec = VECG ? z + BS * (int64_t)si.row0 : reinterpret_cast<double *>(smem);
         uint32_t pf = 0;
         if (t == 0 && pf_bytes) {
             pf = min(sz, pf_bytes);
@@ -471,7 +594,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
         for (int q = t; q < nd; q += TCB<BS>) vec[q] = __ldg(rs + q);
         __syncthreads();
         uint32_t ro = 0;
-        while (true) {
+        while (ro < sz) {
             const uint8_t *p = base + ro;
             const RecHdr h = hdr_from(__ldg(reinterpret_cast<const uint4 *>(p)));
             const uint4 c8 = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
@@ -480,18 +603,27 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
                 prefetch_l2(base + pf, e - pf);
                 pf = e;
             }
-            const bool last = (h.flags & ddi::REC_LAST) != 0;
+            const bool last = (h.flags & ddi::REC_LAST) != 0 || ro + h.bytes >= sz;
             // L level 0 carries no blocks (z_i = r_i in place): no work, no barrier
             const bool skip = !(h.flags & ddi::REC_UPPER) && h.K == 0 && !last;
             if (!skip) {
-                process_record<BS, false, GEN>(GlobalRd{p}, h, c8, t, vec, SpinFlags{nullptr, nullptr});
+                if constexpr (MODE == AM_EC) {
+                    if constexpr (BS == 3)
+                        process_record_ec<GEN>(GlobalRd{p}, h, c8, t, TCB<BS>, vec, [] { __syncthreads(); });
+                } else {
+                    process_record<BS, false, GEN, GlobalRd, MODE == AM_NU>(GlobalRd{p}, h, c8, t, vec,
+                                                                            SpinFlags{nullptr, nullptr});
+                }
                 __syncthreads();
             }
             ro += h.bytes;
             if (last) break;
         }
-        double *zs = z + BS * (int64_t)si.row0;
-        for (int q = t; q < nd; q += TCB<BS>) zs[q] = vec[q];
+        if (!VECG) {
+            // thread t stores the entries it fills for the next subdomain: no barrier
+            double *zs = z + BS * (int64_t)si.row0;
+            for (int q = t; q < nd; q += TCB<BS>) zs[q] = vec[q];
+        }
     }
 }
 
@@ -511,7 +643,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 //   barriers count NW arrivals).
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
 //   the streaming ceiling of the ring.
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN, int MODE = AM_VC>
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
@@ -683,10 +815,17 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             // skips it (no work, no barrier); the sync-free sweep publishes flags
             const bool skip = !SPIN && !upper && h.K == 0 && !last;
             if (mode == 1 || skip) {
+            } else if constexpr (MODE == AM_EC && BS == 3) {
+                auto bar = [] { named_bar_sync(1, TC); };
+                if (pos + h.bytes <= RING)
+                    process_record_ec<GEN>(LinRd{ring + pos}, h, c8, t, TC, vec, bar);
+                else
+                    process_record_ec<GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, TC, vec, bar);
             } else if (pos + h.bytes <= RING) {
-                process_record<BS, SPIN, GEN>(LinRd{ring + pos}, h, c8, t, vec, F);
+                process_record<BS, SPIN, GEN, LinRd, MODE == AM_NU>(LinRd{ring + pos}, h, c8, t, vec, F);
             } else {
-                process_record<BS, SPIN, GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, vec, F);
+                process_record<BS, SPIN, GEN, RingRd<RING>, MODE == AM_NU>(RingRd<RING>{ring, abs0 + ro}, h, c8, t,
+                                                                          vec, F);
             }
             const uint32_t ro0 = ro;
             ro += h.bytes;
@@ -737,9 +876,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
 using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int,
                         ddi::HaloOut);
 
-template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN>
+template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN, int MODE>
 static RingFn ring_fn() {
-    return k_apply_ring<BS, RING, CH, SPIN, GEN>;
+    return k_apply_ring<BS, RING, CH, SPIN, GEN, MODE>;
 }
 
 // ring chunk = RING / 4: every chunk costs the consumers one mbarrier
@@ -747,39 +886,49 @@ static RingFn ring_fn() {
 // thread one arrive, so few large chunks win (measured at config 3: 16 KB
 // chunks 434 us, 8 KB 444 us, 4 KB 485 us); a chunk plus the largest record
 // must still fit the ring (apply_prepare checks)
-template <int BS, int GEN>
-static RingFn pick_ring_bg(int ring, bool spin) {
-    if (!spin) {
-        switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 131072 / DD_CH_DIV, false, GEN>();
-            case 65536: return ring_fn<BS, 65536, 65536 / DD_CH_DIV, false, GEN>();
-            case 32768: return ring_fn<BS, 32768, 32768 / DD_CH_DIV, false, GEN>();
-            case 16384: return ring_fn<BS, 16384, 16384 / DD_CH_DIV, false, GEN>();
-        }
-    } else {
-        switch (ring) {
-            case 131072: return ring_fn<BS, 131072, 131072 / DD_CH_DIV, true, GEN>();
-            case 65536: return ring_fn<BS, 65536, 65536 / DD_CH_DIV, true, GEN>();
-            case 32768: return ring_fn<BS, 32768, 32768 / DD_CH_DIV, true, GEN>();
-            case 16384: return ring_fn<BS, 16384, 16384 / DD_CH_DIV, true, GEN>();
-        }
+template <int BS, int GEN, bool SPIN, int MODE>
+static RingFn pick_ring_m(int ring) {
+    switch (ring) {
+        case 131072: return ring_fn<BS, 131072, 131072 / DD_CH_DIV, SPIN, GEN, MODE>();
+        case 65536: return ring_fn<BS, 65536, 65536 / DD_CH_DIV, SPIN, GEN, MODE>();
+        case 32768: return ring_fn<BS, 32768, 32768 / DD_CH_DIV, SPIN, GEN, MODE>();
+        case 16384: return ring_fn<BS, 16384, 16384 / DD_CH_DIV, SPIN, GEN, MODE>();
     }
     return nullptr;
 }
 
-// gen: the slab has rows with more than 3 blocks in a triangle (general-K path)
-static RingFn pick_ring(int bs, int ring, bool spin, bool gen) {
-    if (bs == 1) return gen ? pick_ring_bg<1, 1>(ring, spin) : pick_ring_bg<1, 0>(ring, spin);
-    return gen ? pick_ring_bg<3, 1>(ring, spin) : pick_ring_bg<3, 0>(ring, spin);
+// gen: the slab has rows with more than 3 blocks in a triangle (general-K
+// path). mode: AM_VC (the product), AM_EC / AM_NU (ablations: BSR3, level set)
+static RingFn pick_ring(int bs, int ring, bool spin, bool gen, int mode = AM_VC) {
+    if (mode != AM_VC) {
+        if (bs != 3 || spin) return nullptr;
+        if (mode == AM_EC) return gen ? pick_ring_m<3, 1, false, AM_EC>(ring) : pick_ring_m<3, 0, false, AM_EC>(ring);
+        return gen ? pick_ring_m<3, 1, false, AM_NU>(ring) : pick_ring_m<3, 0, false, AM_NU>(ring);
+    }
+    if (bs == 1)
+        return spin ? (gen ? pick_ring_m<1, 1, true, AM_VC>(ring) : pick_ring_m<1, 0, true, AM_VC>(ring))
+                    : (gen ? pick_ring_m<1, 1, false, AM_VC>(ring) : pick_ring_m<1, 0, false, AM_VC>(ring));
+    return spin ? (gen ? pick_ring_m<3, 1, true, AM_VC>(ring) : pick_ring_m<3, 0, true, AM_VC>(ring))
+                : (gen ? pick_ring_m<3, 1, false, AM_VC>(ring) : pick_ring_m<3, 0, false, AM_VC>(ring));
 }
 
-using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *);
-static DirectFn pick_direct(int bs, bool gen) {
+using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *,
+                          int);
+// vecg: the vector in global memory (no shared-memory vector)
+static DirectFn pick_direct(int bs, bool gen, int mode = AM_VC, bool vecg = false) {
     // the 3x3 direct ablation keeps the one-block-per-step general path compiled
     // in (GEN 2): the compiler schedules its global loads better that way
     // (458 vs 534 us at config 3)
-    if (bs == 1) return gen ? k_apply_direct<1, 1> : k_apply_direct<1, 0>;
-    return gen ? k_apply_direct<3, 1> : k_apply_direct<3, 2>;
+    if (mode == AM_VC && !vecg) {
+        if (bs == 1) return gen ? k_apply_direct<1, 1> : k_apply_direct<1, 0>;
+        return gen ? k_apply_direct<3, 1> : k_apply_direct<3, 2>;
+    }
+    if (bs != 3) return nullptr;
+    if (mode == AM_EC)
+        return vecg ? (gen ? k_apply_direct<3, 1, AM_EC, true> : k_apply_direct<3, 0, AM_EC, true>)
+                    : (gen ? k_apply_direct<3, 1, AM_EC, false> : k_apply_direct<3, 0, AM_EC, false>);
+    if (mode == AM_VC) return gen ? k_apply_direct<3, 1, AM_VC, true> : k_apply_direct<3, 2, AM_VC, true>;
+    return nullptr;
 }
 
 static int ring_chunk(int ring) { return ring / DD_CH_DIV; }
@@ -836,7 +985,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     // Ring choice: the consumer sweep is latency-bound, so maximise resident
     // CTAs per SM first (cudaOccupancy: shared memory and registers), then
     // take the largest ring that holds the biggest record plus one chunk.
-    auto choose = [&](LaunchCfg &c, bool spin, int64_t max_rec) -> dd_status {
+    auto choose = [&](LaunchCfg &c, bool spin, int64_t max_rec, int mode = AM_VC) -> dd_status {
         const int want = env_int("DD_RING_KB", 0) * 1024;
         const int cands[4] = {131072, 65536, 32768, 16384};
         int occs[4] = {0, 0, 0, 0}, max_occ = 0;
@@ -846,8 +995,8 @@ dd_status apply_prepare(dd_ctx *ctx) {
             const int nst = rc / ring_chunk(rc);
             const int sm = vec_bytes + rc + 16 * nst + (spin ? flag_bytes : 0);
             if (sm > smem_max || max_rec + ring_chunk(rc) > rc) continue;
-            allow_max_smem(pick_ring(bs, rc, spin, gen), smem_max);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs[k], pick_ring(bs, rc, spin, gen), tc + 32, sm);
+            allow_max_smem(pick_ring(bs, rc, spin, gen, mode), smem_max);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs[k], pick_ring(bs, rc, spin, gen, mode), tc + 32, sm);
             max_occ = std::max(max_occ, occs[k]);
         }
         // CTAs per SM worth having: no more than the subdomains can fill
@@ -874,7 +1023,8 @@ dd_status apply_prepare(dd_ctx *ctx) {
         return DD_OK;
     };
     // every variant walks the same level-ordered slab: prepare all of them
-    ctx->variants = DD_LEVELSET | DD_SPINLOOP | DD_DIRECT | DD_UNFUSED;
+    // (DD_ILU0 only if its slab with the non-unit U was built at setup)
+    ctx->variants = DD_LEVELSET | DD_SPINLOOP | DD_DIRECT | DD_UNFUSED | (ctx->variants & DD_ILU0);
     {
         dd_status st = choose(ctx->cfg_lvl, false, ctx->slab_lvl.max_rec_bytes);
         if (st != DD_OK) return st;
@@ -885,7 +1035,22 @@ dd_status apply_prepare(dd_ctx *ctx) {
         ctx->variants &= ~DD_SPINLOOP;
         ctx->cfg_spin = LaunchCfg{};
     }
-    return cudaGetLastError() == cudaSuccess ? DD_OK : DD_E_CUDA;
+    // paper ablations (BSR3): edge-centric atomics with the vector in shared
+    // memory (ring) or in global memory, the vertex-centric sweep with the
+    // vector in global memory, ILU0 with the non-unit U
+    if (bs == 3) {
+        if (choose(ctx->cfg_ec, false, ctx->slab_lvl.max_rec_bytes, AM_EC) == DD_OK) ctx->variants |= DD_EDGE;
+        ctx->variants |= DD_EDGE_GLOBAL | DD_DIRECT_GLOBAL;
+        for (bool vg : {false, true})
+            for (int m : {AM_EC, AM_VC})
+                if (DirectFn f = pick_direct(bs, gen, m, vg)) allow_max_smem(f, smem_max);
+        if ((ctx->variants & DD_ILU0) && choose(ctx->cfg_nu, false, ctx->slab_ilu.max_rec_bytes, AM_NU) != DD_OK)
+            ctx->variants &= ~DD_ILU0;
+    } else {
+        ctx->variants &= ~DD_ILU0;
+    }
+    cudaGetLastError();
+    return DD_OK;
 }
 
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip,
@@ -897,43 +1062,55 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     const int bs = ctx->bs;
     const bool gen = ctx->kmax > 3;
     const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
+    // DD_LOWER: the lower sweep alone, z = L^-1 r (Table 3 analogue)
+    const int phase = (variant & DD_LOWER) ? 1 : 0;
+    variant &= ~DD_LOWER;
     if (variant == 0) variant = DD_LEVELSET;
     const HaloOut ho = halo ? *halo : HaloOut{};
-    if (ho.ptr && variant == DD_DIRECT) {
-        set_error("dd_apply: the fused halo epilogue is a ring-kernel feature");
+    if (ho.ptr && variant != DD_LEVELSET) {
+        set_error("dd_apply: the fused halo epilogue is a level-set ring-kernel feature");
         return DD_E_INVALID_ARG;
     }
+    if (variant != DD_LEVELSET && !(ctx->variants & variant)) {
+        set_error("dd_apply: variant not available for this context (sync-free flags or the largest record do not "
+                  "fit, DD_ILU0 not requested at dd_setup, or a BSR3-only ablation on a scalar matrix)");
+        return variant == DD_SPINLOOP ? DD_E_SUBDOMAIN_TOO_LARGE : DD_E_INVALID_ARG;
+    }
     static const int mode = env_int("DD_APPLY_MODE", 0);  // 1: streaming ceiling (measurement only)
-    if (variant == DD_DIRECT) {
-        static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
-        const LaunchCfg &c = ctx->cfg_direct;
-        pick_direct(bs, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info, nsl, r, z, pf,
-                                                           skip);
-    } else if (variant == DD_LEVELSET) {
-        const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode, skip, 0, ho);
-    } else if (variant == DD_UNFUSED) {
-        // ablation of the fusion (sec. 4.4): the L sweep and the D+U
-        // sweep as two launches of the same kernel; the vector makes a round
-        // trip through HBM in between (z holds L^-1 r after the first)
-        const LaunchCfg &c = ctx->cfg_lvl;
-        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, r, z, vec_bytes, mode, skip, 1, ho);
-        ++ctx->n_launches;
-        pick_ring(bs, c.ring, false, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                   nsl, z, z, vec_bytes, mode, skip, 2, ho);
-    } else if (variant == DD_SPINLOOP) {
-        if (!(ctx->variants & DD_SPINLOOP)) {
-            set_error("dd_apply: sync-free variant unavailable (its ready flags do not fit shared memory)");
-            return DD_E_SUBDOMAIN_TOO_LARGE;
-        }
-        const LaunchCfg &c = ctx->cfg_spin;
-        pick_ring(bs, c.ring, true, gen)<<<c.grid, c.threads, c.smem, st>>>(ctx->slab_lvl.d_bytes, ctx->slab_lvl.d_info,
-                                                                  nsl, r, z, vec_bytes, mode, skip, 0, ho);
-    } else {
-        set_error("dd_apply: unknown variant");
-        return DD_E_INVALID_ARG;
+    static const uint32_t pf = (uint32_t)env_int("DD_DIRECT_PF_KB", 32) * 1024u;
+    const uint8_t *slab = ctx->slab_lvl.d_bytes;
+    const SubInfo *info = ctx->slab_lvl.d_info;
+    auto ring = [&](const LaunchCfg &c, bool spin, int m, const double *rr, int ph, const uint8_t *sb,
+                    const SubInfo *si) {
+        pick_ring(bs, c.ring, spin, gen, m)<<<c.grid, c.threads, c.smem, st>>>(sb, si, nsl, rr, z, vec_bytes, mode,
+                                                                              skip, ph, ho);
+    };
+    auto direct = [&](int m, bool vg, int smem) {
+        pick_direct(bs, gen, m, vg)<<<nsl, ctx->cfg_direct.threads, smem, st>>>(slab, info, nsl, r, z, pf, skip,
+                                                                               phase);
+    };
+    switch (variant) {
+        case DD_LEVELSET: ring(ctx->cfg_lvl, false, AM_VC, r, phase, slab, info); break;
+        case DD_UNFUSED:
+            // ablation of the fusion (sec. 4.4): the L sweep and the
+            // D+U sweep as two launches of the same kernel; the vector makes a
+            // round trip through HBM in between (z holds L^-1 r after the first)
+            ring(ctx->cfg_lvl, false, AM_VC, r, 1, slab, info);
+            if (!phase) {
+                ++ctx->n_launches;
+                ring(ctx->cfg_lvl, false, AM_VC, z, 2, slab, info);
+            }
+            break;
+        case DD_SPINLOOP: ring(ctx->cfg_spin, true, AM_VC, r, phase, slab, info); break;
+        case DD_DIRECT: direct(AM_VC, false, ctx->cfg_direct.smem); break;
+        case DD_EDGE: ring(ctx->cfg_ec, false, AM_EC, r, phase, slab, info); break;
+        case DD_EDGE_GLOBAL: direct(AM_EC, true, 0); break;
+        case DD_DIRECT_GLOBAL: direct(AM_VC, true, 0); break;
+        case DD_ILU0:
+            // the L section of the ILU0 slab equals the ILDU0 one
+            ring(ctx->cfg_nu, false, AM_NU, r, phase, ctx->slab_ilu.d_bytes, ctx->slab_ilu.d_info);
+            break;
+        default: set_error("dd_apply: unknown variant"); return DD_E_INVALID_ARG;
     }
     ++ctx->n_launches;
     const cudaError_t e = cudaGetLastError();

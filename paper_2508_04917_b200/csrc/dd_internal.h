@@ -132,10 +132,12 @@ struct dd_ctx {
     std::vector<int64_t> recv_off;                // [world + 1] into ghost block
     // slabs
     ddi::Slab slab_lvl, slab_spin;
+    ddi::Slab slab_ilu;                 // DD_ILU0 ablation: U records with the non-unit U_ij
+    std::vector<double> Uraw;           // non-unit U_ij (j > i), only when DD_ILU0 is requested
     int32_t variants = 0;
     int32_t solver_variant = DD_LEVELSET;  // apply variant inside dd_bicgstab (timed at setup)
     double variant_ms[3] = {0, 0, 0};      // level set, sync-free, direct
-    ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct;
+    ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct, cfg_ec, cfg_nu;
     // spmv
     ddi::SpmvDev spmv;
     int64_t spmv_bytes = 0;

@@ -115,6 +115,8 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
         return DD_E_INVALID_ARG;
     }
     TRY(refactor_init(c));
+    // the DD_ILU0 ablation slab is not re-factored: the variant goes away
+    c->variants &= ~DD_ILU0;
     auto *rf = reinterpret_cast<RfState *>(c->rf);
     const double *src = vals;
     if (!on_device) {

@@ -494,6 +494,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     ctx->Uci.assign(ctx->Urp[nl], 0);
     ctx->Lv.assign(b2 * ctx->Lrp[nl], 0.0);
     ctx->Uv.assign(b2 * ctx->Urp[nl], 0.0);
+    // DD_ILU0 ablation: keep the non-unit U_ij too (a second slab, BSR3 only)
+    const bool want_ilu = bs == 3 && (o->variants & DD_ILU0) != 0;
+    if (want_ilu) ctx->Uraw.assign(b2 * ctx->Urp[nl], 0.0);
     ctx->Dinv.assign(b2 * nl, 0.0);
     ctx->hmapL.assign(nl, 0);
     ctx->hmapU.assign(nl, 0);
@@ -563,6 +566,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                     } else if (lci[p] > i) {
                         ctx->Uci[qU] = (int32_t)(la + lci[p]);
                         bmul(bs, &ctx->Dinv[b2 * li], &W[b2 * p], &ctx->Uv[b2 * qU]);
+                        if (want_ilu) std::memcpy(&ctx->Uraw[b2 * qU], &W[b2 * p], b2 * sizeof(double));
                         ++qU;
                     }
                 }
@@ -718,7 +722,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         mp = SlabMaps{ctx->SlabLoff.data(), ctx->SlabUoff.data(), ctx->SlabDoff.data(),
                       ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data()};
     }
-    auto build_slab = [&](ddi::Slab &slab, bool spin) {
+    auto build_slab = [&](ddi::Slab &slab, bool spin, const std::vector<double> &Uvals, const SlabMaps &mp) {
         const int rmax = slab.rows_per_rec;
         std::vector<std::vector<uint8_t>> per(nsl);
         slab.info.assign(nsl, SubInfo{});
@@ -736,7 +740,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             auto rowU = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Urp[li + 1] - ctx->Urp[li]), &ctx->Uci[ctx->Urp[li]],
-                              &ctx->Uv[b2 * ctx->Urp[li]], &ctx->Dinv[b2 * li], ctx->Urp[li], li};
+                              &Uvals[b2 * ctx->Urp[li]], &ctx->Dinv[b2 * li], ctx->Urp[li], li};
             };
             std::vector<std::vector<RowRef>> gL, gU;
             std::vector<bool> bL, bU;
@@ -803,7 +807,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     };
     // one level-ordered slab serves every variant (level order is a
     // topological order, which the sync-free variant also walks)
-    build_slab(ctx->slab_lvl, false);
+    build_slab(ctx->slab_lvl, false, ctx->Uv, mp);
+    if (want_ilu) {
+        ctx->slab_ilu.rows_per_rec = ctx->slab_lvl.rows_per_rec;
+        build_slab(ctx->slab_ilu, false, ctx->Uraw, SlabMaps{});
+        std::vector<double>().swap(ctx->Uraw);
+    } else {
+        ctx->variants &= ~DD_ILU0;
+    }
 
     // ---- sliced-ELL SpMV operand
     {
