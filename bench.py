@@ -36,6 +36,9 @@ CONFIGS = {
                  tiles=(16, 16, 8), tol=1e-8, golden="cfg3_laplacian160_P2048"),
     "cfg4": dict(workload="spe10style_60x220x85_bsr3_P3400", kind="spe10", grid=(60, 220, 85),
                  tiles=(10, 20, 17), tol=1e-8, golden="cfg4_spe10style_P3400"),
+    # config 4 with the subdomain size chosen to fill whole waves (dd_choose_tiles)
+    "cfg4auto": dict(workload="spe10style_60x220x85_bsr3_autotiles", kind="spe10", grid=(60, 220, 85),
+                     tiles="auto", tol=1e-8, golden=None),
     "cfg5": dict(workload="laplacian_320^3_bsr3_P2048", kind="laplacian", grid=(320, 320, 320),
                  tiles=(16, 16, 8), tol=1e-8, golden=None),
 }
@@ -184,6 +187,9 @@ def run_reference(args, cfg):
     import numpy as np
     import oracle
     rp, ci, v, b = make_inputs(cfg)
+    if cfg["tiles"] == "auto":  # the host occupancy model of dd_choose_tiles
+        import paper_2508_04917_b200 as dd
+        cfg = dict(cfg, tiles=dd.dd_choose_tiles(cfg["grid"], device=-1))
     oracle.set_threads(0)
     S = oracle.setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"])
     br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
@@ -240,6 +246,7 @@ def run_ours(args, cfg):
     ctx = dd.dd_setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"], device=local, rank=rank, world=world,
                       nccl_id=nccl_id, enable_refactor=True, comm=args.comm if world > 1 else "nccl")
     setup_ms = 1e3 * (time.perf_counter() - t0)
+    cfg = dict(cfg, tiles=ctx.tiles)  # "auto" resolved by dd_choose_tiles
     # GPU numeric re-factorisation of the same pattern, values already on the device
     vd = torch.from_numpy(v).cuda()
     ctx.refactor(vd)
@@ -351,7 +358,7 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "grid": list(cfg["grid"]), "tiles": list(cfg["tiles"]),
+        "config": {"workload": cfg["workload"], "grid": list(cfg["grid"]), "tiles": list(ctx.tiles),
                    "n_block_rows": ctx.N, "nnzb": st["nnzb_before"], "nnzb_after_drop": st["nnzb_after"],
                    "n_subdomains": st["n_sub"], "tol": cfg["tol"], "parallelism": f"subdomains/rank x{world}",
                    "l2": "inputs > L2 (2.2 GB factors + 2.2 GB matrix per apply/SpMV vs 126 MB L2); no flush"},

@@ -294,7 +294,8 @@ dd_status dd_get_send_rows(const dd_ctx *ctx, int32_t peer, int64_t *n, int32_t 
 /* stats[16]: {nnzb_before, nnzb_after, n_sub_global, n_sub_local, max_levels_L,
  *   max_levels_U, max_P, slab_bytes_levelset, slab_bytes_spin, spmv_bytes,
  *   apply_canonical_bytes, spmv_canonical_bytes, n_local, n_ghost,
- *   kernels launched so far, 0};
+ *   kernels launched so far, shared-vector slot swizzle
+ *   (s1 | p1 << 8 | s2 << 16 | p2 << 24: slot(i) = i + (i >> s1) p1 + (i >> s2) p2)};
  * setup_ms[6]: {partition+permute, reorder+drop, ilu0+ildu0, levels,
  *   pack, device upload}. Either may be NULL. */
 dd_status dd_stats(const dd_ctx *ctx, int64_t *stats, double *setup_ms);
@@ -314,6 +315,17 @@ dd_status dd_launch_info(const dd_ctx *ctx, int32_t variant, int64_t *info);
  * DD_SPINLOOP | DD_DIRECT; ms[3] (nullable) = the measured apply times of
  * {level set, sync-free, direct} in ms (0 = not timed / unavailable). */
 dd_status dd_solver_variant(const dd_ctx *ctx, int32_t *variant, double *ms);
+
+/* Subdomain sizing for Alg. 2 tiles (north star: "sizes each subdomain so
+ * its vector fits shared memory"): among tile dims (tx,ty,tz) dividing
+ * (nx,ny,nz) with P = tx*ty*tz in [P_target/2, 2*P_target] (0 -> 2048, the
+ * paper's P:1041) whose vector fits, pick the one whose subdomain count fills
+ * whole waves of the apply kernel's CTA slots on `device` (SMs x resident
+ * CTAs, from the CUDA occupancy API; device < 0: an analytic model), then P
+ * nearest the target, then the most compact tile. Writes g->tx/ty/tz.
+ * dd_setup calls it when opts.grid has tx = ty = tz = 0 (P_target =
+ * opts.subdomain_rows). DD_E_GRID_NOT_DIVISIBLE if no tile shape qualifies. */
+dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_target);
 
 /* 128-byte ncclUniqueId for world > 1 (rank 0 calls it; the caller
  * broadcasts the bytes, e.g. with torch.distributed). */

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -318,16 +319,68 @@ dd_status dd_setup_csr(const dd_csr *A, const dd_opts *o, dd_ctx **out) {
     return setup_common(&B, o, out, 1);
 }
 
-static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o, dd_ctx **out, int bs) {
+dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_target) {
+    if (!g || g->nx <= 0 || g->ny <= 0 || g->nz <= 0 || (bs != 1 && bs != 3)) {
+        set_error("dd_choose_tiles: bad grid or block size");
+        return DD_E_INVALID_ARG;
+    }
+    if (P_target <= 0) P_target = 2048;  // the paper's subdomain size
+    const int64_t N = (int64_t)g->nx * g->ny * g->nz;
+    std::map<int, int> slots_of;
+    double best_key[3] = {-1, 0, 0};
+    int bt[3] = {0, 0, 0};
+    for (int tx = 1; tx <= g->nx; ++tx) {
+        if (g->nx % tx) continue;
+        for (int ty = 1; ty <= g->ny; ++ty) {
+            if (g->ny % ty) continue;
+            for (int tz = 1; tz <= g->nz; ++tz) {
+                if (g->nz % tz) continue;
+                const int64_t P = (int64_t)tx * ty * tz;
+                if (2 * P < P_target || P > 2 * (int64_t)P_target || 8 * bs * P > 232448 - 16384) continue;
+                auto it = slots_of.find((int)P);
+                const int slots = it != slots_of.end() ? it->second : (slots_of[(int)P] = tile_slots(device, bs, (int)P));
+                if (slots <= 0) continue;
+                const int64_t n_sub = N / P;
+                const int64_t waves = (n_sub + slots - 1) / slots;
+                const double eff = (double)n_sub / (double)(waves * slots);
+                // whole waves first (2 % buckets), then P near the target, then
+                // compact tiles (fewer couplings dropped per row)
+                const double key[3] = {std::floor(eff * 50.0) / 50.0, -std::fabs(std::log((double)P / P_target)),
+                                       -(1.0 / tx + 1.0 / ty + 1.0 / tz)};
+                if (std::lexicographical_compare(best_key, best_key + 3, key, key + 3)) {
+                    std::copy(key, key + 3, best_key);
+                    bt[0] = tx, bt[1] = ty, bt[2] = tz;
+                }
+            }
+        }
+    }
+    if (!bt[0]) {
+        set_error("dd_choose_tiles: no tile shape within [P/2, 2P] divides the grid");
+        return DD_E_GRID_NOT_DIVISIBLE;
+    }
+    g->tx = bt[0], g->ty = bt[1], g->tz = bt[2];
+    return DD_OK;
+}
+
+static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **out, int bs) {
     if (!out) {
         set_error("dd_setup: out is NULL");
         return DD_E_INVALID_ARG;
     }
     *out = nullptr;
-    if (!A || !o) {
+    if (!A || !o_in) {
         set_error("dd_setup: NULL argument");
         return DD_E_INVALID_ARG;
     }
+    // grid given with tile dims 0: choose the tiles (dd_choose_tiles)
+    dd_opts o_auto = *o_in;
+    dd_grid g_auto;
+    if (o_in->grid && o_in->grid->tx == 0 && o_in->grid->ty == 0 && o_in->grid->tz == 0) {
+        g_auto = *o_in->grid;
+        TRY(dd_choose_tiles(&g_auto, o_in->host_only ? -1 : o_in->device, bs, o_in->subdomain_rows));
+        o_auto.grid = &g_auto;
+    }
+    const dd_opts *o = &o_auto;
     auto *ctx = new dd_ctx();
     ctx->bs = bs;
     ctx->device = o->device;
@@ -389,6 +442,7 @@ void dd_destroy(dd_ctx *c) {
         cudaFree(c->spmv.vals);
         cudaFree(c->d_new_to_old_local);
         cudaFree(c->d_stage);
+        cudaFree(c->d_vecg);
         if (Workspace *ws = ws_of(c)) {
             for (double *q : {ws->r, ws->rh, ws->p, ws->v, ws->ph, ws->s, ws->sh, ws->t, ws->bd, ws->xd, ws->sc,
                               ws->loc, ws->gathered, ws->sendbuf})
@@ -621,7 +675,9 @@ dd_status dd_stats(const dd_ctx *c, int64_t *stats, double *setup_ms) {
         stats[12] = nl;
         stats[13] = (int64_t)c->ghost_rows.size();
         stats[14] = c->n_launches;
-        stats[15] = 0;
+        // shared-vector swizzle: s1 | p1 << 8 | s2 << 16 | p2 << 24 (identity: p1 = p2 = 0)
+        stats[15] = (int64_t)c->swz.s1 | ((int64_t)c->swz.p1 << 8) | ((int64_t)c->swz.s2 << 16) |
+                    ((int64_t)c->swz.p2 << 24);
     }
     if (setup_ms)
         for (int q = 0; q < 6; ++q) setup_ms[q] = c->setup_ms[q];

@@ -63,6 +63,17 @@ constexpr int TCB = BS == 1 ? 256 : 128;
 
 __host__ __device__ constexpr uint32_t al8(uint32_t x) { return (x + 7u) & ~7u; }
 
+// shared-vector index of element q = bs*i + c of the subdomain (Swz)
+template <int BS>
+__device__ __forceinline__ uint32_t vslot(const ddi::Swz &sw, uint32_t q) {
+    if constexpr (BS == 1) {
+        return sw.slot(q);
+    } else {
+        const uint32_t i = q / 3u;
+        return 3u * sw.slot(i) + (q - 3u * i);
+    }
+}
+
 // ---- readers: map a byte offset inside the current record to data
 struct GlobalRd {  // direct variant: the record in HBM
     const uint8_t *p;
@@ -574,7 +585,8 @@ template <int BS, int GEN, int MODE = AM_VC, bool VECG = false>
 __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
                                                      const double *__restrict__ r, double *__restrict__ z,
-                                                     uint32_t pf_bytes, const int *skip, int phase) {
+                                                     uint32_t pf_bytes, const int *skip, int phase, ddi::Swz sw,
+                                                     double *__restrict__ gvec, int vec_rows) {
     // inside dd_bicgstab: skip (uniformly) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -583,7 +595,9 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
         const SubInfo si = info[s];
         const uint8_t *base = slab + si.stream_off;
         const uint32_t sz = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
-        double *vec = VECG ? z + BS * (int64_t)si.row0 : reinterpret_cast<double *>(smem);
+        // VECG: the vector in global memory, in the slot layout of the
+        // descriptors (one vec_rows-row region per subdomain of gvec)
+        double *vec = VECG ? gvec + BS * (int64_t)s * vec_rows : reinterpret_cast<double *>(smem);
         uint32_t pf = 0;
         if (t == 0 && pf_bytes) {
             pf = min(sz, pf_bytes);
@@ -591,7 +605,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
         }
         const int nd = BS * si.nrows;
         const double *rs = r + BS * (int64_t)si.row0;
-        for (int q = t; q < nd; q += TCB<BS>) vec[q] = __ldg(rs + q);
+        for (int q = t; q < nd; q += TCB<BS>) vec[vslot<BS>(sw, q)] = __ldg(rs + q);
         __syncthreads();
         uint32_t ro = 0;
         while (ro < sz) {
@@ -619,11 +633,9 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
             ro += h.bytes;
             if (last) break;
         }
-        if (!VECG) {
-            // thread t stores the entries it fills for the next subdomain: no barrier
-            double *zs = z + BS * (int64_t)si.row0;
-            for (int q = t; q < nd; q += TCB<BS>) zs[q] = vec[q];
-        }
+        // thread t stores the entries it fills for the next subdomain: no barrier
+        double *zs = z + BS * (int64_t)si.row0;
+        for (int q = t; q < nd; q += TCB<BS>) zs[q] = vec[vslot<BS>(sw, q)];
     }
 }
 
@@ -647,7 +659,7 @@ template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN, int MODE = AM_
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
                  const double *__restrict__ r, double *__restrict__ z, int vec_bytes, int mode, const int *skip,
-                 int phase, ddi::HaloOut ho) {
+                 int phase, ddi::HaloOut ho, ddi::Swz sw) {
     // inside dd_bicgstab: skip (uniformly, before any barrier) once the solver has stopped
     if (skip && *reinterpret_cast<const volatile int *>(skip) != 0) return;
     constexpr uint32_t NST = RING / CH;
@@ -786,7 +798,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             // to z for the previous subdomain -- so no barrier is needed
             // between that store and this fill
             for (uint32_t q = qlo + (t + TC - qlo % TC) % TC; q < qhi; q += TC)
-                vec[q] = *reinterpret_cast<const double *>(ring + ((abs0 + shift + 8u * q) & (RING - 1u)));
+                vec[vslot<BS>(sw, q)] = *reinterpret_cast<const double *>(ring + ((abs0 + shift + 8u * q) & (RING - 1u)));
             if ((c + 1) % (NST / 2) == 0 && c + 1 < nrc) {
                 named_bar_sync(1, TC);
                 release_to(gbase + c + 1);
@@ -848,7 +860,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             release_to(gbase + ro / CH);
         }
         double *zs = z + BS * (int64_t)si.row0;
-        for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[q];
+        for (uint32_t q = t; q < nd; q += TC) zs[q] = vec[vslot<BS>(sw, q)];
         // fused halo: the subdomain's rows that peers read in
         // the next SpMV go straight from shared memory to their destination
         // (send buffer or the peer's ghost block); the CTA then waits before
@@ -860,7 +872,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                     const int li = ho.row[e];
                     double *d = ho.dst[e];
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) d[c] = vec[BS * li + c];
+                    for (int c = 0; c < BS; ++c) d[c] = vec[BS * sw.slot(li) + c];
                 }
                 // peer transports publish the rows with a flag after this
                 // kernel: the NVLink stores must be performed system-wide first
@@ -874,7 +886,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
 
 // ------------------------------------------------------------ host side
 using RingFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, int, int, const int *, int,
-                        ddi::HaloOut);
+                        ddi::HaloOut, ddi::Swz);
 
 template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN, int MODE>
 static RingFn ring_fn() {
@@ -913,7 +925,7 @@ static RingFn pick_ring(int bs, int ring, bool spin, bool gen, int mode = AM_VC)
 }
 
 using DirectFn = void (*)(const uint8_t *, const SubInfo *, int, const double *, double *, uint32_t, const int *,
-                          int);
+                          int, ddi::Swz, double *, int);
 // vecg: the vector in global memory (no shared-memory vector)
 static DirectFn pick_direct(int bs, bool gen, int mode = AM_VC, bool vecg = false) {
     // the 3x3 direct ablation keeps the one-block-per-step general path compiled
@@ -963,8 +975,10 @@ dd_status apply_prepare(dd_ctx *ctx) {
     const int nsl = ctx->sub_last - ctx->sub_first;
     const int bs = ctx->bs;
     const bool gen = ctx->kmax > 3;
-    const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
-    const int flag_bytes = ((8 * ((ctx->max_P + 31) / 32)) + 15) / 16 * 16;  // sync-free ready bits: 2 per row
+    if (ctx->vec_rows <= 0) ctx->vec_rows = ctx->max_P;
+    const int vec_bytes = ((8 * bs * ctx->vec_rows + 127) / 128) * 128;
+    // sync-free ready bits: 2 per shared-vector slot
+    const int flag_bytes = ((8 * ((ctx->vec_rows + 31) / 32)) + 15) / 16 * 16;
     const int tc = bs == 1 ? TCB<1> : TCB<3>;
     // ---- direct (ablation): one CTA per subdomain, as many per SM as fit
     {
@@ -1053,6 +1067,37 @@ dd_status apply_prepare(dd_ctx *ctx) {
     return DD_OK;
 }
 
+// CTA slots (SMs x resident CTAs) the level-set ring kernel gets for
+// subdomains of P rows with 7-point records (the largest ring at the best
+// occupancy, as apply_prepare picks it); 0 if the vector does not fit. Used
+// by dd_choose_tiles to size subdomains in whole waves. Without a device: an
+// analytic model (228 KB shared memory and 3 CTAs per SM by registers).
+int tile_slots(int device, int bs, int P) {
+    using namespace ddk;
+    const int vec_bytes = ((8 * bs * P + 127) / 128) * 128;
+    cudaDeviceProp prop;
+    const bool dev = device >= 0 && cudaGetDeviceProperties(&prop, device) == cudaSuccess;
+    if (!dev) cudaGetLastError();
+    const int sms = dev ? prop.multiProcessorCount : 148;
+    const int smem_max = dev ? (int)prop.sharedMemPerBlockOptin : 232448;
+    const int tc = bs == 1 ? TCB<1> : TCB<3>;
+    int best = 0;
+    for (int rc : {131072, 65536, 32768}) {
+        const int sm = vec_bytes + rc + 16 * (rc / ring_chunk(rc));
+        if (sm > smem_max) continue;
+        int occ = 0;
+        if (dev) {
+            allow_max_smem(pick_ring(bs, rc, false, false), smem_max);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_ring(bs, rc, false, false), tc + 32, sm);
+        } else {
+            occ = std::min(3, (233472 - 1024) / (sm + 1024));
+        }
+        best = std::max(best, occ);
+    }
+    cudaGetLastError();
+    return sms * best;
+}
+
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip,
                        const HaloOut *halo) {
     using namespace ddk;
@@ -1061,7 +1106,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     if (nsl == 0) return DD_OK;
     const int bs = ctx->bs;
     const bool gen = ctx->kmax > 3;
-    const int vec_bytes = ((8 * bs * ctx->max_P + 127) / 128) * 128;
+    const int vec_bytes = ((8 * bs * ctx->vec_rows + 127) / 128) * 128;
     // DD_LOWER: the lower sweep alone, z = L^-1 r (Table 3 analogue)
     const int phase = (variant & DD_LOWER) ? 1 : 0;
     variant &= ~DD_LOWER;
@@ -1083,12 +1128,20 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
     auto ring = [&](const LaunchCfg &c, bool spin, int m, const double *rr, int ph, const uint8_t *sb,
                     const SubInfo *si) {
         pick_ring(bs, c.ring, spin, gen, m)<<<c.grid, c.threads, c.smem, st>>>(sb, si, nsl, rr, z, vec_bytes, mode,
-                                                                              skip, ph, ho);
+                                                                              skip, ph, ho, ctx->swz);
     };
     auto direct = [&](int m, bool vg, int smem) {
-        pick_direct(bs, gen, m, vg)<<<nsl, ctx->cfg_direct.threads, smem, st>>>(slab, info, nsl, r, z, pf, skip,
-                                                                               phase);
+        pick_direct(bs, gen, m, vg)<<<nsl, ctx->cfg_direct.threads, smem, st>>>(
+            slab, info, nsl, r, z, pf, skip, phase, ctx->swz, ctx->d_vecg, ctx->vec_rows);
     };
+    if ((variant == DD_EDGE_GLOBAL || variant == DD_DIRECT_GLOBAL) && !ctx->d_vecg) {
+        // the global-memory vector of the no-LDS ablations (slot layout)
+        if (cudaMalloc(&ctx->d_vecg, sizeof(double) * bs * (size_t)ctx->vec_rows * nsl) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("dd_apply: cannot allocate the global vector of the no-LDS variant");
+            return DD_E_OOM;
+        }
+    }
     switch (variant) {
         case DD_LEVELSET: ring(ctx->cfg_lvl, false, AM_VC, r, phase, slab, info); break;
         case DD_UNFUSED:

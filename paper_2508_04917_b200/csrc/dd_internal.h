@@ -91,6 +91,17 @@ struct HaloOut {
     double *const *dst = nullptr;  // [E]
 };
 
+// Shared-memory slot of subdomain-local row i (bank-conflict swizzle, chosen
+// at setup by a bank model of the slab's access pattern; identity = shifts
+// of 31): slot(i) = i + (i >> s1) * p1 + (i >> s2) * p2. The packer writes
+// slots (not rows) into the record descriptors, so the sweeps index the
+// shared vector directly; only the r fill / z store / halo epilogue map
+// element q = bs*i + c to bs*slot(i) + c.
+struct Swz {
+    uint32_t s1 = 31, p1 = 0, s2 = 31, p2 = 0;
+    __host__ __device__ uint32_t slot(uint32_t i) const { return i + (i >> s1) * p1 + (i >> s2) * p2; }
+};
+
 struct LaunchCfg {
     int grid = 0, threads = 0, smem = 0, ring = 0, consumers = 0;
 };
@@ -114,6 +125,8 @@ struct dd_ctx {
     int32_t sub_first = 0, sub_last = 0;  // local subdomains [first, last)
     int64_t row_first = 0, n_local = 0;   // reordered global rows
     int32_t max_P = 0;
+    ddi::Swz swz;                   // shared-vector slot swizzle (identity for scalar rows)
+    int32_t vec_rows = 0;           // slot(max_P - 1) + 1: rows of the shared vector
     int32_t kmax = 0;  // most blocks of a row in one factor triangle (> 3: general-K kernels)
     // factors of the local rows (local numbering)
     std::vector<int64_t> Lrp, Urp;
@@ -146,6 +159,7 @@ struct dd_ctx {
     // --- device state
     void *d_new_to_old_local = nullptr;  // int32 [n_local]: global orig row of local row
     double *d_stage = nullptr;           // staging for permute (3N doubles)
+    double *d_vecg = nullptr;            // DD_EDGE_GLOBAL / DD_DIRECT_GLOBAL: global vector (slot layout)
     double *d_xghost = nullptr;          // spmv input with ghost space (world>1)
     double *d_sendbuf = nullptr;
     void *dev_ws = nullptr;              // BiCGSTAB workspace (api.cpp)
@@ -181,5 +195,6 @@ double now_ms();
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream,
                        const int *skip = nullptr, const HaloOut *halo = nullptr);
 dd_status apply_prepare(dd_ctx *ctx);  // choose launch cfgs, set smem attributes
+int tile_slots(int device, int bs, int P);  // CTA slots of the level-set kernel for P-row subdomains
 void spmv_launch(const dd_ctx *ctx, const double *x, double *y, void *stream);
 }  // namespace ddi

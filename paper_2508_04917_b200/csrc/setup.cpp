@@ -119,7 +119,7 @@ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Append one record for `rows` (already sorted by nblk descending, stable).
 void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool upper,
-                uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp, int b2) {
+                uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp, int b2, const Swz &sw) {
     const int w = (int)rows.size();
     int K = 0;
     int nnz = 0;
@@ -151,8 +151,9 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
     for (int t = 0; t < w; ++t) {
         uint16_t *d = reinterpret_cast<uint16_t *>(p + off_desc + dw * t);
         for (size_t q = 0; q < dw / 2; ++q) d[q] = 0xFFFF;
-        d[0] = (uint16_t)rows[t].row;
-        for (int k = 0; k < rows[t].nblk; ++k) d[1 + k] = (uint16_t)(rows[t].cols[k] - col_base);
+        // shared-vector slots (Swz), not rows: the kernels index the vector directly
+        d[0] = (uint16_t)sw.slot((uint32_t)rows[t].row);
+        for (int k = 0; k < rows[t].nblk; ++k) d[1 + k] = (uint16_t)sw.slot((uint32_t)(rows[t].cols[k] - col_base));
     }
     if (upper) {
         double *dv = reinterpret_cast<double *>(p + off_dinv);
@@ -185,7 +186,7 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
 // groups: sequences of rows; barrier after each group with barrier flag.
 void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &groups,
                  const std::vector<bool> &barrier, bool upper, int rmax, int32_t col_base,
-                 int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp, int b2) {
+                 int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp, int b2, const Swz &sw) {
     for (size_t g = 0; g < groups.size(); ++g) {
         auto &rows = groups[g];
         std::stable_sort(rows.begin(), rows.end(),
@@ -197,13 +198,114 @@ void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &gr
             uint16_t fl = 0;
             if (e == w && barrier[g]) fl |= REC_BARRIER;
             if (last_section && g + 1 == groups.size() && e == w) fl |= REC_LAST;
-            put_record(out, part, upper, fl, col_base, max_rec, mp, b2);
+            put_record(out, part, upper, fl, col_base, max_rec, mp, b2, sw);
             ++n_rec;
         }
     }
 }
 
 }  // namespace
+
+// ------------------------------------------------ shared-vector swizzle
+// Bank model of the level-set kernel's vector accesses (8-byte accesses, a
+// warp served in two 16-lane halves, 32 four-byte banks): per record warp,
+// the own row's 3 loads + 3 stores and, for each of up to 3 blocks, the 3
+// loads of x_j (absent blocks read the own row, branch-free path). Returns
+// the wavefronts of one subdomain under swizzle sw.
+namespace {
+int64_t bank_cost(const dd_ctx *ctx, int64_t la, int64_t P, int rmax, const Swz &sw) {
+    int64_t cost = 0;
+    auto wave = [](const uint32_t *word, int n) {
+        int64_t tot = 0;
+        for (int h0 = 0; h0 < n; h0 += 16) {
+            uint32_t seen[32][32];
+            int cnt[32] = {0};
+            int mx = 0;
+            for (int l = h0; l < std::min(n, h0 + 16); ++l)
+                for (uint32_t w : {word[l], word[l] + 1}) {
+                    const int b = (int)(w & 31u);
+                    bool dup = false;
+                    for (int q = 0; q < cnt[b]; ++q) dup |= seen[b][q] == w;
+                    if (!dup) seen[b][cnt[b]++] = w;
+                    mx = std::max(mx, cnt[b]);
+                }
+            tot += mx;
+        }
+        return tot;
+    };
+    for (int up = 0; up < 2; ++up) {
+        const auto &hm = up ? ctx->hmapU : ctx->hmapL;
+        const auto &rp = up ? ctx->Urp : ctx->Lrp;
+        const auto &cl = up ? ctx->Uci : ctx->Lci;
+        int32_t hmax = 0;
+        for (int64_t i = 0; i < P; ++i) hmax = std::max(hmax, hm[la + i]);
+        std::vector<std::vector<int64_t>> lv(hmax + 1);
+        for (int64_t i = 0; i < P; ++i) lv[hm[la + i]].push_back(i);
+        for (int32_t l = up ? 0 : 1; l <= hmax; ++l) {
+            auto &rows = lv[l];
+            std::stable_sort(rows.begin(), rows.end(), [&](int64_t a, int64_t b) {
+                return rp[la + a + 1] - rp[la + a] > rp[la + b + 1] - rp[la + b];
+            });
+            for (size_t w0 = 0; w0 < rows.size(); w0 += 32) {
+                // warps never straddle records (rmax is a multiple of 32 or smaller)
+                const int n = (int)std::min<size_t>(32, std::min(rows.size() - w0, (size_t)rmax - w0 % rmax));
+                uint32_t word[32];
+                for (int c = 0; c < 3; ++c) {
+                    for (int q = 0; q < n; ++q) word[q] = 2u * (3u * sw.slot((uint32_t)rows[w0 + q]) + c);
+                    cost += 2 * wave(word, n);
+                }
+                for (int k = 0; k < 3; ++k)
+                    for (int c = 0; c < 3; ++c) {
+                        for (int q = 0; q < n; ++q) {
+                            const int64_t i = rows[w0 + q], li = la + i;
+                            const int64_t j = k < rp[li + 1] - rp[li] ? cl[rp[li] + k] - la : i;
+                            word[q] = 2u * (3u * sw.slot((uint32_t)j) + c);
+                        }
+                        cost += wave(word, n);
+                    }
+            }
+        }
+    }
+    return cost;
+}
+}  // namespace
+
+// Pick the slot swizzle with the fewest modelled wavefronts on (up to 3)
+// sample subdomains, among those that add at most 32 slots (768 B: the
+// shared-memory budget keeps its CTAs per SM). 3x3 rows only; DD_SWZ=0 keeps
+// the identity. Sets ctx->swz and ctx->vec_rows.
+void choose_swizzle(dd_ctx *ctx, int64_t r0) {
+    ctx->swz = Swz{};
+    ctx->vec_rows = ctx->max_P;
+    const char *e = getenv("DD_SWZ");
+    if (ctx->bs != 3 || ctx->max_P <= 0 || (e && atoi(e) == 0)) return;
+    const int nsl = ctx->sub_last - ctx->sub_first;
+    std::vector<Swz> cands{Swz{}};
+    for (uint32_t s1 = 4; s1 <= 9; ++s1)
+        for (uint32_t p1 = 1; p1 <= 7; ++p1)
+            for (uint32_t s2 : {31u, 8u, 9u, 10u, 11u})
+                for (uint32_t p2 : {0u, 1u, 2u, 3u, 5u}) {
+                    if ((s2 == 31) != (p2 == 0) || (s2 != 31 && s2 <= s1)) continue;
+                    const Swz c{s1, p1, s2, p2};
+                    if (c.slot((uint32_t)ctx->max_P - 1) + 1 - (uint32_t)ctx->max_P <= 32) cands.push_back(c);
+                }
+    std::vector<int64_t> cost(cands.size(), 0);
+    const int rmax = ctx->bs == 1 ? 256 : 128;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int q = 0; q < (int)cands.size(); ++q)
+        for (int s = 0; s < std::min(nsl, 3); ++s) {
+            const int32_t g = ctx->sub_first + s * std::max(1, nsl / 3);
+            const int64_t a = ctx->sub_ptr[g], P = ctx->sub_ptr[g + 1] - a;
+            cost[q] += bank_cost(ctx, a - r0, P, rmax, cands[q]);
+        }
+    int best = 0;
+    for (int q = 1; q < (int)cands.size(); ++q)
+        if (cost[q] < cost[best]) best = q;
+    // keep the identity unless the gain is worth the extra integer work (> 5 %)
+    if (cost[best] * 20 >= cost[0] * 19) best = 0;
+    ctx->swz = cands[best];
+    ctx->vec_rows = (int32_t)ctx->swz.slot((uint32_t)ctx->max_P - 1) + 1;
+}
 
 // ------------------------------------------------------------ host setup
 dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
@@ -711,6 +813,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         ctx->slab_lvl.rows_per_rec = rmax;
         ctx->slab_spin.rows_per_rec = rmax;
     }
+    choose_swizzle(ctx, r0);
     SlabMaps mp;
     if (ctx->refactor) {
         ctx->SlabLoff.assign(ctx->Lci.size(), 0);
@@ -775,9 +878,9 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             }
             int32_t nrec = 0;
             int64_t mr = 0;
-            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp, b2);
+            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp, b2, ctx->swz);
             slab.info[q].u_off = (int32_t)per[q].size();
-            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp, b2);
+            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp, b2, ctx->swz);
             slab.info[q].stream_bytes = (int32_t)per[q].size();
             slab.info[q].row0 = (int32_t)la;
             slab.info[q].nrows = (int32_t)P;
