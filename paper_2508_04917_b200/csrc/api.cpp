@@ -78,7 +78,7 @@ dd_status upload_slab(Slab &sl) {
     if (!sl.bytes.empty()) TRY(h2d_big(sl.d_bytes, sl.bytes.data(), sl.bytes.size()));
     if (!sl.info.empty())
         CK(cudaMemcpy(sl.d_info, sl.info.data(), sl.info.size() * sizeof(SubInfo), cudaMemcpyHostToDevice));
-    std::vector<uint8_t>().swap(sl.bytes);  // device copy is authoritative
+    decltype(sl.bytes)().swap(sl.bytes);  // device copy is authoritative
     return DD_OK;
 }
 

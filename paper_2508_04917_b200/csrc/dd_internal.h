@@ -4,7 +4,9 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "dd.h"
@@ -17,6 +19,27 @@
 #endif
 
 namespace ddi {
+
+// Large host arrays that are fully overwritten after allocation: resize()
+// leaves the elements uninitialised (no single-threaded zero fill of GBs).
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U> &) {}
+    template <class U>
+    void construct(U *) noexcept {}
+    template <class U, class... A>
+    void construct(U *p, A &&...a) {
+        ::new ((void *)p) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using uvector = std::vector<T, UninitAlloc<T>>;
 
 // ---------------------------------------------------------------------------
 // Factor-slab record format. One byte stream per
@@ -73,7 +96,7 @@ struct SpmvDev {
 };
 
 struct Slab {
-    std::vector<uint8_t> bytes;   // host copy (all local subdomains)
+    uvector<uint8_t> bytes;       // host copy (all local subdomains)
     std::vector<SubInfo> info;
     int32_t rows_per_rec = 128;
     int64_t max_rec_bytes = 0;
@@ -131,13 +154,13 @@ struct dd_ctx {
     // factors of the local rows (local numbering)
     std::vector<int64_t> Lrp, Urp;
     std::vector<int32_t> Lci, Uci;
-    std::vector<double> Lv, Uv, Dinv;
+    ddi::uvector<double> Lv, Uv, Dinv;
     std::vector<int32_t> hmapL, hmapU;
     int32_t max_lev_L = 0, max_lev_U = 0;
     // local rows of A_r, columns in local+ghost numbering
     std::vector<int64_t> Arp;
     std::vector<int32_t> Aci;
-    std::vector<double> Av;
+    ddi::uvector<double> Av;
     std::vector<int64_t> ghost_rows;   // reordered global ids, ascending
     std::vector<int32_t> ghost_owner;
     // halo send lists per peer (local row ids) and recv counts per peer
@@ -146,7 +169,7 @@ struct dd_ctx {
     // slabs
     ddi::Slab slab_lvl, slab_spin;
     ddi::Slab slab_ilu;                 // DD_ILU0 ablation: U records with the non-unit U_ij
-    std::vector<double> Uraw;           // non-unit U_ij (j > i), only when DD_ILU0 is requested
+    ddi::uvector<double> Uraw;          // non-unit U_ij (j > i), only when DD_ILU0 is requested
     int32_t variants = 0;
     int32_t solver_variant = DD_LEVELSET;  // apply variant inside dd_bicgstab (timed at setup)
     double variant_ms[3] = {0, 0, 0};      // level set, sync-free, direct

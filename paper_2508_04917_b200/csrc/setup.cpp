@@ -118,7 +118,15 @@ struct SlabMaps {
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Append one record for `rows` (already sorted by nblk descending, stable).
-void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool upper,
+// Output of the packer: p == nullptr sizes the stream only (first pass);
+// otherwise records are written at p + pos (p = the subdomain's stream in the
+// final slab buffer, second pass).
+struct Sink {
+    uint8_t *p = nullptr;
+    size_t pos = 0;
+};
+
+void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
                 uint16_t flags, int32_t col_base, int64_t &max_rec, const SlabMaps &mp, int b2, const Swz &sw) {
     const int w = (int)rows.size();
     int K = 0;
@@ -131,9 +139,12 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
     const size_t off_dinv = rec_off_dinv(K, w);
     const size_t off_val = off_dinv + (upper ? 8 * (size_t)b2 * w : 0);
     const size_t bytes = al(off_val + 8 * (size_t)b2 * nnz, 16);
-    const size_t base = out.size();
-    out.resize(base + bytes, 0);
-    uint8_t *p = out.data() + base;
+    const size_t base = out.pos;
+    out.pos += bytes;
+    max_rec = std::max<int64_t>(max_rec, (int64_t)bytes);
+    if (!out.p) return;
+    uint8_t *p = out.p + base;
+    std::memset(p, 0, bytes);  // padding (the slab buffer is not initialised)
     RecHdr h;
     h.w = (uint16_t)w;
     h.K = (uint16_t)K;
@@ -180,11 +191,10 @@ void put_record(std::vector<uint8_t> &out, const std::vector<RowRef> &rows, bool
             }
         pos += ck;
     }
-    max_rec = std::max<int64_t>(max_rec, (int64_t)bytes);
 }
 
 // groups: sequences of rows; barrier after each group with barrier flag.
-void pack_groups(std::vector<uint8_t> &out, std::vector<std::vector<RowRef>> &groups,
+void pack_groups(Sink &out, std::vector<std::vector<RowRef>> &groups,
                  const std::vector<bool> &barrier, bool upper, int rmax, int32_t col_base,
                  int32_t &n_rec, int64_t &max_rec, bool last_section, const SlabMaps &mp, int b2, const Swz &sw) {
     for (size_t g = 0; g < groups.size(); ++g) {
@@ -470,7 +480,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     const int64_t nnz_loc = Arp[nl];
     std::vector<int32_t> gcol(nnz_loc);
-    ctx->Av.assign(b2 * nnz_loc, 0.0);
+    ctx->Av.resize(b2 * nnz_loc);  // every block written below
     ctx->refactor = o->enable_refactor != 0;
     ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
     if (ctx->refactor) ctx->Asrc.assign(nnz_loc, -1);
@@ -594,12 +604,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     ctx->Lci.assign(ctx->Lrp[nl], 0);
     ctx->Uci.assign(ctx->Urp[nl], 0);
-    ctx->Lv.assign(b2 * ctx->Lrp[nl], 0.0);
-    ctx->Uv.assign(b2 * ctx->Urp[nl], 0.0);
+    ctx->Lv.resize(b2 * ctx->Lrp[nl]);  // written by the scatter below
+    ctx->Uv.resize(b2 * ctx->Urp[nl]);
     // DD_ILU0 ablation: keep the non-unit U_ij too (a second slab, BSR3 only)
     const bool want_ilu = bs == 3 && (o->variants & DD_ILU0) != 0;
-    if (want_ilu) ctx->Uraw.assign(b2 * ctx->Urp[nl], 0.0);
-    ctx->Dinv.assign(b2 * nl, 0.0);
+    if (want_ilu) ctx->Uraw.resize(b2 * ctx->Urp[nl]);
+    ctx->Dinv.resize(b2 * nl);
     ctx->hmapL.assign(nl, 0);
     ctx->hmapU.assign(nl, 0);
 
@@ -825,13 +835,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         mp = SlabMaps{ctx->SlabLoff.data(), ctx->SlabUoff.data(), ctx->SlabDoff.data(),
                       ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data()};
     }
-    auto build_slab = [&](ddi::Slab &slab, bool spin, const std::vector<double> &Uvals, const SlabMaps &mp) {
+    auto build_slab = [&](ddi::Slab &slab, bool spin, const uvector<double> &Uvals, const SlabMaps &mp) {
         const int rmax = slab.rows_per_rec;
-        std::vector<std::vector<uint8_t>> per(nsl);
         slab.info.assign(nsl, SubInfo{});
         int64_t max_rec = 0;
-#pragma omp parallel for schedule(dynamic, 1) reduction(max : max_rec)
-        for (int32_t q = 0; q < nsl; ++q) {
+        // subdomain q's record stream into `out` (two passes: sizes, then the
+        // records written in place in the final buffer -- no per-subdomain
+        // staging copies, no zero fill of the whole slab)
+        auto pack_sub = [&](int32_t q, Sink &out, const SlabMaps &maps, int32_t &nrec, int64_t &mr, int32_t &u_off) {
             const int32_t s = s0 + q;
             const int64_t a = ctx->sub_ptr[s], e = ctx->sub_ptr[s + 1], P = e - a;
             const int64_t la = a - r0;
@@ -876,14 +887,23 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 bL.assign(gL.size(), true);
                 bU.assign(gU.size(), true);
             }
-            int32_t nrec = 0;
+            nrec = 0;
+            mr = 0;
+            pack_groups(out, gL, bL, false, rmax, (int32_t)la, nrec, mr, false, maps, b2, ctx->swz);
+            u_off = (int32_t)out.pos;
+            pack_groups(out, gU, bU, true, rmax, (int32_t)la, nrec, mr, true, maps, b2, ctx->swz);
+        };
+#pragma omp parallel for schedule(dynamic, 4) reduction(max : max_rec)
+        for (int32_t q = 0; q < nsl; ++q) {
+            Sink sz;
+            int32_t nrec = 0, u_off = 0;
             int64_t mr = 0;
-            pack_groups(per[q], gL, bL, false, rmax, (int32_t)la, nrec, mr, false, mp, b2, ctx->swz);
-            slab.info[q].u_off = (int32_t)per[q].size();
-            pack_groups(per[q], gU, bU, true, rmax, (int32_t)la, nrec, mr, true, mp, b2, ctx->swz);
-            slab.info[q].stream_bytes = (int32_t)per[q].size();
-            slab.info[q].row0 = (int32_t)la;
-            slab.info[q].nrows = (int32_t)P;
+            pack_sub(q, sz, SlabMaps{}, nrec, mr, u_off);
+            const int32_t s = s0 + q;
+            slab.info[q].u_off = u_off;
+            slab.info[q].stream_bytes = (int32_t)sz.pos;
+            slab.info[q].row0 = (int32_t)(ctx->sub_ptr[s] - r0);
+            slab.info[q].nrows = (int32_t)(ctx->sub_ptr[s + 1] - ctx->sub_ptr[s]);
             slab.info[q].n_rec = nrec;
             max_rec = std::max(max_rec, mr);
         }
@@ -895,8 +915,10 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         slab.bytes.resize(off);
 #pragma omp parallel for schedule(dynamic, 4)
         for (int32_t q = 0; q < nsl; ++q) {
-            std::memcpy(slab.bytes.data() + slab.info[q].stream_off, per[q].data(), per[q].size());
-            std::vector<uint8_t>().swap(per[q]);
+            Sink out{slab.bytes.data() + slab.info[q].stream_off, 0};
+            int32_t nrec = 0, u_off = 0;
+            int64_t mr = 0;
+            pack_sub(q, out, mp, nrec, mr, u_off);
             if (mp.Loff) {  // stream-relative -> slab-absolute offsets
                 const int64_t so = slab.info[q].stream_off;
                 for (int64_t li = slab.info[q].row0; li < slab.info[q].row0 + slab.info[q].nrows; ++li) {
@@ -914,7 +936,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     if (want_ilu) {
         ctx->slab_ilu.rows_per_rec = ctx->slab_lvl.rows_per_rec;
         build_slab(ctx->slab_ilu, false, ctx->Uraw, SlabMaps{});
-        std::vector<double>().swap(ctx->Uraw);
+        uvector<double>().swap(ctx->Uraw);
     } else {
         ctx->variants &= ~DD_ILU0;
     }
