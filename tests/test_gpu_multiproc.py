@@ -78,14 +78,20 @@ def test_ipc_world_parity(case, world, tmp_path):
     x = np.concatenate([q["x"] for q in res])
     A = __import__("tests.helpers", fromlist=["bsr"]).bsr(S["rp_r"], S["ci_r"], S["v_r"])
     assert np.linalg.norm(A @ x - b_re) <= 1e-7 * np.linalg.norm(b_re)
-    # dd_solve_host: every rank wrote its rows of the original-order solution
+    # dd_solve_host: every rank wrote its rows of the original-order solution,
+    # the same solve as dd_bicgstab from x0 = 0 -> bitwise the permuted x
     xh = np.zeros(3 * N)
     n2o = S["new_to_old"]
     for q in res:
         f, n = int(q["first"]), int(q["n"])
         rows = n2o[f:f + n]
         xh.reshape(-1, 3)[rows] = q["xh"].reshape(-1, 3)[rows]
-    assert np.linalg.norm(xh - xs) <= 1e-6 * np.linalg.norm(xs)
+    x_orig = np.zeros(3 * N)
+    x_orig.reshape(-1, 3)[n2o] = x.reshape(-1, 3)
+    assert np.array_equal(xh, x_orig)
+    # the manufactured solution, to the accuracy the tolerance allows for this
+    # conditioning (SPE10-style: ~7 decades of permeability contrast)
+    assert np.linalg.norm(xh - xs) <= (1e-3 if case.startswith("spe10") else 1e-6) * np.linalg.norm(xs)
 
 
 def test_ipc_iterations_equal_world1_laplacian(tmp_path):

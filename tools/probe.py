@@ -15,7 +15,7 @@ ap.add_argument("--spe10", type=int, default=0)
 ap.add_argument("--stencil27", type=int, default=0, help="1: random 27-point BSR3 (general-K record path)")
 ap.add_argument("--warm", type=int, default=0, help="1: no L2 flush between reps (L2-warm)")
 a = ap.parse_args()
-grid = tuple(map(int, a.grid.split(","))); tiles = tuple(map(int, a.tiles.split(",")))
+grid = tuple(map(int, a.grid.split(","))); tiles = tuple(map(int, a.tiles.split(","))) if a.tiles != "auto" else "auto"
 t = time.time()
 if a.spe10:
     rp, ci, v, _ = spe10_style_bsr3(*grid)
@@ -26,7 +26,8 @@ else:
     rp, ci, v = laplacian_bsr3(*grid)
 print("gen", time.time() - t, flush=True)
 t = time.time()
-ctx = dd.dd_setup(rp, ci, v, grid=grid, tiles=tiles, variants=7)
+ctx = dd.dd_setup(rp, ci, v, grid=grid, tiles=tiles if a.tiles != "auto" else "auto", variants=7 | dd.DD_ILU0)
+print("tiles", ctx.tiles, "swizzle", [(ctx.stats()["swizzle"] >> s) & 255 for s in (0, 8, 16, 24)], flush=True)
 print("setup", time.time() - t, json.dumps(ctx.stats()), flush=True)
 n = ctx.n_local
 r = torch.from_numpy(apply_input(n)).cuda(); z = torch.empty_like(r)
@@ -41,13 +42,17 @@ def timeit(fn, reps):
         e0.record(); fn(); e1.record(); torch.cuda.synchronize()
         if i >= 3: ts.append(e0.elapsed_time(e1))
     return float(np.median(ts)), float(np.min(ts))
-for var, name in ((1, "levelset"), (2, "spin"), (4, "direct"), (8, "unfused")):
+VARS = [(1, "levelset"), (2, "spin"), (4, "direct"), (8, "unfused"), (16, "edge"), (32, "edge_global"),
+        (128, "direct_glob"), (64, "ilu0")]
+if os.environ.get("PROBE_LOWER", "1") == "1":  # Table 3 analogue: the lower sweep alone
+    VARS += [(v | dd.DD_LOWER, n + "+L") for v, n in VARS]
+for var, name in VARS:
     try:
         med, mn = timeit(lambda: ctx.apply(r, z, var), a.reps)
     except dd.DDError as e:
         print(f"apply {name:9s} unavailable: {e}", flush=True)
         continue
-    print(f"apply {name:9s} median {med*1e3:8.1f} us  min {mn*1e3:8.1f} us  canonical {st['apply_canonical_bytes']/med/1e6:7.1f} GB/s  slab {st['slab_bytes_levelset']/med/1e6:7.1f} GB/s  launch {ctx.launch_info(var)}", flush=True)
+    print(f"apply {name:13s} median {med*1e3:8.1f} us  min {mn*1e3:8.1f} us  canonical {st['apply_canonical_bytes']/med/1e6:7.1f} GB/s  slab {st['slab_bytes_levelset']/med/1e6:7.1f} GB/s  launch {ctx.launch_info(var)}", flush=True)
 y = torch.empty_like(r)
 med, mn = timeit(lambda: ctx.spmv(r, y), a.reps)
 print(f"spmv median {med*1e3:.1f} us  canonical {st['spmv_canonical_bytes']/med/1e6:.1f} GB/s", flush=True)
