@@ -121,6 +121,9 @@ typedef struct {
 #define DD_DIRECT_GLOBAL 128 /* vertex-centric level set with the vector in global memory */
 #define DD_LOWER 256        /* modifier OR-ed into a variant for dd_apply_variant: the lower
                                sweep alone, z = L^-1 r (Table 3's lower-solve analogue)  */
+#define DD_TREE 512         /* row-parallel: 4 lanes per row, one block per lane, partial
+                               sums combined by a fixed warp-shuffle tree (R19);
+                               deterministic, not bitwise the oracle's chain             */
 
 typedef struct {
     int32_t subdomain_rows;   /* P when grid == NULL: contiguous chunks (R26)   */
@@ -158,17 +161,21 @@ typedef struct {
  *                  world > 1 too. nccl_unique_id is any 128-byte key the ranks
  *                  share (it names the host rendezvous used during dd_setup,
  *                  dd_refactor and dd_destroy: POSIX shared memory).
- *   DD_COMM_LOCAL  the same peer-memory transport with the ranks as contexts
- *                  of ONE process (one per GPU, or several sharing a GPU),
- *                  each created and driven by its own host thread; mailboxes
- *                  are shared as plain device pointers (devices must be peer-
- *                  accessible). nccl_unique_id is any 128-byte key.
- * With either peer transport dd_setup, dd_spmv, dd_bicgstab, dd_solve_host,
- * dd_refactor and dd_destroy are collective. A device-side wait that sees no
- * progress for DD_PEER_TIMEOUT_S seconds (default 120) stops the solve and the
- * call returns DD_E_NCCL; a host rendezvous that waits longer than that fails
- * the same way. Setup and refactor status is agreed over the ranks (every rank
- * returns the same status). */
+ *   DD_COMM_LOCAL  the ranks are contexts of ONE process (one per GPU, or
+ *                  several sharing a GPU -- the single-GPU test vehicle), each
+ *                  created and driven by its own host thread; exchanges are
+ *                  device-to-device copies (and the fused apply's stores into
+ *                  the peer's ghost block) ordered by CUDA events and a host
+ *                  rendezvous per exchange, so no kernel ever waits on another
+ *                  rank (ranks sharing a GPU stay deadlock-free whatever the
+ *                  host threads do); no graph loop. nccl_unique_id is any
+ *                  128-byte key.
+ * With DD_COMM_IPC / DD_COMM_LOCAL, dd_setup, dd_spmv, dd_bicgstab,
+ * dd_solve_host, dd_refactor and dd_destroy are collective. A device-side
+ * wait that sees no progress for DD_PEER_TIMEOUT_S seconds (default 120)
+ * stops the solve and the call returns DD_E_NCCL; a host rendezvous that
+ * waits longer than that fails the same way. Setup and refactor status is
+ * agreed over the ranks (every rank returns the same status). */
 #define DD_COMM_NCCL 0
 #define DD_COMM_LOCAL 1
 #define DD_COMM_IPC 2
@@ -227,7 +234,7 @@ dd_status dd_local_range(const dd_ctx *ctx, int64_t *first_block_row, int64_t *n
 
 /* z = M^-1 r (this rank's subdomains; no communication). variant = one of
  * DD_LEVELSET / DD_SPINLOOP / DD_DIRECT / DD_UNFUSED / DD_EDGE /
- * DD_EDGE_GLOBAL / DD_DIRECT_GLOBAL / DD_ILU0, optionally | DD_LOWER;
+ * DD_EDGE_GLOBAL / DD_DIRECT_GLOBAL / DD_ILU0 / DD_TREE, optionally | DD_LOWER;
  * 0 = DD_LEVELSET. r (and z for DD_UNFUSED) must be 16-byte aligned for the
  * ring variants (DD_E_INVALID_ARG otherwise). */
 dd_status dd_apply(dd_ctx *ctx, const double *r, double *z, void *stream);

@@ -27,7 +27,7 @@ DD_LEVELSET, DD_SPINLOOP, DD_DIRECT, DD_UNFUSED = 1, 2, 4, 8
 # paper ablations (include/dd.h): edge-centric (shared / global vector), ILU0
 # with the non-unit U, vertex-centric with the vector in global memory, and the
 # DD_LOWER modifier (lower sweep alone)
-DD_EDGE, DD_EDGE_GLOBAL, DD_ILU0, DD_DIRECT_GLOBAL, DD_LOWER = 16, 32, 64, 128, 256
+DD_EDGE, DD_EDGE_GLOBAL, DD_ILU0, DD_DIRECT_GLOBAL, DD_LOWER, DD_TREE = 16, 32, 64, 128, 256, 512
 DD_PART_CHUNKS, DD_PART_BFS = 0, 1
 DD_COMM_NCCL, DD_COMM_LOCAL, DD_COMM_IPC = 0, 1, 2
 STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP", "DD_E_MISSING_DIAG",

@@ -96,7 +96,7 @@ dd_status tune_solver_variant(dd_ctx *ctx) {
     // the deterministic variants, and (ablation solves, R19) the paper's others
     static const std::pair<const char *, int> names[] = {
         {"spin", DD_SPINLOOP}, {"direct", DD_DIRECT}, {"edge", DD_EDGE}, {"edge_global", DD_EDGE_GLOBAL},
-        {"direct_global", DD_DIRECT_GLOBAL}, {"ilu0", DD_ILU0}, {"unfused", DD_UNFUSED}};
+        {"direct_global", DD_DIRECT_GLOBAL}, {"ilu0", DD_ILU0}, {"unfused", DD_UNFUSED}, {"tree", DD_TREE}};
     int v = 0;
     for (auto &nv : names)
         if (want == nv.first) v = nv.second;
@@ -416,6 +416,7 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **ou
         if (st == DD_OK) st = comm_agree(ctx, device_setup(ctx));
         if (st == DD_OK) st = comm_connect(ctx);
         if (st == DD_OK) st = tune_solver_variant(ctx);
+        if (st == DD_OK) st = solver_prepare(ctx);
     }
     if (st != DD_OK) {
         const std::string msg = last_error_c();
@@ -467,6 +468,8 @@ void dd_destroy(dd_ctx *c) {
             if (ws->graph) cudaGraphDestroy(ws->graph);
             if (ws->cap) cudaStreamDestroy(ws->cap);
             for (auto e : ws->ev)
+                if (e) cudaEventDestroy(e);
+            for (auto e : {ws->xev_ready, ws->xev_done, ws->xev_app, ws->xev_free})
                 if (e) cudaEventDestroy(e);
             cudaFree(ws->d_send_idx);
             cudaFree(ws->d_hptr);
@@ -698,6 +701,7 @@ dd_status dd_launch_info(const dd_ctx *c, int32_t variant, int64_t *info) {
                          : (variant == DD_DIRECT || variant == DD_EDGE_GLOBAL || variant == DD_DIRECT_GLOBAL)
                              ? &c->cfg_direct
                          : variant == DD_EDGE ? &c->cfg_ec
+                         : variant == DD_TREE ? &c->cfg_tree
                          : variant == DD_ILU0 ? &c->cfg_nu
                                               : &c->cfg_lvl;
     info[0] = l->grid;

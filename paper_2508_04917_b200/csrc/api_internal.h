@@ -76,7 +76,10 @@ struct Workspace {
     ddi::HaloOut hout;
     int32_t *d_hptr = nullptr, *d_hrow = nullptr;
     double **d_hdst = nullptr;
-    // ---- peer transports (DD_COMM_LOCAL / DD_COMM_IPC, peer.cuh)
+    // ---- DD_COMM_LOCAL: the group's contexts and the exchange events
+    std::vector<dd_ctx *> local_peers;
+    cudaEvent_t xev_ready = nullptr, xev_done = nullptr, xev_app = nullptr, xev_free = nullptr;
+    // ---- peer-memory transport (DD_COMM_IPC, peer.cuh)
     uint8_t *box = nullptr;              // own mailbox: flags | gathered | xg
     int64_t box_bytes = 0;
     std::vector<uint8_t *> peer_box;     // [world] mailboxes mapped here (own at [rank])
@@ -122,7 +125,7 @@ struct DeviceGuard {
         return DD_E_CUDA;                                                \
     }
 
-bool peer_comm(const dd_ctx *c);  // world > 1 with DD_COMM_LOCAL or DD_COMM_IPC
+bool peer_comm(const dd_ctx *c);  // world > 1 with DD_COMM_IPC (device-flag transport)
 
 // ---- comm.cpp
 // After the host setup: create the NCCL communicator / join the rendezvous
@@ -148,8 +151,8 @@ dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaS
 // ncclCommGetAsyncError (aborts the communicator and fails on an error)
 dd_status comm_wait_event(dd_ctx *c, cudaEvent_t ev);
 // after a synchronisation: a peer wait that timed out -> DD_E_NCCL
-dd_status comm_check(dd_ctx *c);
-// the iteration body can be captured into a CUDA graph (world 1, peer transports)
+dd_status comm_check(dd_ctx *c, cudaStream_t st);
+// the iteration body can be captured into a CUDA graph (world 1, DD_COMM_IPC)
 bool comm_graph_ok(const dd_ctx *c);
 
 // ---- api.cpp
@@ -163,5 +166,8 @@ void refactor_free(dd_ctx *c);
 
 // ---- solver.cpp
 void prof_free(dd_ctx *c);
+// device history + the captured solve graph (dd_setup, after the transport
+// is connected and the solver's apply variant is chosen)
+dd_status solver_prepare(dd_ctx *c);
 
 }  // namespace ddi

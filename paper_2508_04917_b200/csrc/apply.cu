@@ -479,6 +479,85 @@ __device__ __forceinline__ void process_record(const Rd &rd, const RecHdr &h, co
         process_record1<SPIN, GEN>(rd, h, c8, t, vec, F);
 }
 
+// Tree-shuffle record (ablation, R19/R42; the paper's row-parallel design,
+// P:409 "threads within a wavefront process the row's nonzero columns in
+// parallel"): a group of 4 lanes per row, lane k forms the products of the
+// row's blocks k, k+4, ... (p = B x_j, one FMA chain per component), the 4
+// partial sums meet in a fixed shuffle tree ((l0+l1)+(l2+l3)), and lane 0
+// writes x_i = a_i - S with a_i = z_i (L) or D_i z_i (U). Deterministic but a
+// different summation order than the oracle's chain: 1e-10 bar, not bitwise.
+// 32 rows per pass, ceil(w / 32) passes per record; all lanes take part in
+// every shuffle.
+template <int GEN, class Rd>
+__device__ __forceinline__ void process_record_tree(const Rd &rd, const RecHdr &h, const uint4 &c8, int t, int TC,
+                                                    double *vec) {
+    const uint32_t w = h.w, K = h.K;
+    const bool upper = (h.flags & ddi::REC_UPPER) != 0;
+    const uint32_t off_desc = ddi::rec_off_desc(K), dw = ddi::rec_dw(K);
+    const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
+    const uint32_t lk = (uint32_t)t & 3u;
+    for (uint32_t r0 = 0; r0 < w; r0 += (uint32_t)TC / 4u) {
+        const uint32_t r = r0 + (uint32_t)t / 4u;
+        const bool row_ok = r < w;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+        uint32_t i = 0;
+        if (row_ok) {
+            i = rd.template ld<uint16_t>(off_desc + dw * r);
+            uint32_t pre = 0;
+            for (uint32_t k = 0; k < K; ++k) {
+                const uint32_t ck = (GEN == 0 || K <= 3) ? (k == 0 ? (c8.x & 0xffffu) : k == 1 ? (c8.x >> 16) : (c8.y & 0xffffu))
+                                                          : rd.template ld<uint16_t>(16u + 2u * k);
+                if (r >= ck) break;  // rows sorted by block count: no block k or later
+                if ((k & 3u) == lk) {
+                    const uint32_t j = rd.template ld<uint16_t>(off_desc + dw * r + 2u * (1u + k));
+                    const uint32_t vb = h.off_val + 72u * pre + 8u * r, st = 8u * ck;
+                    double b[9];
+#pragma unroll
+                    for (int v = 0; v < 9; ++v) b[v] = rd.template ld<double>(vb + st * v);
+                    const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+                    p0 = __fma_rn(b[0], x0, p0);
+                    p0 = __fma_rn(b[1], x1, p0);
+                    p0 = __fma_rn(b[2], x2, p0);
+                    p1 = __fma_rn(b[3], x0, p1);
+                    p1 = __fma_rn(b[4], x1, p1);
+                    p1 = __fma_rn(b[5], x2, p1);
+                    p2 = __fma_rn(b[6], x0, p2);
+                    p2 = __fma_rn(b[7], x1, p2);
+                    p2 = __fma_rn(b[8], x2, p2);
+                }
+                pre += ck;
+            }
+        }
+        p0 += __shfl_xor_sync(0xffffffffu, p0, 1);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, 1);
+        p2 += __shfl_xor_sync(0xffffffffu, p2, 1);
+        p0 += __shfl_xor_sync(0xffffffffu, p0, 2);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, 2);
+        p2 += __shfl_xor_sync(0xffffffffu, p2, 2);
+        if (row_ok && lk == 0) {
+            double a0 = vec[3 * i], a1 = vec[3 * i + 1], a2 = vec[3 * i + 2];
+            if (upper) {
+                double D[9];
+#pragma unroll
+                for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + r));
+                const double z0 = a0, z1 = a1, z2 = a2;
+                a0 = D[0] * z0;
+                a0 = __fma_rn(D[1], z1, a0);
+                a0 = __fma_rn(D[2], z2, a0);
+                a1 = D[3] * z0;
+                a1 = __fma_rn(D[4], z1, a1);
+                a1 = __fma_rn(D[5], z2, a1);
+                a2 = D[6] * z0;
+                a2 = __fma_rn(D[7], z1, a2);
+                a2 = __fma_rn(D[8], z2, a2);
+            }
+            vec[3 * i] = a0 - p0;
+            vec[3 * i + 1] = a1 - p1;
+            vec[3 * i + 2] = a2 - p2;
+        }
+    }
+}
+
 // Edge-centric record (dag_ec_*, Table 3/4 ablation, BSR3): the
 // record's nnz blocks are spread over the TC consumer threads (block e of
 // the jagged planes: k = the plane it falls in, row slot t = e - prefix_k),
@@ -580,7 +659,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 // VECG: the vector lives in GLOBAL memory (z itself, initialised from r):
 // with MODE 1 the paper's dag_ec_no_lds (Table 3), global atomics.
 // phase 1: the lower sweep alone (z = L^-1 r, Table 3's lower solve).
-enum : int { AM_VC = 0, AM_EC = 1, AM_NU = 2 };
+enum : int { AM_VC = 0, AM_EC = 1, AM_NU = 2, AM_TREE = 3 };
 template <int BS, int GEN, int MODE = AM_VC, bool VECG = false>
 __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restrict__ slab,
                                                      const SubInfo *__restrict__ info, int n_sub,
@@ -827,6 +906,11 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             // skips it (no work, no barrier); the sync-free sweep publishes flags
             const bool skip = !SPIN && !upper && h.K == 0 && !last;
             if (mode == 1 || skip) {
+            } else if constexpr (MODE == AM_TREE && BS == 3) {
+                if (pos + h.bytes <= RING)
+                    process_record_tree<GEN>(LinRd{ring + pos}, h, c8, t, TC, vec);
+                else
+                    process_record_tree<GEN>(RingRd<RING>{ring, abs0 + ro}, h, c8, t, TC, vec);
             } else if constexpr (MODE == AM_EC && BS == 3) {
                 auto bar = [] { named_bar_sync(1, TC); };
                 if (pos + h.bytes <= RING)
@@ -915,6 +999,8 @@ static RingFn pick_ring(int bs, int ring, bool spin, bool gen, int mode = AM_VC)
     if (mode != AM_VC) {
         if (bs != 3 || spin) return nullptr;
         if (mode == AM_EC) return gen ? pick_ring_m<3, 1, false, AM_EC>(ring) : pick_ring_m<3, 0, false, AM_EC>(ring);
+        if (mode == AM_TREE)
+            return gen ? pick_ring_m<3, 1, false, AM_TREE>(ring) : pick_ring_m<3, 0, false, AM_TREE>(ring);
         return gen ? pick_ring_m<3, 1, false, AM_NU>(ring) : pick_ring_m<3, 0, false, AM_NU>(ring);
     }
     if (bs == 1)
@@ -1054,6 +1140,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
     // vector in global memory, ILU0 with the non-unit U
     if (bs == 3) {
         if (choose(ctx->cfg_ec, false, ctx->slab_lvl.max_rec_bytes, AM_EC) == DD_OK) ctx->variants |= DD_EDGE;
+        if (choose(ctx->cfg_tree, false, ctx->slab_lvl.max_rec_bytes, AM_TREE) == DD_OK) ctx->variants |= DD_TREE;
         ctx->variants |= DD_EDGE_GLOBAL | DD_DIRECT_GLOBAL;
         for (bool vg : {false, true})
             for (int m : {AM_EC, AM_VC})
@@ -1157,6 +1244,7 @@ dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, voi
         case DD_SPINLOOP: ring(ctx->cfg_spin, true, AM_VC, r, phase, slab, info); break;
         case DD_DIRECT: direct(AM_VC, false, ctx->cfg_direct.smem); break;
         case DD_EDGE: ring(ctx->cfg_ec, false, AM_EC, r, phase, slab, info); break;
+        case DD_TREE: ring(ctx->cfg_tree, false, AM_TREE, r, phase, slab, info); break;
         case DD_EDGE_GLOBAL: direct(AM_EC, true, 0); break;
         case DD_DIRECT_GLOBAL: direct(AM_VC, true, 0); break;
         case DD_ILU0:

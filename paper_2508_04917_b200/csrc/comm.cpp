@@ -3,7 +3,8 @@
 // double-double dot partials, over three transports (dd.h):
 //   DD_COMM_NCCL  grouped ncclSend/ncclRecv + ncclAllGather, async errors polled
 //   DD_COMM_IPC   peer memory between processes (CUDA IPC handles), device flags
-//   DD_COMM_LOCAL peer memory between contexts of one process, device flags
+//   DD_COMM_LOCAL contexts of one process: device-to-device copies ordered by
+//                 CUDA events and a host rendezvous per exchange
 // plus the host rendezvous (setup / refactor / destroy only) that agrees on
 // a status over the ranks and exchanges the mailbox addresses.
 #include <cuda_runtime.h>
@@ -302,7 +303,8 @@ int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 
 }  // namespace
 
-bool peer_comm(const dd_ctx *c) { return c->world > 1 && (c->comm == DD_COMM_LOCAL || c->comm == DD_COMM_IPC); }
+bool peer_comm(const dd_ctx *c) { return c->world > 1 && c->comm == DD_COMM_IPC; }
+static bool local_comm(const dd_ctx *c) { return c->world > 1 && c->comm == DD_COMM_LOCAL; }
 
 dd_status comm_agree(dd_ctx *c, dd_status st) {
     if (c->world <= 1 || c->host_only) return st;
@@ -383,6 +385,9 @@ dd_status comm_alloc(dd_ctx *c) {
         TRY(dmalloc(&ws->gathered, 6 * (size_t)std::max(1, c->world)));
         TRY(dmalloc(&ws->sendbuf, std::max<size_t>(1, c->bs * sidx.size())));
         TRY(upload_vec(&ws->d_send_idx, sidx));
+        if (local_comm(c))
+            for (cudaEvent_t *e : {&ws->xev_ready, &ws->xev_done, &ws->xev_app, &ws->xev_free})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         return DD_OK;
     }
     // mailbox: flags | gathered | xg (+16 B slack)
@@ -419,6 +424,35 @@ dd_status comm_alloc(dd_ctx *c) {
 dd_status comm_connect(dd_ctx *c) {
     if (c->world <= 1) return DD_OK;
     Workspace *ws = ws_of(c);
+    if (local_comm(c)) {
+        // the group's contexts (this process): the fused apply stores the rows
+        // straight into the consumer's ghost block
+        Rendezvous *R = rdv_of(c);
+        std::vector<uint8_t> all;
+        const dd_ctx *me = c;
+        if (!R->allgather(&me, sizeof me, all)) {
+            set_error("DD_COMM_LOCAL: host rendezvous timed out during dd_setup");
+            return DD_E_NCCL;
+        }
+        ws->local_peers.assign(c->world, nullptr);
+        for (int q = 0; q < c->world; ++q) std::memcpy(&ws->local_peers[q], &all[q * sizeof me], sizeof me);
+        dd_status st = DD_OK;
+        for (dd_ctx *q : ws->local_peers)
+            if (q->device != c->device) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, c->device, q->device);
+                if (can && cudaDeviceEnablePeerAccess(q->device, 0) != cudaSuccess) cudaGetLastError();
+                if (!can) ws->halo_fuse = false;  // copies still work without peer access
+            }
+        st = halo_lists_build(
+            c,
+            [&](int q, int64_t p) {
+                dd_ctx *peer = ws->local_peers[q];
+                return ws_of(peer)->xg + c->bs * (peer->recv_off[c->rank] + p);
+            },
+            false);
+        return comm_agree(c, st);
+    }
     if (!peer_comm(c)) {
         // NCCL: the fused apply packs the send buffer
         return halo_lists_build(
@@ -504,7 +538,7 @@ dd_status comm_connect(dd_ctx *c) {
 void comm_end(dd_ctx *c) {
     if (c->world <= 1 || c->host_only) return;
     Workspace *ws = ws_of(c);
-    if (peer_comm(c)) {
+    if (peer_comm(c) || local_comm(c)) {
         // no peer may still be storing into this rank's mailbox (a FREE count
         // or the last halo rows): every rank is idle before the memory goes
         if (Rendezvous *R = rdv_of(c)) R->barrier();
@@ -518,10 +552,79 @@ void comm_end(dd_ctx *c) {
     c->rdv = nullptr;
 }
 
+// ---- DD_COMM_LOCAL: every exchange records a "ready" event after the
+// outgoing data, meets the group at a host rendezvous, makes its stream wait
+// on the producers' events and copies device-to-device, records "done",
+// meets again, and waits on its consumers' "done" before the outgoing buffer
+// can be overwritten. Every wait names an event recorded before the
+// rendezvous, so all GPU work of all ranks is enqueued before anything waits
+// on it: no kernel ever waits on another rank (a spinning kernel would
+// deadlock ranks that share a GPU with a host call that waits for the device,
+// e.g. a cudaMalloc of the test's own tensors).
+#define LOCAL_MEET(c)                                                                          \
+    do {                                                                                       \
+        if (!rdv_of(c)->barrier()) {                                                           \
+            set_error("DD_COMM_LOCAL rendezvous timed out (a rank stopped calling)");          \
+            return DD_E_NCCL;                                                                  \
+        }                                                                                      \
+    } while (0)
+
+static dd_status local_allgather(dd_ctx *c, int nv, cudaStream_t st) {
+    Workspace *ws = ws_of(c);
+    const size_t bytes = 2 * (size_t)nv * sizeof(double);
+    CK(cudaEventRecord(ws->xev_ready, st));
+    LOCAL_MEET(c);
+    for (int q = 0; q < c->world; ++q) {
+        Workspace *pw = ws_of(ws->local_peers[q]);
+        if (q != c->rank) CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
+        CK(cudaMemcpyAsync(ws->gathered + 2 * (size_t)nv * q, pw->loc, bytes, cudaMemcpyDefault, st));
+    }
+    CK(cudaEventRecord(ws->xev_done, st));
+    LOCAL_MEET(c);
+    for (int q = 0; q < c->world; ++q)
+        if (q != c->rank) CK(cudaStreamWaitEvent(st, ws_of(ws->local_peers[q])->xev_done, 0));
+    return DD_OK;
+}
+
+static dd_status local_halo(dd_ctx *c, cudaStream_t st) {
+    Workspace *ws = ws_of(c);
+    CK(cudaEventRecord(ws->xev_ready, st));
+    LOCAL_MEET(c);
+    for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) continue;
+        const int64_t ro = c->recv_off[q], rn = c->recv_off[q + 1] - ro;
+        if (!rn) continue;
+        dd_ctx *peer = ws->local_peers[q];
+        Workspace *pw = ws_of(peer);
+        CK(cudaStreamWaitEvent(st, pw->xev_ready, 0));
+        CK(cudaMemcpyAsync(ws->xg + c->bs * ro, pw->sendbuf + c->bs * pw->send_off[c->rank], c->bs * rn * sizeof(double),
+                           cudaMemcpyDefault, st));
+    }
+    CK(cudaEventRecord(ws->xev_done, st));
+    LOCAL_MEET(c);
+    for (int q = 0; q < c->world; ++q)
+        if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
+            CK(cudaStreamWaitEvent(st, ws_of(ws->local_peers[q])->xev_done, 0));
+    return DD_OK;
+}
+
 dd_status halo(dd_ctx *c, const double *x, cudaStream_t st, bool packed, const int *skip) {
     if (c->world <= 1) return DD_OK;
     Workspace *ws = ws_of(c);
     packed = packed && ws->halo_fuse;
+    if (local_comm(c)) {
+        const int64_t ns = ws->send_off[c->world];
+        if (!packed) {
+            if (ns) ddk::launch_gather3(c, ns, ws->d_send_idx, x, ws->sendbuf, st);
+            return local_halo(c, st);
+        }
+        // every producer has recorded xev_app after its fused apply
+        LOCAL_MEET(c);
+        for (int q = 0; q < c->world; ++q)
+            if (q != c->rank && c->recv_off[q + 1] > c->recv_off[q])
+                CK(cudaStreamWaitEvent(st, ws_of(ws->local_peers[q])->xev_app, 0));
+        return DD_OK;
+    }
     if (peer_comm(c)) {
         if (!packed) {
             ddk::launch_peer_wait(ws->pd, ddk::PCH_FREE, ws->d_send_to, ws->n_send_to, 1, skip, st);
@@ -548,6 +651,9 @@ dd_status halo(dd_ctx *c, const double *x, cudaStream_t st, bool packed, const i
 }
 
 dd_status halo_consumed(dd_ctx *c, cudaStream_t st, const int *skip) {
+    // DD_COMM_LOCAL with the fused halo: peers' next fused applies write this
+    // rank's ghost block only after this SpMV has read it
+    if (local_comm(c) && ws_of(c)->halo_fuse) CK(cudaEventRecord(ws_of(c)->xev_free, st));
     if (!peer_comm(c)) return DD_OK;
     Workspace *ws = ws_of(c);
     ddk::launch_peer_signal(ws->pd, ddk::PCH_FREE, ws->d_recv_from, ws->n_recv_from, skip, st);
@@ -559,6 +665,13 @@ dd_status apply_halo(dd_ctx *c, const double *r, double *z, cudaStream_t st, con
     Workspace *ws = ws_of(c);
     const bool fuse = c->world > 1 && ws->halo_fuse;
     const bool peer = fuse && peer_comm(c);
+    const bool local = fuse && local_comm(c);
+    if (local) {
+        LOCAL_MEET(c);
+        for (int q = 0; q < c->world; ++q)
+            if (q != c->rank && ws->send_off[q + 1] > ws->send_off[q])
+                CK(cudaStreamWaitEvent(st, ws_of(ws->local_peers[q])->xev_free, 0));
+    }
     // peer transports: the epilogue stores into the consumers' ghost blocks,
     // so every consumer must have read the previous rows first
     if (peer) {
@@ -571,6 +684,7 @@ dd_status apply_halo(dd_ctx *c, const double *r, double *z, cudaStream_t st, con
         ddk::launch_peer_signal(ws->pd, ddk::PCH_HALO, ws->d_send_to, ws->n_send_to, skip, st);
         ++c->n_launches;
     }
+    if (local) CK(cudaEventRecord(ws->xev_app, st));
     return DD_OK;
 }
 
@@ -579,6 +693,9 @@ dd_status reduce_across(dd_ctx *c, int nv, int op, const ddk::RedArgs &ra, cudaS
     Workspace *ws = ws_of(c);
     if (peer_comm(c)) {
         ddk::launch_peer_allgather_finalize(ws->pd, nv, ws->loc, ra, op, st);
+    } else if (local_comm(c)) {
+        TRY(local_allgather(c, nv, st));
+        ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ra, op, st);
     } else {
         NK(ncclAllGather(ws->loc, ws->gathered, 2 * nv, ncclDouble, nccl_of(c), st));
         ddk::launch_finalize_gathered(c->world, nv, ws->gathered, ra, op, st);
@@ -608,8 +725,8 @@ dd_status comm_wait_event(dd_ctx *c, cudaEvent_t ev) {
     }
 }
 
-dd_status comm_check(dd_ctx *c) {
-    if (c->world <= 1) return DD_OK;
+dd_status comm_check(dd_ctx *c, cudaStream_t st) {
+    if (c->world <= 1 || local_comm(c)) return DD_OK;
     if (c->comm == DD_COMM_NCCL) {
         if (!c->nccl) {
             set_error("NCCL communicator was aborted after an asynchronous error");
@@ -624,7 +741,8 @@ dd_status comm_check(dd_ctx *c) {
         return DD_OK;
     }
     int err = 0;
-    CK(cudaMemcpy(&err, ws_of(c)->perr, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(&err, ws_of(c)->perr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     if (err) {
         set_error("peer transport: a device-side wait saw no progress for DD_PEER_TIMEOUT_S seconds "
                   "(a rank stopped calling, or its memory is unreachable)");

@@ -173,7 +173,7 @@ struct dd_ctx {
     int32_t variants = 0;
     int32_t solver_variant = DD_LEVELSET;  // apply variant inside dd_bicgstab (timed at setup)
     double variant_ms[3] = {0, 0, 0};      // level set, sync-free, direct
-    ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct, cfg_ec, cfg_nu;
+    ddi::LaunchCfg cfg_lvl, cfg_spin, cfg_direct, cfg_ec, cfg_nu, cfg_tree;
     // spmv
     ddi::SpmvDev spmv;
     int64_t spmv_bytes = 0;

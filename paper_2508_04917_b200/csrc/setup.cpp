@@ -281,8 +281,9 @@ int64_t bank_cost(const dd_ctx *ctx, int64_t la, int64_t P, int rmax, const Swz 
 }  // namespace
 
 // Pick the slot swizzle with the fewest modelled wavefronts on (up to 3)
-// sample subdomains, among those that add at most 32 slots (768 B: the
-// shared-memory budget keeps its CTAs per SM). 3x3 rows only; DD_SWZ=0 keeps
+// sample subdomains, among those that add at most 16 slots (384 B: at P 2048
+// the level-set and sync-free kernels keep two CTAs per SM; 32 slots cost the
+// sync-free variant its second CTA, measured 0.54 -> 0.89 ms). 3x3 rows only; DD_SWZ=0 keeps
 // the identity. Sets ctx->swz and ctx->vec_rows.
 void choose_swizzle(dd_ctx *ctx, int64_t r0) {
     ctx->swz = Swz{};
@@ -297,7 +298,7 @@ void choose_swizzle(dd_ctx *ctx, int64_t r0) {
                 for (uint32_t p2 : {0u, 1u, 2u, 3u, 5u}) {
                     if ((s2 == 31) != (p2 == 0) || (s2 != 31 && s2 <= s1)) continue;
                     const Swz c{s1, p1, s2, p2};
-                    if (c.slot((uint32_t)ctx->max_P - 1) + 1 - (uint32_t)ctx->max_P <= 32) cands.push_back(c);
+                    if (c.slot((uint32_t)ctx->max_P - 1) + 1 - (uint32_t)ctx->max_P <= 16) cands.push_back(c);
                 }
     std::vector<int64_t> cost(cands.size(), 0);
     const int rmax = ctx->bs == 1 ? 256 : 128;

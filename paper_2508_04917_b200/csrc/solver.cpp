@@ -18,6 +18,11 @@ using namespace ddi;
 
 namespace {
 
+// device residual history held from dd_setup: solves of up to this many
+// iterations take the captured graph (longer ones the batched loop, with a
+// stream-ordered reallocation)
+constexpr int kHistIters = 10000;
+
 // Optional per-kernel timing inside dd_bicgstab (dd_profile): CUDA events on
 // the solver's stream around every apply / SpMV / BLAS-1 launch, harvested at
 // the solver's own synchronisation points (no extra host syncs).
@@ -129,61 +134,49 @@ dd_status enqueue_iteration(dd_ctx *c, ddk::RedArgs ra, int k, double *x, cudaSt
     return DD_OK;
 }
 
-// CUDA-graph solve loop: the iteration body captured once per
-// solution vector under a conditional WHILE node, so a whole solve is one
-// graph launch -- no host round trip per iteration or batch. Used for
-// world == 1 and for the peer transports (whose exchanges are kernels) when
-// per-kernel profiling is off (DD_GRAPH=0 disables it).
-dd_status graph_solve(dd_ctx *c, const ddk::RedArgs &ra, double *x, int32_t max_iter, cudaStream_t st,
-                      int64_t *launches_per_iter) {
+// CUDA-graph solve loop: the iteration body captured ONCE at
+// dd_setup under a conditional WHILE node, for the workspace solution vector
+// ws->xd and the device history ws->d_hist, so a whole solve is one graph
+// launch and dd_bicgstab neither captures, instantiates nor allocates (with
+// the peer transports a rank may already be spinning on this one's signals;
+// a host call that waits for the device -- cudaFree, say -- would then
+// deadlock ranks that share a GPU). Used for world == 1 and the peer
+// transports when per-kernel profiling is off (DD_GRAPH=0 disables it).
+dd_status graph_capture(dd_ctx *c) {
     Workspace *ws = ws_of(c);
-    if (!ws->gexec || ws->gx != x || ws->ghist != ws->d_hist) {
-        if (ws->gexec) cudaGraphExecDestroy(ws->gexec);
-        if (ws->graph) cudaGraphDestroy(ws->graph);
-        ws->gexec = nullptr;
-        ws->graph = nullptr;
-        if (!ws->cap) CK(cudaStreamCreateWithFlags(&ws->cap, cudaStreamNonBlocking));
-        CK(cudaGraphCreate(&ws->graph, 0));
-        cudaGraphConditionalHandle h;
-        CK(cudaGraphConditionalHandleCreate(&h, ws->graph, 1, cudaGraphCondAssignDefault));
-        cudaGraphNodeParams p = {};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = h;
-        p.conditional.type = cudaGraphCondTypeWhile;
-        p.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, ws->graph, nullptr, 0, &p));
-        cudaGraph_t body = p.conditional.phGraph_out[0];
-        const int64_t n0 = c->n_launches;
-        CK(cudaStreamBeginCaptureToGraph(ws->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        ddk::launch_iter_head(ws->ctl, ws->cap);
-        dd_status e = enqueue_iteration(c, ra, -1, x, ws->cap);
-        ddk::launch_iter_tail(ws->ctl, h, ws->cap);
-        cudaGraph_t out = nullptr;
-        const cudaError_t ce = cudaStreamEndCapture(ws->cap, &out);
-        if (e != DD_OK) return e;
-        if (ce != cudaSuccess) {
-            set_error(std::string("dd_bicgstab: graph capture failed: ") + cudaGetErrorString(ce));
-            return DD_E_CUDA;
-        }
-        ws->g_launches = c->n_launches - n0;
-        c->n_launches = n0;
-        CK(cudaGraphInstantiate(&ws->gexec, ws->graph, 0));
-        ws->gx = x;
-        ws->ghist = ws->d_hist;
+    if (!ws->cap) CK(cudaStreamCreateWithFlags(&ws->cap, cudaStreamNonBlocking));
+    CK(cudaGraphCreate(&ws->graph, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, ws->graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, ws->graph, nullptr, 0, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    ddk::RedArgs ra = red_args(c);
+    ra.ctl = ws->ctl;
+    ra.hist = ws->d_hist;
+    ra.k = -1;
+    const int64_t n0 = c->n_launches;
+    CK(cudaStreamBeginCaptureToGraph(ws->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    ddk::launch_iter_head(ws->ctl, ws->cap);
+    dd_status e = enqueue_iteration(c, ra, -1, ws->xd, ws->cap);
+    ddk::launch_iter_tail(ws->ctl, h, ws->cap);
+    cudaGraph_t out = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ws->cap, &out);
+    if (e != DD_OK) return e;
+    if (ce != cudaSuccess) {
+        set_error(std::string("dd_setup: graph capture failed: ") + cudaGetErrorString(ce));
+        return DD_E_CUDA;
     }
-    *ws->h_max = max_iter;
-    CK(cudaMemcpyAsync(ws->ctl + ddk::C_MAX, ws->h_max, sizeof(int), cudaMemcpyHostToDevice, st));
-    CK(cudaGraphLaunch(ws->gexec, st));
-    *launches_per_iter = ws->g_launches;
-    return DD_OK;
-}
-
-dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
-    Workspace *ws = ws_of(c);
-    CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(ws->ev[0], st));
-    TRY(comm_wait_event(c, ws->ev[0]));
+    ws->g_launches = c->n_launches - n0;
+    c->n_launches = n0;
+    CK(cudaGraphInstantiate(&ws->gexec, ws->graph, 0));
+    ws->gx = ws->xd;
+    ws->ghist = ws->d_hist;
     return DD_OK;
 }
 
@@ -196,7 +189,28 @@ void prof_free(dd_ctx *c) {
     delete reinterpret_cast<Prof *>(c->prof);
     c->prof = nullptr;
 }
+
+dd_status solver_prepare(dd_ctx *c) {
+    Workspace *ws = ws_of(c);
+    ws->hist_cap = 2 * (int64_t)kHistIters + 1;
+    TRY(dmalloc(&ws->d_hist, (size_t)ws->hist_cap));
+    static const bool graphs_env = !getenv("DD_GRAPH") || atoi(getenv("DD_GRAPH")) != 0;
+    if (graphs_env && comm_graph_ok(c) && c->n_local > 0) TRY(graph_capture(c));
+    return DD_OK;
+}
 }  // namespace ddi
+
+namespace {
+
+dd_status read_scalars(dd_ctx *c, cudaStream_t st) {
+    Workspace *ws = ws_of(c);
+    CK(cudaMemcpyAsync(ws->h_sc, ws->sc, ddk::S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ws->ev[0], st));
+    TRY(comm_wait_event(c, ws->ev[0]));
+    return DD_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -217,11 +231,22 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     Workspace *ws = ws_of(c);
     const int64_t m = ws->m;
     if (ws->hist_cap < 2 * (int64_t)max_iter + 1) {
-        cudaFree(ws->d_hist);
+        // stream-ordered (no device-wide synchronisation, see graph_capture)
+        CK(cudaFreeAsync(ws->d_hist, st));
         ws->d_hist = nullptr;
         ws->hist_cap = 0;
-        TRY(dmalloc(&ws->d_hist, 2 * (size_t)max_iter + 1));
+        CK(cudaMallocAsync(reinterpret_cast<void **>(&ws->d_hist), sizeof(double) * (2 * (size_t)max_iter + 1), st));
         ws->hist_cap = 2 * (int64_t)max_iter + 1;
+    }
+    static const bool graphs_env = !getenv("DD_GRAPH") || atoi(getenv("DD_GRAPH")) != 0;
+    const bool use_graph = graphs_env && ws->gexec && ws->ghist == ws->d_hist &&
+                           !(c->prof && reinterpret_cast<Prof *>(c->prof)->on);
+    // the graph runs on ws->xd: the caller's x goes in and out by D2D copies
+    // (2 x 24 n bytes, ~0.03 ms at 160^3)
+    double *const x_user = x;
+    if (use_graph && x != ws->xd) {
+        CK(cudaMemcpyAsync(ws->xd, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+        x = ws->xd;
     }
     CK(cudaMemsetAsync(ws->ctl, 0, 8 * sizeof(int), st));
     *ws->h_tol = tol;
@@ -244,10 +269,12 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     // ranks stop together.
     constexpr int BATCH = 2;
     int k_enq = 0, j = 0;
-    static const bool graphs_env = !getenv("DD_GRAPH") || atoi(getenv("DD_GRAPH")) != 0;
-    const bool use_graph = graphs_env && comm_graph_ok(c) && !(c->prof && reinterpret_cast<Prof *>(c->prof)->on);
-    int64_t g_per_iter = 0;
-    if (use_graph) TRY(graph_solve(c, ra, x, max_iter, st, &g_per_iter));
+    const int64_t g_per_iter = ws->g_launches;
+    if (use_graph) {
+        *ws->h_max = max_iter;
+        CK(cudaMemcpyAsync(ws->ctl + ddk::C_MAX, ws->h_max, sizeof(int), cudaMemcpyHostToDevice, st));
+        CK(cudaGraphLaunch(ws->gexec, st));
+    }
     for (bool stop = use_graph; !stop; ++j) {
         for (int q = 0; q < BATCH && k_enq < max_iter; ++q) {
             const int k = ++k_enq;
@@ -266,11 +293,12 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     CK(cudaMemcpyAsync(ws->h_ctl, ws->ctl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ws->ev[0], st));
     TRY(comm_wait_event(c, ws->ev[0]));
-    TRY(comm_check(c));
+    TRY(comm_check(c, st));
     const int state = ws->h_ctl[ddk::C_STATE], kf = ws->h_ctl[ddk::C_K], nh = ws->h_ctl[ddk::C_NH];
     if (use_graph) c->n_launches += g_per_iter * std::max(1, ws->h_ctl[ddk::C_ITER]) + 2 * std::max(1, ws->h_ctl[ddk::C_ITER]);
     std::vector<double> hv(std::max(1, nh));
-    CK(cudaMemcpy(hv.data(), ws->d_hist, sizeof(double) * std::max(1, nh), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(hv.data(), ws->d_hist, sizeof(double) * std::max(1, nh), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     if (hist) std::memcpy(hist, hv.data(), sizeof(double) * nh);
     double iters = 0.0;
     int64_t napp = 0;
@@ -298,8 +326,9 @@ dd_status dd_bicgstab(dd_ctx *c, const double *b, double *x, double tol, int32_t
     TRY(spmv_mode(c, ddk::SPMV_PLAIN, x, ws->t, nullptr, ra_plain, st));
     ddk::launch_resid(c, m, b, ws->t, ra_plain, st);
     TRY(reduce_across(c, 2, ddk::FIN_RESID, ra_plain, st));
+    if (x != x_user) CK(cudaMemcpyAsync(x_user, x, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
     TRY(read_scalars(c, st));
-    TRY(comm_check(c));
+    TRY(comm_check(c, st));
     CK(cudaGetLastError());
     const double *sc = ws->h_sc;
     if (rep) {

@@ -6,6 +6,8 @@ each against the oracle on the same seeded inputs:
 * DD_LOWER (the lower sweep alone, Table 3) for every deterministic variant
   vs oracle.lower -- bitwise;
 * DD_DIRECT_GLOBAL (vertex-centric, vector in global memory) -- bitwise;
+* DD_TREE (4 lanes per row, fixed warp-shuffle tree of the partial sums,
+  P:409): deterministic, a different summation order -> 1e-10 bar;
 * DD_EDGE (dag_ec_ILDU0_fused: edge-centric atomics, shared-memory vector)
   and DD_EDGE_GLOBAL (dag_ec_no_lds): atomics in an unfixed order, so
   max relative error <= 1e-10 (north-star bar) instead of bitwise (R19), and
@@ -80,7 +82,7 @@ def test_direct_global_bitwise(name):
     assert np.array_equal(run(ctx, r, dd.DD_DIRECT_GLOBAL), oracle.apply(S, r))
 
 
-@pytest.mark.parametrize("variant", [dd.DD_EDGE, dd.DD_EDGE_GLOBAL], ids=["edge", "edge_global"])
+@pytest.mark.parametrize("variant", [dd.DD_EDGE, dd.DD_EDGE_GLOBAL, dd.DD_TREE], ids=["edge", "edge_global", "tree"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_edge_centric_within_bar(name, variant):
     _, _, _, S, ctx = get(name)
@@ -94,7 +96,7 @@ def test_edge_centric_within_bar(name, variant):
     assert np.abs(zl - zl_ref).max() <= 1e-10 * np.abs(zl_ref).max()
 
 
-@pytest.mark.parametrize("solver", ["edge", "edge_global", "ilu0", "direct_global"])
+@pytest.mark.parametrize("solver", ["edge", "edge_global", "ilu0", "direct_global", "tree"])
 @pytest.mark.parametrize("name", ["cfg1_16^3", "random_blocks", "chunks_ragged_oddP"])
 def test_ablation_solver_iterations(name, solver, monkeypatch):
     import torch

@@ -43,7 +43,7 @@ def timeit(fn, reps):
         if i >= 3: ts.append(e0.elapsed_time(e1))
     return float(np.median(ts)), float(np.min(ts))
 VARS = [(1, "levelset"), (2, "spin"), (4, "direct"), (8, "unfused"), (16, "edge"), (32, "edge_global"),
-        (128, "direct_glob"), (64, "ilu0")]
+        (128, "direct_glob"), (64, "ilu0"), (512, "tree")]
 if os.environ.get("PROBE_LOWER", "1") == "1":  # Table 3 analogue: the lower sweep alone
     VARS += [(v | dd.DD_LOWER, n + "+L") for v, n in VARS]
 for var, name in VARS:
