@@ -268,6 +268,9 @@ dd_status dd_unpermute(dd_ctx *ctx, const double *v_reord_dev, double *v_orig_ho
  * dd_setup computed on the host (dd_refactor updates only device state). */
 dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original order*/,
                            int32_t *new_to_old /*[N]*/);
+/* The Alg. 2 grid and tile dims the partition used (the chosen ones when
+ * dd_setup picked them; all zeros for a chunk or BFS partition). */
+dd_status dd_get_grid(const dd_ctx *ctx, dd_grid *out);
 /* which: 0 = L (hmapL), 1 = U (hmapU); local rows, reordered order. */
 dd_status dd_get_levels(const dd_ctx *ctx, int32_t which, int32_t *hmap);
 
@@ -329,9 +332,14 @@ dd_status dd_solver_variant(const dd_ctx *ctx, int32_t *variant, double *ms);
  * paper's P:1041) whose vector fits, pick the one whose subdomain count fills
  * whole waves of the apply kernel's CTA slots on `device` (SMs x resident
  * CTAs, from the CUDA occupancy API; device < 0: an analytic model), then P
- * nearest the target, then the most compact tile. Writes g->tx/ty/tz.
- * dd_setup calls it when opts.grid has tx = ty = tz = 0 (P_target =
- * opts.subdomain_rows). DD_E_GRID_NOT_DIVISIBLE if no tile shape qualifies. */
+ * nearest the target, then the most compact tile -- precisely: maximise
+ * fill x bw x (1 - 3 x dropped) with fill = the wave fill, bw = 0.82 for one
+ * resident CTA per SM (latency-bound), 1 otherwise, dropped = the share of
+ * the grid couplings that cross tile faces (uniform weights here). Writes
+ * g->tx/ty/tz. dd_setup makes the same choice when opts.grid has
+ * tx = ty = tz = 0 (P_target = opts.subdomain_rows), weighting each grid
+ * plane by the Frobenius norms of the matrix blocks that cross it.
+ * DD_E_GRID_NOT_DIVISIBLE if no tile shape qualifies. */
 dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_target);
 
 /* 128-byte ncclUniqueId for world > 1 (rank 0 calls it; the caller

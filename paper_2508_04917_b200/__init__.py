@@ -36,7 +36,7 @@ STATUS = ["DD_OK", "DD_E_INVALID_ARG", "DD_E_NOT_SQUARE", "DD_E_UNSORTED_OR_DUP"
 EXPORTS = ["dd_setup", "dd_setup_csr", "dd_destroy", "dd_local_range", "dd_apply", "dd_apply_variant", "dd_spmv",
            "dd_bicgstab", "dd_solve_host", "dd_permute", "dd_unpermute", "dd_get_partition",
            "dd_get_levels", "dd_levels_device", "dd_get_factors", "dd_get_halo", "dd_get_send_rows", "dd_stats", "dd_launch_info",
-           "dd_solver_variant", "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_choose_tiles", "dd_last_error"]
+           "dd_solver_variant", "dd_profile", "dd_refactor", "dd_nccl_unique_id", "dd_choose_tiles", "dd_get_grid", "dd_last_error"]
 
 
 class DDError(RuntimeError):
@@ -90,7 +90,7 @@ def lib():
             "dd_permute": [P, P, P, P], "dd_unpermute": [P, P, P, P], "dd_get_partition": [P, P, P],
             "dd_get_levels": [P, i32, P], "dd_levels_device": [P, P, P, P], "dd_get_factors": [P] * 10, "dd_get_halo": [P, P, P, P], "dd_get_send_rows": [P, i32, P, P],
             "dd_stats": [P, P, P], "dd_profile": [P, i32, P], "dd_refactor": [P, P, i32, P], "dd_launch_info": [P, i32, P], "dd_solver_variant": [P, P, P], "dd_nccl_unique_id": [P],
-            "dd_choose_tiles": [P, i32, i32, i32],
+            "dd_choose_tiles": [P, i32, i32, i32], "dd_get_grid": [P, P],
             "dd_last_error": [],
         }
         for name, args in sig.items():
@@ -342,8 +342,9 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     A = BSR3(n, col_idx.shape[0], _ptr(row_ptr), _ptr(col_idx), _ptr(vals))
     o = Opts()
     g = None
-    if isinstance(tiles, str) and tiles == "auto":  # wave-filling subdomain size (dd_choose_tiles)
-        tiles = dd_choose_tiles(grid, -1 if host_only else device, 1 if csr else 3, int(P or 2048))
+    if isinstance(tiles, str) and tiles == "auto":
+        # dd_setup chooses the tiles (wave fill x coupling weight the drop removes, R41)
+        tiles = (0, 0, 0)
     if tiles is not None:
         g = Grid(*grid, *tiles)
         o.grid = C.addressof(g)
@@ -361,7 +362,9 @@ def dd_setup(row_ptr, col_idx, vals, *, grid=None, tiles=None, P=None, variants=
     h = C.c_void_p()
     _check((lib().dd_setup_csr if csr else lib().dd_setup)(C.byref(A), C.byref(o), C.byref(h)))
     ctx = Context(h, n, keep=(g, idbuf), bs=1 if csr else 3, nnzb=int(col_idx.shape[0]))
-    ctx.tiles = tuple(tiles) if tiles is not None else None
+    gq = Grid()
+    _check(lib().dd_get_grid(h, C.byref(gq)))
+    ctx.tiles = (gq.tx, gq.ty, gq.tz) if tiles is not None else None
     return ctx
 
 

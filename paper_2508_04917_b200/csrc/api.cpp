@@ -319,13 +319,27 @@ dd_status dd_setup_csr(const dd_csr *A, const dd_opts *o, dd_ctx **out) {
     return setup_common(&B, o, out, 1);
 }
 
-dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_target) {
-    if (!g || g->nx <= 0 || g->ny <= 0 || g->nz <= 0 || (bs != 1 && bs != 3)) {
-        set_error("dd_choose_tiles: bad grid or block size");
-        return DD_E_INVALID_ARG;
-    }
+// Tile choice (R41). For every admissible tile shape: the wave fill of the
+// apply kernel's CTA slots, a bandwidth factor for one resident CTA per SM
+// (latency-bound: 0.82 of two per SM at 160^3), and the share
+// of the coupling weight the drop removes (a convergence proxy: the faces
+// between tiles; wx/wy/wz = coupling weight across each grid plane, uniform
+// without a matrix). score = fill * bw * (1 - 3 * dropped_share); ties: P
+// nearest the target, then the most compact tile.
+static dd_status choose_tiles_impl(dd_grid *g, int32_t device, int32_t bs, int32_t P_target,
+                                   const std::vector<double> &wx, const std::vector<double> &wy,
+                                   const std::vector<double> &wz) {
     if (P_target <= 0) P_target = 2048;  // the paper's subdomain size
     const int64_t N = (int64_t)g->nx * g->ny * g->nz;
+    double wtot = 0;
+    for (auto *w : {&wx, &wy, &wz})
+        for (double v : *w) wtot += v;
+    auto cut = [](const std::vector<double> &w, int t) {
+        double s = 0;
+        for (size_t i = 0; i + 1 < w.size(); ++i)
+            if ((i + 1) % t == 0) s += w[i];
+        return s;
+    };
     std::map<int, int> slots_of;
     double best_key[3] = {-1, 0, 0};
     int bt[3] = {0, 0, 0};
@@ -338,14 +352,23 @@ dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_targ
                 const int64_t P = (int64_t)tx * ty * tz;
                 if (2 * P < P_target || P > 2 * (int64_t)P_target || 8 * bs * P > 232448 - 16384) continue;
                 auto it = slots_of.find((int)P);
-                const int slots = it != slots_of.end() ? it->second : (slots_of[(int)P] = tile_slots(device, bs, (int)P));
+                int per_sm = 0;
+                if (it == slots_of.end()) {
+                    const int sl = tile_slots(device, bs, (int)P, &per_sm);
+                    slots_of[(int)P] = sl;
+                    slots_of[-(int)P] = per_sm;
+                    it = slots_of.find((int)P);
+                }
+                const int slots = it->second;
+                per_sm = slots_of[-(int)P];
                 if (slots <= 0) continue;
                 const int64_t n_sub = N / P;
                 const int64_t waves = (n_sub + slots - 1) / slots;
-                const double eff = (double)n_sub / (double)(waves * slots);
-                // whole waves first (2 % buckets), then P near the target, then
-                // compact tiles (fewer couplings dropped per row)
-                const double key[3] = {std::floor(eff * 50.0) / 50.0, -std::fabs(std::log((double)P / P_target)),
+                const double fill = (double)n_sub / (double)(waves * slots);
+                const double drop = wtot > 0 ? (cut(wx, tx) + cut(wy, ty) + cut(wz, tz)) / wtot : 0.0;
+                const double bw = per_sm <= 1 ? 0.82 : 1.0;
+                const double score = fill * bw * (1.0 - 3.0 * drop);
+                const double key[3] = {std::floor(score * 200.0) / 200.0, -std::fabs(std::log((double)P / P_target)),
                                        -(1.0 / tx + 1.0 / ty + 1.0 / tz)};
                 if (std::lexicographical_compare(best_key, best_key + 3, key, key + 3)) {
                     std::copy(key, key + 3, best_key);
@@ -360,6 +383,40 @@ dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_targ
     }
     g->tx = bt[0], g->ty = bt[1], g->tz = bt[2];
     return DD_OK;
+}
+
+dd_status dd_choose_tiles(dd_grid *g, int32_t device, int32_t bs, int32_t P_target) {
+    if (!g || g->nx <= 0 || g->ny <= 0 || g->nz <= 0 || (bs != 1 && bs != 3)) {
+        set_error("dd_choose_tiles: bad grid or block size");
+        return DD_E_INVALID_ARG;
+    }
+    // without a matrix: every grid edge weighs the same (a 7-point stencil)
+    // (plane i couples i and i + 1: the last plane of each axis has none)
+    std::vector<double> wx(g->nx, (double)g->ny * g->nz), wy(g->ny, (double)g->nx * g->nz),
+        wz(g->nz, (double)g->nx * g->ny);
+    wx.back() = wy.back() = wz.back() = 0.0;
+    return choose_tiles_impl(g, device, bs, P_target, wx, wy, wz);
+}
+
+// coupling weight (Frobenius norm of the off-diagonal blocks) across every
+// grid plane, for a matrix in the grid's natural order (dd_setup, tiles 0)
+static void plane_weights(const dd_bsr3 *A, const dd_grid &g, int bs, std::vector<double> &wx,
+                          std::vector<double> &wy, std::vector<double> &wz) {
+    wx.assign(g.nx, 0.0), wy.assign(g.ny, 0.0), wz.assign(g.nz, 0.0);
+    const int64_t sx = 1, sy = g.nx, sz = (int64_t)g.nx * g.ny;
+    const int b2 = bs * bs;
+    for (int64_t r = 0; r < A->n_block_rows; ++r)
+        for (int64_t p = A->row_ptr[r]; p < A->row_ptr[r + 1]; ++p) {
+            const int64_t c = A->col_idx[p];
+            if (c <= r) continue;  // each coupling once (upper), plus its transpose below
+            double w = 0;
+            for (int v = 0; v < b2; ++v) w += A->vals[b2 * p + v] * A->vals[b2 * p + v];
+            w = std::sqrt(w);
+            const int64_t d = c - r;
+            if (d == sx && (r % g.nx) + 1 < g.nx) wx[r % g.nx] += 2 * w;
+            else if (d == sy) wy[(r / g.nx) % g.ny] += 2 * w;
+            else if (d == sz) wz[r / sz] += 2 * w;
+        }
 }
 
 static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **out, int bs) {
@@ -377,7 +434,14 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **ou
     dd_grid g_auto;
     if (o_in->grid && o_in->grid->tx == 0 && o_in->grid->ty == 0 && o_in->grid->tz == 0) {
         g_auto = *o_in->grid;
-        TRY(dd_choose_tiles(&g_auto, o_in->host_only ? -1 : o_in->device, bs, o_in->subdomain_rows));
+        if (g_auto.nx <= 0 || g_auto.ny <= 0 || g_auto.nz <= 0 ||
+            (int64_t)g_auto.nx * g_auto.ny * g_auto.nz != A->n_block_rows) {
+            set_error("dd_setup: grid does not match the matrix");
+            return DD_E_INVALID_ARG;
+        }
+        std::vector<double> wx, wy, wz;
+        plane_weights(A, g_auto, bs, wx, wy, wz);
+        TRY(choose_tiles_impl(&g_auto, o_in->host_only ? -1 : o_in->device, bs, o_in->subdomain_rows, wx, wy, wz));
         o_auto.grid = &g_auto;
     }
     const dd_opts *o = &o_auto;
@@ -410,6 +474,7 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **ou
     // can fail on one rank only (a singular pivot in its subdomains, a
     // launch shape that does not fit), so no rank is left waiting in a
     // collective its peers never reach
+    if (o->grid) ctx->grid = *o->grid;
     dd_status st = host_setup(ctx, A, o);
     if (!ctx->host_only) {
         st = comm_begin(ctx, o->nccl_unique_id, st);
@@ -557,6 +622,12 @@ dd_status dd_get_partition(const dd_ctx *c, int32_t *labels, int32_t *new_to_old
     if (!c) return DD_E_INVALID_ARG;
     if (labels) std::memcpy(labels, c->labels.data(), c->N * sizeof(int32_t));
     if (new_to_old) std::memcpy(new_to_old, c->new_to_old.data(), c->N * sizeof(int32_t));
+    return DD_OK;
+}
+
+dd_status dd_get_grid(const dd_ctx *c, dd_grid *out) {
+    if (!c || !out) return DD_E_INVALID_ARG;
+    *out = c->grid;
     return DD_OK;
 }
 

@@ -1159,7 +1159,7 @@ dd_status apply_prepare(dd_ctx *ctx) {
 // occupancy, as apply_prepare picks it); 0 if the vector does not fit. Used
 // by dd_choose_tiles to size subdomains in whole waves. Without a device: an
 // analytic model (228 KB shared memory and 3 CTAs per SM by registers).
-int tile_slots(int device, int bs, int P) {
+int tile_slots(int device, int bs, int P, int *per_sm) {
     using namespace ddk;
     const int vec_bytes = ((8 * bs * P + 127) / 128) * 128;
     cudaDeviceProp prop;
@@ -1182,6 +1182,7 @@ int tile_slots(int device, int bs, int P) {
         best = std::max(best, occ);
     }
     cudaGetLastError();
+    if (per_sm) *per_sm = best;
     return sms * best;
 }
 

@@ -148,6 +148,7 @@ struct dd_ctx {
     int32_t sub_first = 0, sub_last = 0;  // local subdomains [first, last)
     int64_t row_first = 0, n_local = 0;   // reordered global rows
     int32_t max_P = 0;
+    dd_grid grid = {0, 0, 0, 0, 0, 0};  // Alg. 2 grid and tiles used (zeros: chunk / BFS partition)
     ddi::Swz swz;                   // shared-vector slot swizzle (identity for scalar rows)
     int32_t vec_rows = 0;           // slot(max_P - 1) + 1: rows of the shared vector
     int32_t kmax = 0;  // most blocks of a row in one factor triangle (> 3: general-K kernels)
@@ -218,6 +219,7 @@ double now_ms();
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream,
                        const int *skip = nullptr, const HaloOut *halo = nullptr);
 dd_status apply_prepare(dd_ctx *ctx);  // choose launch cfgs, set smem attributes
-int tile_slots(int device, int bs, int P);  // CTA slots of the level-set kernel for P-row subdomains
+// CTA slots (SMs x resident CTAs) of the level-set kernel for P-row subdomains
+int tile_slots(int device, int bs, int P, int *per_sm = nullptr);
 void spmv_launch(const dd_ctx *ctx, const double *x, double *y, void *stream);
 }  // namespace ddi

@@ -164,42 +164,50 @@ def test_csr_errors_and_refactor_rejected():
 
 def _slots_model(P, bs=3):
     """the analytic occupancy model of tile_slots (no device): 228 KB shared
-    memory per SM, at most 3 CTAs per SM, the ring kernel's smem per CTA"""
+    memory per SM, at most 3 CTAs per SM, the ring kernel's smem per CTA;
+    returns (CTAs per SM, slots)"""
     vec = (8 * bs * P + 127) // 128 * 128
     best = 0
     for rc in (131072, 65536, 32768):
         sm = vec + rc + 16 * 4
         if sm <= 232448:
             best = max(best, min(3, (233472 - 1024) // (sm + 1024)))
-    return 148 * best
+    return best, 148 * best
 
 
 @pytest.mark.parametrize("grid,P", [((160, 160, 160), 2048), ((60, 220, 85), 2048), ((64, 64, 64), 2048),
                                     ((96, 96, 48), 1024)])
-def test_choose_tiles_fills_waves(grid, P):
-    """dd_choose_tiles (host model): the tiles divide the grid, P is inside
-    [P/2, 2P], and no other admissible tile shape fills its waves better
-    (2 % buckets)."""
+def test_choose_tiles_score(grid, P):
+    """dd_choose_tiles (host model, R41): the tiles divide the grid, P is
+    inside [P/2, 2P], and no admissible tile shape scores higher on
+    fill x bw x (1 - 3 dropped) (fill = wave fill of the CTA slots, bw = 0.82
+    for one CTA per SM, dropped = share of the grid's couplings crossing tile
+    faces; 0.5 % buckets)."""
     import math
     tx, ty, tz = dd.dd_choose_tiles(grid, device=-1, P_target=P)
     nx, ny, nz = grid
     assert nx % tx == 0 and ny % ty == 0 and nz % tz == 0
-    Pc = tx * ty * tz
-    assert P / 2 <= Pc <= 2 * P
+    assert P / 2 <= tx * ty * tz <= 2 * P
     N = nx * ny * nz
+    tot = (nx - 1) * ny * nz + nx * (ny - 1) * nz + nx * ny * (nz - 1)
 
-    def eff(p):
-        s = _slots_model(p)
+    def score(a, b, c):
+        p = a * b * c
+        per_sm, s = _slots_model(p)
         n = N // p
-        return math.floor(n / (-(-n // s) * s) * 50) / 50
-    best = max(eff(a * b * c) for a in range(1, nx + 1) if nx % a == 0 for b in range(1, ny + 1) if ny % b == 0
+        fill = n / (-(-n // s) * s)
+        drop = ((nx // a - 1) * ny * nz + (ny // b - 1) * nx * nz + (nz // c - 1) * nx * ny) / tot
+        return math.floor(fill * (0.82 if per_sm <= 1 else 1.0) * (1 - 3 * drop) * 200) / 200
+    best = max(score(a, b, c) for a in range(1, nx + 1) if nx % a == 0 for b in range(1, ny + 1) if ny % b == 0
                for c in range(1, nz + 1) if nz % c == 0 if P / 2 <= a * b * c <= 2 * P)
-    assert eff(Pc) == best
+    assert score(tx, ty, tz) == best
 
 
 def test_setup_auto_tiles_equals_choose_tiles():
     rp, ci, v = laplacian_bsr3(24, 24, 24)
     t = dd.dd_choose_tiles((24, 24, 24), device=-1, P_target=512)
+    # the Laplacian's couplings weigh the same on every plane: the matrix-weighted
+    # choice inside dd_setup equals the geometric one
     ctx = dd.dd_setup(rp, ci, v, grid=(24, 24, 24), tiles="auto", P=512, host_only=True)
     S = oracle.setup(rp, ci, v, grid=(24, 24, 24), tiles=t)
     lab, _ = ctx.partition()

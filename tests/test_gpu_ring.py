@@ -44,10 +44,13 @@ def run_case(P, n_sub=6, seed=41, h=0):
     return ring
 
 
-def test_level0_wider_than_a_record_crosses_chunks():
-    # P 2048: level 0 = 1024 rows = 8 skipped records after a 48 KB r slice
+def test_level0_wider_than_a_record_crosses_chunks(monkeypatch):
+    # P 2048: level 0 = 1024 rows = 8 skipped records after a 48 KB r slice;
+    # a 32 KB ring (8 KB chunks) makes the skipped run cross a chunk boundary
+    monkeypatch.setenv("DD_RING_KB", "32")
     ring = run_case(2048)
-    assert l0_bytes(2048) // (ring // 4) > (24 * 2048) // (ring // 4)  # the skipped run crosses a chunk
+    assert ring == 32768
+    assert l0_bytes(2048) // (ring // 4) > (24 * 2048) // (ring // 4)
 
 
 def candidates(ch):
