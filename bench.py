@@ -187,9 +187,8 @@ def run_reference(args, cfg):
     import numpy as np
     import oracle
     rp, ci, v, b = make_inputs(cfg)
-    if cfg["tiles"] == "auto":  # the host occupancy model of dd_choose_tiles
-        import paper_2508_04917_b200 as dd
-        cfg = dict(cfg, tiles=dd.dd_choose_tiles(cfg["grid"], device=-1))
+    if cfg["tiles"] == "auto":
+        raise SystemExit("--impl reference needs explicit tiles (the oracle does not choose them)")
     oracle.set_threads(0)
     S = oracle.setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"])
     br = b.reshape(-1, 3)[S["new_to_old"]].ravel()
@@ -346,10 +345,11 @@ def run_ours(args, cfg):
     achieved = canon / (apply_ms * 1e-3) / 1e9
     traffic = None
     try:
+        # stored ncu --set full captures, keyed by workload (tools/ncu_summary.py)
         with open(os.path.join(ROOT, "profiles", "ncu_apply_traffic.json")) as f:
-            tr = json.load(f)
+            tr = json.load(f).get(cfg["workload"], {})
         same_kernel = ("k_apply_direct" in tr.get("kernel", "")) == (sv == dd.DD_DIRECT)
-        if tr.get("workload") == cfg["workload"] and tr.get("n_gpus", 1) == world and same_kernel:
+        if tr and tr.get("n_gpus", 1) == world and same_kernel:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass

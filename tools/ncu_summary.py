@@ -56,7 +56,7 @@ def launches(path):
 
 
 def main(rnd, d):
-    lines = [f"# ncu summary, {rnd} (B200, config 3: 160^3 BSR3, P 2048)", "",
+    lines = [f"# ncu summary, {rnd} (B200; config 3: 160^3 BSR3, P 2048 unless named)", "",
              "Captured with `ncu --set full --clock-control none` (one launch each, after warm-up) and a",
              "launch list `ncu --metrics gpu__time_duration.sum --clock-control none` of one bench solve.",
              "ncu launch times are serialised and cold-cache: compare shares, not absolutes.", ""]
@@ -69,8 +69,21 @@ def main(rnd, d):
             lines.append(f"| `{k}` | {n} | {t / 1e3:.2f} | {t / n:.1f} | {100 * t / tot:.1f} % |")
         lines.append("")
     traffic = {}
-    for tag, rep in (("apply (level-set ring)", "prof_apply.ncu-rep"), ("SpMV", "prof_spmv.ncu-rep"),
-                     ("apply (direct ablation)", "prof_direct.ncu-rep")):
+    try:
+        traffic = json.load(open("profiles/ncu_apply_traffic.json"))
+        if "workload" in traffic:  # round-1 single-entry form
+            traffic = {traffic["workload"]: traffic}
+    except Exception:
+        traffic = {}
+    for tag, rep, wl in (("apply (level-set ring)", "prof_apply.ncu-rep", "laplacian_160^3_bsr3_P2048"),
+                         ("SpMV", "prof_spmv.ncu-rep", None),
+                         ("apply (direct ablation)", "prof_direct.ncu-rep", None),
+                         ("apply, config 4 with dd_setup-chosen tiles (6,20,17)", "prof_apply_cfg4auto.ncu-rep",
+                          "spe10style_60x220x85_bsr3_autotiles"),
+                         ("apply, config 4 tiles (10,20,17)", "prof_apply_cfg4.ncu-rep",
+                          "spe10style_60x220x85_bsr3_P3400"),
+                         ("apply (edge-centric ablation, DD_EDGE)", "prof_edge.ncu-rep", None),
+                         ("apply (non-unit ILU0 ablation, DD_ILU0)", "prof_ilu0.ncu-rep", None)):
         p = os.path.join(d, rep)
         if not os.path.exists(p):
             continue
@@ -89,10 +102,10 @@ def main(rnd, d):
         except Exception:
             pass
         lines.append("")
-        if rep == "prof_apply.ncu-rep" and rd is not None:
-            traffic = {"workload": "laplacian_160^3_bsr3_P2048", "n_gpus": 1, "kernel": name,
-                       "dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
-                       "source": f"profiles/{rnd}_ncu_summary.md (ncu --set full, one launch)"}
+        if wl and rd is not None:
+            traffic[wl] = {"workload": wl, "n_gpus": 1, "kernel": name,
+                           "dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
+                           "source": f"profiles/{rnd}_ncu_summary.md (ncu --set full, one launch)"}
     os.makedirs("profiles", exist_ok=True)
     open(f"profiles/{rnd}_ncu_summary.md", "w").write("\n".join(lines) + "\n")
     if traffic:
