@@ -202,6 +202,7 @@ struct dd_ctx {
     std::vector<int64_t> Uptr;           // per W position: update range
     std::vector<int32_t> UpdQ, UpdT;     // (U_kj position, target position)
     std::vector<int32_t> LevRows, LevPtr, SubLev;
+    std::vector<int32_t> URows, SubU;    // rows in U-record order per subdomain (refactor's Dinv / U_unit pass)
     std::vector<int64_t> SlabLoff, SlabUoff, SlabDoff;  // byte offsets into the slab
     std::vector<int32_t> SlabLst, SlabUst, SlabDst;     // plane strides (bytes)
     void *rf = nullptr;                  // device-side refactor state (api.cpp)

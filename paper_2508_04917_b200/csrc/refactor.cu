@@ -113,15 +113,26 @@ __global__ void __launch_bounds__(128) k_refactor(RfArgs a) {
             }
 #pragma unroll
             for (int v = 0; v < 9; ++v) a.Dinv[9 * li + v] = inv[v];
-            rf_scatter(a.slab, a.Doff[li], a.Dst[li], inv);
-            for (int64_t p = d + 1; p < w1; ++p) {
-                double Uu[9];
-                rf_mul3(inv, a.W + 9 * p, Uu);  // U_unit_ij = Dinv_i * U_ij
-                const int64_t b = a.Urp[li] + (p - d - 1);
-                rf_scatter(a.slab, a.Uoff[b], a.Ust[b], Uu);
-            }
+            (void)w1;
         }
         __syncthreads();
+    }
+    // Dinv and U_unit_ij = Dinv_i U_ij of every row, in the order of the U
+    // records (consecutive threads -> consecutive plane elements): no
+    // dependencies between rows here, only on this row's final W and Dinv
+    for (int idx = a.SubU[q] + threadIdx.x; idx < a.SubU[q + 1]; idx += blockDim.x) {
+        const int64_t li = a.URows[idx];
+        const int64_t d = a.Wdiag[li], w1 = a.Wrp[li + 1];
+        double inv[9];
+#pragma unroll
+        for (int v = 0; v < 9; ++v) inv[v] = a.Dinv[9 * li + v];
+        rf_scatter(a.slab, a.Doff[li], a.Dst[li], inv);
+        for (int64_t p = d + 1; p < w1; ++p) {
+            double Uu[9];
+            rf_mul3(inv, a.W + 9 * p, Uu);  // U_unit_ij = Dinv_i * U_ij
+            const int64_t b = a.Urp[li] + (p - d - 1);
+            rf_scatter(a.slab, a.Uoff[b], a.Ust[b], Uu);
+        }
     }
 }
 

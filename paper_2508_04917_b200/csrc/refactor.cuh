@@ -8,6 +8,7 @@ namespace ddk {
 
 struct RfArgs {
     const int32_t *SubLev, *LevPtr, *LevRows;
+    const int32_t *SubU, *URows;  // rows in U-record order per subdomain
     const int64_t *Wrp, *Wdiag, *Uptr, *Lrp, *Urp;
     const int32_t *Wcol, *UpdQ, *UpdT;
     double *W, *Dinv;

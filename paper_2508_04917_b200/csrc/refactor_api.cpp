@@ -17,6 +17,7 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
 
 // device copies of the refactor maps (allocated at the first dd_refactor)
 struct RfState {
+    int32_t *SubU = nullptr, *URows = nullptr;
     int32_t *SubLev = nullptr, *LevPtr = nullptr, *LevRows = nullptr, *Wcol = nullptr, *UpdQ = nullptr,
             *UpdT = nullptr, *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
     int64_t *Wrp = nullptr, *Wdiag = nullptr, *Uptr = nullptr, *Lrp = nullptr, *Urp = nullptr, *Loff = nullptr,
@@ -33,6 +34,8 @@ dd_status refactor_init(dd_ctx *c) {
     TRY(upload_vec(&rf->SubLev, c->SubLev));
     TRY(upload_vec(&rf->LevPtr, c->LevPtr));
     TRY(upload_vec(&rf->LevRows, c->LevRows));
+    TRY(upload_vec(&rf->SubU, c->SubU));
+    TRY(upload_vec(&rf->URows, c->URows));
     TRY(upload_vec(&rf->Wcol, c->Wcol));
     TRY(upload_vec(&rf->UpdQ, c->UpdQ));
     TRY(upload_vec(&rf->UpdT, c->UpdT));
@@ -80,7 +83,7 @@ namespace ddi {
 void refactor_free(dd_ctx *c) {
     auto *rf = reinterpret_cast<RfState *>(c->rf);
     if (!rf) return;
-    for (void *p : {(void *)rf->SubLev, (void *)rf->LevPtr, (void *)rf->LevRows, (void *)rf->Wcol, (void *)rf->UpdQ,
+    for (void *p : {(void *)rf->SubU, (void *)rf->URows, (void *)rf->SubLev, (void *)rf->LevPtr, (void *)rf->LevRows, (void *)rf->Wcol, (void *)rf->UpdQ,
                     (void *)rf->UpdT, (void *)rf->Lst, (void *)rf->Ust, (void *)rf->Dst, (void *)rf->Wrp,
                     (void *)rf->Wdiag, (void *)rf->Uptr, (void *)rf->Lrp, (void *)rf->Urp, (void *)rf->Loff,
                     (void *)rf->Uoff, (void *)rf->Doff, (void *)rf->Wsrc, (void *)rf->Esrc, (void *)rf->W,
@@ -128,7 +131,7 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
     ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
     *rf->h_bad = ~0ull;
     CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    ddk::RfArgs a{rf->SubLev, rf->LevPtr, rf->LevRows, rf->Wrp, rf->Wdiag, rf->Uptr, rf->Lrp, rf->Urp,
+    ddk::RfArgs a{rf->SubLev, rf->LevPtr, rf->LevRows, rf->SubU, rf->URows, rf->Wrp, rf->Wdiag, rf->Uptr, rf->Lrp, rf->Urp,
                   rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes, rf->Loff, rf->Uoff, rf->Doff,
                   rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad, c->row_first};
     const int nsl = c->sub_last - c->sub_first;

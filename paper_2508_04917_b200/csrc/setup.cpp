@@ -776,25 +776,47 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 ctx->UpdT[at] = (int32_t)t;
             });
         }
-        // level lists per local subdomain: L levels ascending, rows ascending
+        // level lists per local subdomain: L levels ascending, rows in the
+        // order of the slab's L records (stable by L block count, descending),
+        // so the refactor kernel's L-block stores to the slab planes are
+        // coalesced; and all rows in the order of the U records (U levels
+        // ascending, stable by U block count) for its Dinv / U_unit pass
         ctx->SubLev.assign(nsl + 1, 0);
+        ctx->SubU.assign(nsl + 1, 0);
         ctx->LevPtr.clear();
         ctx->LevRows.clear();
         ctx->LevRows.reserve(nl);
+        ctx->URows.clear();
+        ctx->URows.reserve(nl);
+        auto nL = [&](int32_t li) { return ctx->Lrp[li + 1] - ctx->Lrp[li]; };
+        auto nU = [&](int32_t li) { return ctx->Urp[li + 1] - ctx->Urp[li]; };
         for (int32_t q = 0; q < nsl; ++q) {
             const int64_t a = ctx->sub_ptr[s0 + q] - r0, e = ctx->sub_ptr[s0 + q + 1] - r0;
-            int32_t hl = 0;
-            for (int64_t li = a; li < e; ++li) hl = std::max(hl, ctx->hmapL[li]);
-            std::vector<std::vector<int32_t>> lv(hl + 1);
-            for (int64_t li = a; li < e; ++li) lv[ctx->hmapL[li]].push_back((int32_t)li);
+            int32_t hl = 0, hu = 0;
+            for (int64_t li = a; li < e; ++li) {
+                hl = std::max(hl, ctx->hmapL[li]);
+                hu = std::max(hu, ctx->hmapU[li]);
+            }
+            std::vector<std::vector<int32_t>> lv(hl + 1), uv(hu + 1);
+            for (int64_t li = a; li < e; ++li) {
+                lv[ctx->hmapL[li]].push_back((int32_t)li);
+                uv[ctx->hmapU[li]].push_back((int32_t)li);
+            }
             ctx->SubLev[q] = (int32_t)ctx->LevPtr.size();
             for (auto &l : lv) {
+                std::stable_sort(l.begin(), l.end(), [&](int32_t x, int32_t y) { return nL(x) > nL(y); });
                 ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
                 ctx->LevRows.insert(ctx->LevRows.end(), l.begin(), l.end());
+            }
+            ctx->SubU[q] = (int32_t)ctx->URows.size();
+            for (auto &u : uv) {
+                std::stable_sort(u.begin(), u.end(), [&](int32_t x, int32_t y) { return nU(x) > nU(y); });
+                ctx->URows.insert(ctx->URows.end(), u.begin(), u.end());
             }
         }
         ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
         ctx->SubLev[nsl] = (int32_t)ctx->LevPtr.size() - 1;
+        ctx->SubU[nsl] = (int32_t)ctx->URows.size();
     }
     const double t4 = now_ms();
     ctx->setup_ms[3] = t4 - t3;
