@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "dd_internal.h"
 #include "refactor.cuh"
@@ -136,11 +137,130 @@ __global__ void __launch_bounds__(128) k_refactor(RfArgs a) {
     }
 }
 
+// Nine lanes per 3x3 block ("a warp per row and 9 lanes per 3x3
+// op"): lane v = 3r + c of a 9-lane group owns element (r, c) of every block
+// the group touches, so each block load / store is 72 contiguous bytes and
+// every element of W is only ever loaded and stored by the same lane (no
+// cross-lane memory ordering inside a group); the other elements a product
+// needs arrive by warp shuffles. Three groups per warp (lanes 27-31 idle),
+// so a 512-thread CTA factors 48 rows of a level at once. Loops run to the
+// warp's maximum trip count with predicated memory operations, so every
+// shuffle is warp-uniform. Per element the FMA order is rf_mul3 /
+// rf_sub_mul / rf_inv3's (= the host setup's): identical bits.
+constexpr int RF9_THREADS = 512;
+
+__device__ __forceinline__ double g9(double x, int gbase, int src) {
+    return __shfl_sync(0xffffffffu, x, (gbase + src) & 31);
+}
+
+__device__ __forceinline__ int warp_max(int x) { return __reduce_max_sync(0xffffffffu, x); }
+
+__global__ void __launch_bounds__(RF9_THREADS) k_refactor9(RfArgs a) {
+    const int q = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / 9;  // 0..2 active, 3 = idle lanes 27..31
+    const int v = lane - 9 * grp, r3 = 3 * (v / 3), c = v % 3;
+    const int gbase = 9 * grp;
+    const bool live = grp < 3;
+    const int per_pass = 3 * (blockDim.x / 32);
+    for (int lev = a.SubLev[q]; lev < a.SubLev[q + 1]; ++lev) {
+        const int lo = a.LevPtr[lev], hi = a.LevPtr[lev + 1];
+        for (int base = lo + 3 * warp; base < hi; base += per_pass) {
+            const int idx = base + grp;
+            const bool has = live && idx < hi;
+            const int64_t li = has ? a.LevRows[idx] : 0;
+            const int64_t w0 = has ? a.Wrp[li] : 0, d = has ? a.Wdiag[li] : 0;
+            const int nlow = has ? (int)(d - w0) : 0;
+            const int maxlow = warp_max(nlow);
+            for (int jp = 0; jp < maxlow; ++jp) {
+                const bool ok = jp < nlow;
+                const int64_t p = w0 + jp;
+                const int64_t k = ok ? a.Wcol[p] : 0;
+                const double wv = ok ? a.W[9 * p + v] : 0.0;
+                const double dv = ok ? a.Dinv[9 * k + v] : 0.0;
+                // L_ik = W_ik * U_kk^-1 (R12): rf_mul3(W, Dinv, L)
+                const double Lv = __fma_rn(g9(wv, gbase, r3 + 2), g9(dv, gbase, 6 + c),
+                                           __fma_rn(g9(wv, gbase, r3 + 1), g9(dv, gbase, 3 + c),
+                                                    g9(wv, gbase, r3) * g9(dv, gbase, c)));
+                if (ok) {
+                    a.W[9 * p + v] = Lv;
+                    const int64_t b = a.Lrp[li] + jp;
+                    *reinterpret_cast<double *>(a.slab + a.Loff[b] + (int64_t)a.Lst[b] * v) = Lv;
+                }
+                const int64_t u0 = ok ? a.Uptr[p] : 0;
+                const int nup = ok ? (int)(a.Uptr[p + 1] - u0) : 0;
+                const int maxup = warp_max(nup);
+                for (int ju = 0; ju < maxup; ++ju) {
+                    const bool okk = ju < nup;
+                    const int64_t t = okk ? a.UpdT[u0 + ju] : 0, qq = okk ? a.UpdQ[u0 + ju] : 0;
+                    const double wt = okk ? a.W[9 * t + v] : 0.0;
+                    const double uq = okk ? a.W[9 * qq + v] : 0.0;
+                    // W_ij -= L_ik U_kj: rf_sub_mul's order
+                    double w = __fma_rn(-g9(Lv, gbase, r3), g9(uq, gbase, c), wt);
+                    w = __fma_rn(-g9(Lv, gbase, r3 + 1), g9(uq, gbase, 3 + c), w);
+                    w = __fma_rn(-g9(Lv, gbase, r3 + 2), g9(uq, gbase, 6 + c), w);
+                    if (okk) a.W[9 * t + v] = w;
+                }
+            }
+            // Dinv_i = inv(U_ii): every lane of the group gathers the block
+            const double mv = has ? a.W[9 * d + v] : 0.0;
+            double m[9], inv[9];
+#pragma unroll
+            for (int e = 0; e < 9; ++e) m[e] = g9(mv, gbase, e);
+            const bool okinv = rf_inv3(m, a.floor_, inv);
+            if (has) {
+                if (!okinv) {
+                    if (v == 0) atomicMin(a.bad, (unsigned long long)(a.row_first + li));
+                } else {
+                    double mine = inv[0];
+#pragma unroll
+                    for (int e = 1; e < 9; ++e)
+                        if (e == v) mine = inv[e];
+                    a.Dinv[9 * li + v] = mine;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // Dinv and U_unit_ij = Dinv_i U_ij in the order of the U records
+    const int ulo = a.SubU[q], uhi = a.SubU[q + 1];
+    for (int base = ulo + 3 * warp; base < uhi; base += per_pass) {
+        const int idx = base + grp;
+        const bool has = live && idx < uhi;
+        const int64_t li = has ? a.URows[idx] : 0;
+        const int64_t d = has ? a.Wdiag[li] : 0, w1 = has ? a.Wrp[li + 1] : 0;
+        const double iv = has ? a.Dinv[9 * li + v] : 0.0;
+        if (has) *reinterpret_cast<double *>(a.slab + a.Doff[li] + (int64_t)a.Dst[li] * v) = iv;
+        const int nu = has ? (int)(w1 - d - 1) : 0;
+        const int maxu = warp_max(nu);
+        for (int ju = 0; ju < maxu; ++ju) {
+            const bool ok = ju < nu;
+            const int64_t p = d + 1 + ju;
+            const double wv = ok ? a.W[9 * p + v] : 0.0;
+            // rf_mul3(inv, W, Uu)
+            const double uu = __fma_rn(g9(iv, gbase, r3 + 2), g9(wv, gbase, 6 + c),
+                                       __fma_rn(g9(iv, gbase, r3 + 1), g9(wv, gbase, 3 + c),
+                                                g9(iv, gbase, r3) * g9(wv, gbase, c)));
+            if (ok) {
+                const int64_t b = a.Urp[li] + ju;
+                *reinterpret_cast<double *>(a.slab + a.Uoff[b] + (int64_t)a.Ust[b] * v) = uu;
+            }
+        }
+    }
+}
+
 void launch_gather_blocks(int64_t n, const int64_t *src, const double *from, double *to, int ell, int grid,
                           cudaStream_t st) {
     k_gather_blocks<<<grid, 256, 0, st>>>(n, src, from, to, ell);
 }
 
-void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st) { k_refactor<<<nsl, 128, 0, st>>>(a); }
+// DD_REFACTOR_KERNEL=1: the round-1 kernel (one thread per row), for A/B
+void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st) {
+    static const bool old = getenv("DD_REFACTOR_KERNEL") && atoi(getenv("DD_REFACTOR_KERNEL")) == 1;
+    if (old)
+        k_refactor<<<nsl, 128, 0, st>>>(a);
+    else
+        k_refactor9<<<nsl, RF9_THREADS, 0, st>>>(a);
+}
 
 }  // namespace ddk
