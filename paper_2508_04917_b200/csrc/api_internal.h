@@ -40,8 +40,8 @@ dd_status dmalloc(T **p, size_t count) {
     return DD_OK;
 }
 
-template <class T>
-dd_status upload_vec(T **d, const std::vector<T> &h) {
+template <class T, class A>
+dd_status upload_vec(T **d, const std::vector<T, A> &h) {
     TRY(dmalloc(d, std::max<size_t>(1, h.size())));
     if (!h.empty()) CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
     return DD_OK;

@@ -154,13 +154,13 @@ struct dd_ctx {
     int32_t kmax = 0;  // most blocks of a row in one factor triangle (> 3: general-K kernels)
     // factors of the local rows (local numbering)
     std::vector<int64_t> Lrp, Urp;
-    std::vector<int32_t> Lci, Uci;
+    ddi::uvector<int32_t> Lci, Uci;
     ddi::uvector<double> Lv, Uv, Dinv;
     std::vector<int32_t> hmapL, hmapU;
     int32_t max_lev_L = 0, max_lev_U = 0;
     // local rows of A_r, columns in local+ghost numbering
     std::vector<int64_t> Arp;
-    std::vector<int32_t> Aci;
+    ddi::uvector<int32_t> Aci;
     ddi::uvector<double> Av;
     std::vector<int64_t> ghost_rows;   // reordered global ids, ascending
     std::vector<int32_t> ghost_owner;
@@ -195,16 +195,17 @@ struct dd_ctx {
     // --- refactor (dd_refactor) symbolic maps, built when opts.enable_refactor
     bool refactor = false;
     double pivot_floor = 1e-300;
-    std::vector<int64_t> Asrc;           // reordered local A_r block -> original block index
-    std::vector<int64_t> Wrp, Wsrc;      // A_dd working layout (rank-local rows)
-    std::vector<int32_t> Wcol;
+    ddi::uvector<int64_t> Asrc;          // reordered local A_r block -> original block index
+    std::vector<int64_t> Wrp;            // A_dd working layout (rank-local rows)
+    ddi::uvector<int64_t> Wsrc;
+    ddi::uvector<int32_t> Wcol;
     std::vector<int64_t> Wdiag;
-    std::vector<int64_t> Uptr;           // per W position: update range
-    std::vector<int32_t> UpdQ, UpdT;     // (U_kj position, target position)
+    ddi::uvector<int64_t> Uptr;          // per W position: update range
+    ddi::uvector<int32_t> UpdQ, UpdT;    // (U_kj position, target position)
     std::vector<int32_t> LevRows, LevPtr, SubLev;
     std::vector<int32_t> URows, SubU;    // rows in U-record order per subdomain (refactor's Dinv / U_unit pass)
-    std::vector<int64_t> SlabLoff, SlabUoff, SlabDoff;  // byte offsets into the slab
-    std::vector<int32_t> SlabLst, SlabUst, SlabDst;     // plane strides (bytes)
+    ddi::uvector<int64_t> SlabLoff, SlabUoff, SlabDoff;  // byte offsets into the slab
+    ddi::uvector<int32_t> SlabLst, SlabUst, SlabDst;     // plane strides (bytes)
     void *rf = nullptr;                  // device-side refactor state (api.cpp)
     mutable int64_t n_launches = 0;      // kernels launched by this context
     void *prof = nullptr;                // api.cpp profiling state

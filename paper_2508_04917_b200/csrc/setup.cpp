@@ -13,6 +13,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -480,11 +481,11 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         Arp[li + 1] = Arp[li] + (rp[m + 1] - rp[m]);
     }
     const int64_t nnz_loc = Arp[nl];
-    std::vector<int32_t> gcol(nnz_loc);
+    uvector<int32_t> gcol(nnz_loc);  // every entry written below
     ctx->Av.resize(b2 * nnz_loc);  // every block written below
     ctx->refactor = o->enable_refactor != 0;
     ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
-    if (ctx->refactor) ctx->Asrc.assign(nnz_loc, -1);
+    if (ctx->refactor) ctx->Asrc.resize(nnz_loc);  // every entry written below
 #pragma omp parallel for schedule(static)
     for (int64_t li = 0; li < nl; ++li) {
         const int64_t m = ctx->new_to_old[r0 + li];
@@ -564,7 +565,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             need.erase(std::unique(need.begin(), need.end()), need.end());
             ctx->send_rows[q] = std::move(need);
         }
-        ctx->Aci.assign(nnz_loc, 0);
+        ctx->Aci.resize(nnz_loc);
 #pragma omp parallel for schedule(static)
         for (int64_t p = 0; p < nnz_loc; ++p) {
             const int32_t g = gcol[p];
@@ -603,8 +604,8 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         ctx->Lrp[li + 1] += ctx->Lrp[li];
         ctx->Urp[li + 1] += ctx->Urp[li];
     }
-    ctx->Lci.assign(ctx->Lrp[nl], 0);
-    ctx->Uci.assign(ctx->Urp[nl], 0);
+    ctx->Lci.resize(ctx->Lrp[nl]);
+    ctx->Uci.resize(ctx->Urp[nl]);
     ctx->Lv.resize(b2 * ctx->Lrp[nl]);  // written by the scatter below
     ctx->Uv.resize(b2 * ctx->Urp[nl]);
     // DD_ILU0 ablation: keep the non-unit U_ij too (a second slab, BSR3 only)
@@ -724,11 +725,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             set_error("dd_setup: refactor maps need fewer than 2^31 dropped-pattern blocks per rank");
             return DD_E_INVALID_ARG;
         }
-        ctx->Wsrc.assign(nW, 0);
-        ctx->Wcol.assign(nW, 0);
+        ctx->Wsrc.resize(nW);
+        ctx->Wcol.resize(nW);
         ctx->Wdiag.assign(nl, 0);
-        ctx->Uptr.assign(nW + 1, 0);
-        std::vector<int32_t> nupd(nW, 0);
+        ctx->Uptr.resize(nW + 1);
+        ctx->Uptr[0] = 0;
+        uvector<int32_t> nupd(nW);
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < nW; ++p) nupd[p] = 0;
 #pragma omp parallel for schedule(static)
         for (int64_t li = 0; li < nl; ++li) {
             const int32_t s = row_sub[li];
@@ -744,6 +748,8 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 }
             }
         }
+        static const bool trace = getenv("DD_SETUP_TRACE") != nullptr;
+        if (trace) fprintf(stderr, "[dd setup] refactor W layout %9.1f ms\n", now_ms() - t3);
         // update lists: for lower position p = (i, k): every U_kj (j > k) whose
         // column j is in row i's pattern -> (position of U_kj, position of W_ij),
         // in ascending j (the order of the host / oracle elimination)
@@ -764,32 +770,30 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
 #pragma omp parallel for schedule(static)
         for (int64_t li = 0; li < nl; ++li) for_updates(li, [&](int64_t p, int64_t, int64_t) { ++nupd[p]; });
         for (int64_t p = 0; p < nW; ++p) ctx->Uptr[p + 1] = ctx->Uptr[p] + nupd[p];
-        ctx->UpdQ.assign(ctx->Uptr[nW], 0);
-        ctx->UpdT.assign(ctx->Uptr[nW], 0);
+        ctx->UpdQ.resize(ctx->Uptr[nW]);
+        ctx->UpdT.resize(ctx->Uptr[nW]);
 #pragma omp parallel for schedule(static)
         for (int64_t li = 0; li < nl; ++li) {
-            std::vector<int64_t> fill;
+            // for_updates visits the updates of one position p consecutively
+            int64_t last = -1, at = 0;
             for_updates(li, [&](int64_t p, int64_t qk, int64_t t) {
-                const int64_t at = ctx->Uptr[p] + (int64_t)std::count(fill.begin(), fill.end(), p);
-                fill.push_back(p);
+                at = p == last ? at + 1 : ctx->Uptr[p];
+                last = p;
                 ctx->UpdQ[at] = (int32_t)qk;
                 ctx->UpdT[at] = (int32_t)t;
             });
         }
+        if (trace) fprintf(stderr, "[dd setup] refactor updates  %9.1f ms\n", now_ms() - t3);
         // level lists per local subdomain: L levels ascending, rows in the
         // order of the slab's L records (stable by L block count, descending),
         // so the refactor kernel's L-block stores to the slab planes are
         // coalesced; and all rows in the order of the U records (U levels
         // ascending, stable by U block count) for its Dinv / U_unit pass
-        ctx->SubLev.assign(nsl + 1, 0);
-        ctx->SubU.assign(nsl + 1, 0);
-        ctx->LevPtr.clear();
-        ctx->LevRows.clear();
-        ctx->LevRows.reserve(nl);
-        ctx->URows.clear();
-        ctx->URows.reserve(nl);
         auto nL = [&](int32_t li) { return ctx->Lrp[li + 1] - ctx->Lrp[li]; };
         auto nU = [&](int32_t li) { return ctx->Urp[li + 1] - ctx->Urp[li]; };
+        // per subdomain in parallel, then concatenated in subdomain order
+        std::vector<std::vector<int32_t>> lrows(nsl), lptr(nsl), urows(nsl);
+#pragma omp parallel for schedule(dynamic, 8)
         for (int32_t q = 0; q < nsl; ++q) {
             const int64_t a = ctx->sub_ptr[s0 + q] - r0, e = ctx->sub_ptr[s0 + q + 1] - r0;
             int32_t hl = 0, hu = 0;
@@ -802,17 +806,30 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                 lv[ctx->hmapL[li]].push_back((int32_t)li);
                 uv[ctx->hmapU[li]].push_back((int32_t)li);
             }
-            ctx->SubLev[q] = (int32_t)ctx->LevPtr.size();
             for (auto &l : lv) {
                 std::stable_sort(l.begin(), l.end(), [&](int32_t x, int32_t y) { return nL(x) > nL(y); });
-                ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
-                ctx->LevRows.insert(ctx->LevRows.end(), l.begin(), l.end());
+                lptr[q].push_back((int32_t)lrows[q].size());
+                lrows[q].insert(lrows[q].end(), l.begin(), l.end());
             }
-            ctx->SubU[q] = (int32_t)ctx->URows.size();
             for (auto &u : uv) {
                 std::stable_sort(u.begin(), u.end(), [&](int32_t x, int32_t y) { return nU(x) > nU(y); });
-                ctx->URows.insert(ctx->URows.end(), u.begin(), u.end());
+                urows[q].insert(urows[q].end(), u.begin(), u.end());
             }
+        }
+        ctx->SubLev.assign(nsl + 1, 0);
+        ctx->SubU.assign(nsl + 1, 0);
+        ctx->LevPtr.clear();
+        ctx->LevRows.clear();
+        ctx->LevRows.reserve(nl);
+        ctx->URows.clear();
+        ctx->URows.reserve(nl);
+        for (int32_t q = 0; q < nsl; ++q) {
+            ctx->SubLev[q] = (int32_t)ctx->LevPtr.size();
+            const int32_t off = (int32_t)ctx->LevRows.size();
+            for (int32_t p : lptr[q]) ctx->LevPtr.push_back(off + p);
+            ctx->LevRows.insert(ctx->LevRows.end(), lrows[q].begin(), lrows[q].end());
+            ctx->SubU[q] = (int32_t)ctx->URows.size();
+            ctx->URows.insert(ctx->URows.end(), urows[q].begin(), urows[q].end());
         }
         ctx->LevPtr.push_back((int32_t)ctx->LevRows.size());
         ctx->SubLev[nsl] = (int32_t)ctx->LevPtr.size() - 1;
@@ -849,12 +866,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     choose_swizzle(ctx, r0);
     SlabMaps mp;
     if (ctx->refactor) {
-        ctx->SlabLoff.assign(ctx->Lci.size(), 0);
-        ctx->SlabLst.assign(ctx->Lci.size(), 0);
-        ctx->SlabUoff.assign(ctx->Uci.size(), 0);
-        ctx->SlabUst.assign(ctx->Uci.size(), 0);
-        ctx->SlabDoff.assign(nl, 0);
-        ctx->SlabDst.assign(nl, 0);
+        ctx->SlabLoff.resize(ctx->Lci.size());
+        ctx->SlabLst.resize(ctx->Lci.size());
+        ctx->SlabUoff.resize(ctx->Uci.size());
+        ctx->SlabUst.resize(ctx->Uci.size());
+        ctx->SlabDoff.resize(nl);
+        ctx->SlabDst.resize(nl);
         mp = SlabMaps{ctx->SlabLoff.data(), ctx->SlabUoff.data(), ctx->SlabDoff.data(),
                       ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data()};
     }
