@@ -4,7 +4,11 @@
 #pragma once
 
 #include <cstdint>
+#include <sys/mman.h>
+
+#include <cstdlib>
 #include <memory>
+#include <new>
 #include <string>
 #include <utility>
 #include <vector>
@@ -22,6 +26,8 @@ namespace ddi {
 
 // Large host arrays that are fully overwritten after allocation: resize()
 // leaves the elements uninitialised (no single-threaded zero fill of GBs).
+// Buffers of 32 MB and more come 2 MB-aligned with MADV_HUGEPAGE: the
+// first-touch page faults of GBs of 4 KB pages were a visible part of setup.
 template <class T>
 struct UninitAlloc : std::allocator<T> {
     template <class U>
@@ -31,6 +37,22 @@ struct UninitAlloc : std::allocator<T> {
     UninitAlloc() = default;
     template <class U>
     UninitAlloc(const UninitAlloc<U> &) {}
+    static constexpr size_t kBig = 32u << 20, kHuge = 2u << 20;
+    T *allocate(size_t n) {
+        const size_t bytes = n * sizeof(T);
+        if (bytes < kBig) return std::allocator<T>::allocate(n);
+        const size_t sz = (bytes + kHuge - 1) / kHuge * kHuge;
+        void *p = std::aligned_alloc(kHuge, sz);
+        if (!p) throw std::bad_alloc();
+        madvise(p, sz, MADV_HUGEPAGE);
+        return static_cast<T *>(p);
+    }
+    void deallocate(T *p, size_t n) {
+        if (n * sizeof(T) < kBig)
+            std::allocator<T>::deallocate(p, n);
+        else
+            std::free(p);
+    }
     template <class U>
     void construct(U *) noexcept {}
     template <class U, class... A>
