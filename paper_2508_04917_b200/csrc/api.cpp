@@ -27,19 +27,20 @@ namespace {
 // other (pageable cudaMemcpy runs at ~3 GB/s; this at ~10-20 GB/s).
 dd_status h2d_big(void *dst, const void *src, size_t bytes) {
     constexpr size_t STG = 32u << 20;
+    constexpr int NB = 4;  // staging buffers in flight
     if (bytes < 2 * STG) {
         CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
         return DD_OK;
     }
-    uint8_t *stg[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    uint8_t *stg[NB] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[NB] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t st = nullptr;
     dd_status rc = DD_OK;
-    if (cudaMallocHost(reinterpret_cast<void **>(&stg[0]), STG) != cudaSuccess ||
-        cudaMallocHost(reinterpret_cast<void **>(&stg[1]), STG) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    bool ok = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess;
+    for (int q = 0; q < NB && ok; ++q)
+        ok = cudaMallocHost(reinterpret_cast<void **>(&stg[q]), STG) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
         cudaGetLastError();
         rc = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? DD_OK : DD_E_CUDA;
     } else {
@@ -47,8 +48,8 @@ dd_status h2d_big(void *dst, const void *src, size_t bytes) {
         uint8_t *d8 = reinterpret_cast<uint8_t *>(dst);
         for (size_t off = 0, i = 0; off < bytes; off += STG, ++i) {
             const size_t n = std::min(STG, bytes - off);
-            uint8_t *b = stg[i % 2];
-            if (i >= 2) cudaEventSynchronize(ev[i % 2]);  // its previous DMA is done
+            uint8_t *b = stg[i % NB];
+            if (i >= NB) cudaEventSynchronize(ev[i % NB]);  // its previous DMA is done
             const int nt = 16;
 #pragma omp parallel for num_threads(nt) schedule(static)
             for (int q = 0; q < nt; ++q) {
@@ -59,7 +60,7 @@ dd_status h2d_big(void *dst, const void *src, size_t bytes) {
                 rc = DD_E_CUDA;
                 break;
             }
-            cudaEventRecord(ev[i % 2], st);
+            cudaEventRecord(ev[i % NB], st);
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) rc = DD_E_CUDA;
     }
@@ -181,34 +182,32 @@ dd_status device_setup(dd_ctx *ctx) {
         }
         tr("ell pointers");
         const int b2 = ctx->bs * ctx->bs;
-        // uninitialised buffers, every slot written once by the slice that owns
-        // it (padding slots: column -1, values 0) -- no serial zero-fill pass
-        std::unique_ptr<int32_t[]> cols(new int32_t[std::max<int64_t>(1, S.n_slots)]);
-        std::unique_ptr<double[]> vals(new double[std::max<int64_t>(1, b2 * S.n_slots)]);
-#pragma omp parallel for schedule(static)
-        for (int64_t s = 0; s < S.n_slices; ++s) {
-            const int64_t K = (sp[s + 1] - sp[s]) / 32;
-            for (int64_t k = 0; k < K; ++k) {
-                int32_t *cs = &cols[sp[s] + 32 * k];
-                double *vs = &vals[b2 * (sp[s] + 32 * k)];
-                for (int lane = 0; lane < 32; ++lane) {
-                    const int64_t li = 32 * s + lane;
-                    const bool has = li < nl && k < ctx->Arp[li + 1] - ctx->Arp[li];
-                    const int64_t p = has ? ctx->Arp[li] + k : 0;
-                    cs[lane] = has ? ctx->Aci[p] : -1;
-                    for (int v = 0; v < b2; ++v) vs[32 * v + lane] = has ? ctx->Av[b2 * p + v] : 0.0;
-                }
-            }
-        }
         TRY(dmalloc(&S.slot_ptr, sp.size()));
         TRY(dmalloc(&S.cols, std::max<int64_t>(1, S.n_slots)));
         TRY(dmalloc(&S.vals, std::max<int64_t>(1, b2 * S.n_slots)));
         CK(cudaMemcpy(S.slot_ptr, sp.data(), sp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
         if (S.n_slots) {
-            tr("ell fill");
-            TRY(h2d_big(S.cols, cols.get(), S.n_slots * sizeof(int32_t)));
-            TRY(h2d_big(S.vals, vals.get(), b2 * S.n_slots * sizeof(double)));
-            tr("ell upload");
+            // the rank's reordered rows (row pointers, local+ghost columns,
+            // values) go up as they are; a kernel lays them out as sliced ELL
+            // (no host pass over the 2 GB of values, no host ELL buffers)
+            int64_t *d_rp = nullptr;
+            int32_t *d_ci = nullptr;
+            double *d_av = nullptr;
+            const int64_t nnz = ctx->Arp[nl];
+            TRY(dmalloc(&d_rp, nl + 1));
+            TRY(dmalloc(&d_ci, std::max<int64_t>(1, nnz)));
+            TRY(dmalloc(&d_av, std::max<int64_t>(1, b2 * nnz)));
+            CK(cudaMemcpy(d_rp, ctx->Arp.data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+            TRY(h2d_big(d_ci, ctx->Aci.data(), nnz * sizeof(int32_t)));
+            TRY(h2d_big(d_av, ctx->Av.data(), b2 * nnz * sizeof(double)));
+            tr("ell rows upload");
+            ddk::launch_build_ell(ctx->bs, S.n_slices, nl, S.slot_ptr, d_rp, d_ci, d_av, S.cols, S.vals, nullptr);
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
+            cudaFree(d_rp);
+            cudaFree(d_ci);
+            cudaFree(d_av);
+            tr("ell build");
         }
     }
     // permutation index of the local rows (original global row of local row li)
@@ -226,8 +225,14 @@ dd_status device_setup(dd_ctx *ctx) {
     ctx->dev_ws = ws;
     ws->m = ctx->bs * nl;
     const size_t mm = (size_t)ws->m + 2;  // +2: 16-byte slack past the end (dd.h)
-    for (double **q : {&ws->r, &ws->rh, &ws->p, &ws->v, &ws->ph, &ws->s, &ws->sh, &ws->t, &ws->bd, &ws->xd})
-        TRY(dmalloc(q, mm));
+    // the ten solver vectors in one allocation (one cudaMalloc instead of
+    // ten: ~10 ms each at 98 MB), each 256-byte aligned with 16 B of slack
+    {
+        const size_t stride = (mm * sizeof(double) + 255) / 256 * 256 / sizeof(double);
+        TRY(dmalloc(&ws->vecs, 10 * stride));
+        double **v[10] = {&ws->r, &ws->rh, &ws->p, &ws->v, &ws->ph, &ws->s, &ws->sh, &ws->t, &ws->bd, &ws->xd};
+        for (int q = 0; q < 10; ++q) *v[q] = ws->vecs + q * stride;
+    }
     TRY(dmalloc(&ws->sc, ddk::S_COUNT));
     CK(cudaMemset(ws->sc, 0, ddk::S_COUNT * sizeof(double)));
     CK(cudaMalloc(&ws->partials, ddk::partials_bytes(ctx)));
@@ -510,9 +515,7 @@ void dd_destroy(dd_ctx *c) {
         cudaFree(c->d_stage);
         cudaFree(c->d_vecg);
         if (Workspace *ws = ws_of(c)) {
-            for (double *q : {ws->r, ws->rh, ws->p, ws->v, ws->ph, ws->s, ws->sh, ws->t, ws->bd, ws->xd, ws->sc,
-                              ws->loc, ws->gathered, ws->sendbuf})
-                cudaFree(q);
+            for (double *q : {ws->vecs, ws->sc, ws->loc, ws->gathered, ws->sendbuf}) cudaFree(q);
             if (!ws->box) cudaFree(ws->xg);
             cudaFree(ws->box);
             cudaFree(ws->d_boxes);

@@ -49,6 +49,7 @@ dd_status upload_vec(T **d, const std::vector<T, A> &h) {
 
 struct Workspace {
     int64_t m = 0;  // bs * n_local
+    double *vecs = nullptr;  // one allocation holding the ten vectors below
     double *r = nullptr, *rh = nullptr, *p = nullptr, *v = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr,
            *t = nullptr, *bd = nullptr, *xd = nullptr;
     double *sc = nullptr;        // device scalars [S_COUNT]

@@ -681,6 +681,37 @@ void launch_resid(const dd_ctx *ctx, int64_t m, const double *b, double *t, cons
 void launch_finalize_gathered(int world, int nv, const double *gathered, const RedArgs &ra, int op, cudaStream_t st) {
     k_finalize_gathered<<<1, 32, 0, st>>>(world, nv, gathered, ra, op);
 }
+template <int BS>
+__global__ void k_build_ell(int64_t n_slices, int64_t n_rows, const int64_t *__restrict__ slot_ptr,
+                            const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            const double *__restrict__ av, int32_t *__restrict__ cols, double *__restrict__ vals) {
+    constexpr int B2 = BS * BS;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); s < n_slices; s += warps) {
+        const int64_t li = 32 * s + lane;
+        const int64_t p0 = li < n_rows ? rp[li] : 0, len = li < n_rows ? rp[li + 1] - p0 : 0;
+        const int64_t K = (slot_ptr[s + 1] - slot_ptr[s]) / 32;
+        for (int64_t k = 0; k < K; ++k) {
+            const bool has = k < len;
+            const int64_t slot = slot_ptr[s] + 32 * k;
+            cols[slot + lane] = has ? ci[p0 + k] : -1;
+#pragma unroll
+            for (int v = 0; v < B2; ++v) vals[B2 * slot + 32 * v + lane] = has ? av[B2 * (p0 + k) + v] : 0.0;
+        }
+    }
+}
+
+void launch_build_ell(int bs, int64_t n_slices, int64_t n_rows, const int64_t *slot_ptr, const int64_t *rp,
+                      const int32_t *ci, const double *av, int32_t *cols, double *vals, cudaStream_t st) {
+    if (n_slices <= 0) return;
+    const int g = (int)std::min<int64_t>(4096, (n_slices + 7) / 8);
+    if (bs == 3)
+        k_build_ell<3><<<g, 256, 0, st>>>(n_slices, n_rows, slot_ptr, rp, ci, av, cols, vals);
+    else
+        k_build_ell<1><<<g, 256, 0, st>>>(n_slices, n_rows, slot_ptr, rp, ci, av, cols, vals);
+}
+
 void launch_peer_allgather_finalize(const PeerDev &d, int nv, const double *loc, const RedArgs &ra, int op,
                                     cudaStream_t st) {
     k_peer_allgather_finalize<<<1, 32, 0, st>>>(d, nv, loc, ra, op);

@@ -88,5 +88,10 @@ void launch_gather3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const doub
 void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const double *in, double *out,
                      cudaStream_t st);
 size_t partials_bytes(const dd_ctx *ctx);
+// sliced-ELL SpMV operand from the rank's reordered rows (dd_setup): slot
+// (k, lane) of slice s = block k of row 32 s + lane (column -1 and zero
+// values past a row's end), values as bs*bs planes of 32 per k
+void launch_build_ell(int bs, int64_t n_slices, int64_t n_rows, const int64_t *slot_ptr, const int64_t *rp,
+                      const int32_t *ci, const double *av, int32_t *cols, double *vals, cudaStream_t st);
 
 }  // namespace ddk
