@@ -364,6 +364,8 @@ def run_ours(args, cfg):
                    "l2": "inputs > L2 (2.2 GB factors + 2.2 GB matrix per apply/SpMV vs 126 MB L2); no flush"},
         "iterations": r0["iterations"], "n_applies": r0["n_applies"], "true_rel_resid": r0["true_rel_resid"],
         "setup_ms": round(setup_ms, 1),
+        "setup_phases_ms": {k[:-3]: round(st[k], 1) for k in ("partition_ms", "reorder_drop_ms", "ilu0_ms", "levels_ms",
+                                                             "pack_ms", "upload_ms")},
         "refactor_ms": round(refactor_ms, 2),
         "levels_device_ms": round(levels_device_ms, 3),
         "apply": {"ms": round(apply_ms, 4), "launches": prof["n_apply"],
