@@ -219,10 +219,12 @@ dd_status device_setup(dd_ctx *ctx) {
             const int64_t nnz = ctx->Arp[nl];
             TRY(dmalloc(&d_rp, nl + 1));
             TRY(dmalloc(&d_ci, std::max<int64_t>(1, nnz)));
-            TRY(dmalloc(&d_av, std::max<int64_t>(1, b2 * nnz)));
             CK(cudaMemcpy(d_rp, ctx->Arp.data(), (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
             TRY(h2d_big(d_ci, ctx->Aci.data(), nnz * sizeof(int32_t)));
-            TRY(h2d_big(d_av, ctx->Av.data(), b2 * nnz * sizeof(double)));
+            if (!ctx->gpu_numeric) {  // GPU numeric path: the values arrive with the factorisation
+                TRY(dmalloc(&d_av, std::max<int64_t>(1, b2 * nnz)));
+                TRY(h2d_big(d_av, ctx->Av.data(), b2 * nnz * sizeof(double)));
+            }
             tr("ell rows upload");
             ddk::launch_build_ell(ctx->bs, S.n_slices, nl, S.slot_ptr, d_rp, d_ci, d_av, S.cols, S.vals, nullptr);
             CK(cudaGetLastError());
@@ -503,10 +505,26 @@ static dd_status setup_common(const dd_bsr3 *A, const dd_opts *o_in, dd_ctx **ou
     // launch shape that does not fit), so no rank is left waiting in a
     // collective its peers never reach
     if (o->grid) ctx->grid = *o->grid;
+    {
+        const char *e = getenv("DD_HOST_ILU0");  // 1: the host computes the factors (round-1 path)
+        ctx->gpu_numeric = !ctx->host_only && bs == 3 && !(o->variants & DD_ILU0) && !(e && atoi(e) == 1);
+    }
     dd_status st = host_setup(ctx, A, o);
     if (!ctx->host_only) {
         st = comm_begin(ctx, o->nccl_unique_id, st);
         if (st == DD_OK) st = comm_agree(ctx, device_setup(ctx));
+        if (st == DD_OK && ctx->gpu_numeric) {
+            // block ILU0 -> ILDU0 of every local subdomain on the device, from
+            // the matrix's own values, into the slab and the SpMV operand
+            const double t0 = now_ms();
+            cudaStream_t s0 = nullptr;
+            dd_status fs = cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking) == cudaSuccess ? DD_OK : DD_E_CUDA;
+            if (fs == DD_OK) fs = refactor_values(ctx, A->vals, false, s0);
+            if (s0) cudaStreamDestroy(s0);
+            if (fs == DD_E_SINGULAR_PIVOT) set_error(std::string("dd_setup: ") + last_error_c());
+            st = comm_agree(ctx, fs);
+            ctx->setup_ms[2] += now_ms() - t0;
+        }
         if (st == DD_OK) st = comm_connect(ctx);
         if (st == DD_OK) st = tune_solver_variant(ctx);
         if (st == DD_OK) st = solver_prepare(ctx);
@@ -720,6 +738,28 @@ dd_status dd_levels_device(dd_ctx *c, int32_t *hmapL, int32_t *hmapU, double *ms
 dd_status dd_get_factors(const dd_ctx *c, int64_t *nL, int64_t *nU, int64_t *Lrp, int32_t *Lci, double *Lv,
                          int64_t *Urp, int32_t *Uci, double *Uv, double *Dinv) {
     if (!c) return DD_E_INVALID_ARG;
+    if (c->gpu_numeric && (Lv || Uv || Dinv)) {
+        // the factors live on the device: L from W's lower blocks, U_unit =
+        // Dinv_i U_ij with the host's 3x3 product (same FMA order as the
+        // kernel's and the host ILU0's, section 4)
+        std::vector<double> W, D;
+        TRY(refactor_fetch(c, W, D));
+        for (int64_t li = 0; li < c->n_local; ++li) {
+            const int64_t w0 = c->Wrp[li], d = c->Wdiag[li], w1 = c->Wrp[li + 1];
+            if (Lv)
+                for (int64_t p = w0; p < d; ++p) std::memcpy(Lv + 9 * (c->Lrp[li] + (p - w0)), &W[9 * p], 72);
+            if (Uv)
+                for (int64_t p = d + 1; p < w1; ++p) {
+                    const double *A = &D[9 * li], *B = &W[9 * p];
+                    double *C = Uv + 9 * (c->Urp[li] + (p - d - 1));
+                    for (int r = 0; r < 3; ++r)
+                        for (int cc = 0; cc < 3; ++cc)
+                            C[3 * r + cc] = std::fma(A[3 * r + 2], B[6 + cc], std::fma(A[3 * r + 1], B[3 + cc], A[3 * r] * B[cc]));
+                }
+        }
+        if (Dinv) std::memcpy(Dinv, D.data(), D.size() * sizeof(double));
+        Lv = Uv = Dinv = nullptr;
+    }
     if (nL) *nL = (int64_t)c->Lci.size();
     if (nU) *nU = (int64_t)c->Uci.size();
     if (Lrp) std::memcpy(Lrp, c->Lrp.data(), c->Lrp.size() * sizeof(int64_t));

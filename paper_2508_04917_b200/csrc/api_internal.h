@@ -164,6 +164,12 @@ bool usable(dd_ctx *c);
 
 // ---- refactor_api.cpp
 void refactor_free(dd_ctx *c);
+// numeric factorisation of new values on the device (dd_refactor's body; the
+// GPU numeric path of dd_setup calls it with the matrix's own values)
+dd_status refactor_values(dd_ctx *c, const double *vals, bool on_device, cudaStream_t st);
+// the device factor state: W (L blocks, U_ii, U_ij per row in the dropped
+// pattern) and Dinv, for dd_get_factors on the GPU numeric path
+dd_status refactor_fetch(const dd_ctx *c, std::vector<double> &W, std::vector<double> &Dinv);
 
 // ---- solver.cpp
 void prof_free(dd_ctx *c);

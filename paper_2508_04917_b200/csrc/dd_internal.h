@@ -215,7 +215,8 @@ struct dd_ctx {
     double *h_pinned = nullptr;          // small pinned scalars
     int num_sms = 148;
     // --- refactor (dd_refactor) symbolic maps, built when opts.enable_refactor
-    bool refactor = false;
+    bool refactor = false;               // refactor maps built (enable_refactor, or the GPU numeric path)
+    bool gpu_numeric = false;            // dd_setup factors on the device (k_refactor9), host holds no values
     double pivot_floor = 1e-300;
     ddi::uvector<int64_t> Asrc;          // reordered local A_r block -> original block index
     std::vector<int64_t> Wrp;            // A_dd working layout (rank-local rows)

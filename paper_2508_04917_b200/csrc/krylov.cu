@@ -696,8 +696,9 @@ __global__ void k_build_ell(int64_t n_slices, int64_t n_rows, const int64_t *__r
             const bool has = k < len;
             const int64_t slot = slot_ptr[s] + 32 * k;
             cols[slot + lane] = has ? ci[p0 + k] : -1;
+            if (av || !has)  // av null: the values are gathered later (GPU numeric setup), padding zeroed here
 #pragma unroll
-            for (int v = 0; v < B2; ++v) vals[B2 * slot + 32 * v + lane] = has ? av[B2 * (p0 + k) + v] : 0.0;
+                for (int v = 0; v < B2; ++v) vals[B2 * slot + 32 * v + lane] = has ? av[B2 * (p0 + k) + v] : 0.0;
         }
     }
 }

@@ -93,6 +93,22 @@ void refactor_free(dd_ctx *c) {
     delete rf;
     c->rf = nullptr;
 }
+dd_status refactor_values(dd_ctx *c, const double *vals, bool on_device, cudaStream_t st) {
+    return refactor_run(c, vals, on_device ? 1 : 0, st);
+}
+
+dd_status refactor_fetch(const dd_ctx *c, std::vector<double> &W, std::vector<double> &Dinv) {
+    auto *rf = reinterpret_cast<const RfState *>(c->rf);
+    if (!rf) {
+        set_error("factors are not on the device");
+        return DD_E_INVALID_ARG;
+    }
+    W.resize(9 * c->Wsrc.size());
+    Dinv.resize(9 * (size_t)c->n_local);
+    if (!W.empty()) CK(cudaMemcpy(W.data(), rf->W, W.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (!Dinv.empty()) CK(cudaMemcpy(Dinv.data(), rf->Dinv, Dinv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    return DD_OK;
+}
 }  // namespace ddi
 
 extern "C" {
@@ -141,7 +157,7 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     if (*rf->h_bad != ~0ull) {
-        set_error("dd_refactor: singular pivot block (|det| < pivot_floor) at reordered row " +
+        set_error("singular pivot block (|det| < pivot_floor) at reordered row " +
                   std::to_string(*rf->h_bad));
         return DD_E_SINGULAR_PIVOT;
     }

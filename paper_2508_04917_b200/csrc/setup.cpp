@@ -169,8 +169,9 @@ void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
     }
     if (upper) {
         double *dv = reinterpret_cast<double *>(p + off_dinv);
-        for (int v = 0; v < b2; ++v)
-            for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
+        if (rows[0].dinv)  // null: the values come from the device (GPU numeric path)
+            for (int v = 0; v < b2; ++v)
+                for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
         if (mp.Doff)
             for (int t = 0; t < w; ++t) {
                 mp.Doff[rows[t].li] = (int64_t)(base + off_dinv + 8 * (size_t)t);
@@ -181,8 +182,9 @@ void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
     size_t pos = 0;
     for (int k = 0; k < K; ++k) {
         const int ck = cnt[k];
-        for (int v = 0; v < b2; ++v)
-            for (int t = 0; t < ck; ++t) vv[b2 * pos + (size_t)v * ck + t] = rows[t].vals[b2 * (size_t)k + v];
+        if (rows[0].vals)
+            for (int v = 0; v < b2; ++v)
+                for (int t = 0; t < ck; ++t) vv[b2 * pos + (size_t)v * ck + t] = rows[t].vals[b2 * (size_t)k + v];
         int64_t *mo = upper ? mp.Uoff : mp.Loff;
         int32_t *ms = upper ? mp.Ust : mp.Lst;
         if (mo)
@@ -482,8 +484,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     const int64_t nnz_loc = Arp[nl];
     uvector<int32_t> gcol(nnz_loc);  // every entry written below
-    ctx->Av.resize(b2 * nnz_loc);  // every block written below
     ctx->refactor = o->enable_refactor != 0;
+    // GPU numeric path (dd_setup on a device, BSR3, no DD_ILU0 slab): the host
+    // does the symbolic work only -- pattern, levels, slab layout, refactor
+    // maps -- and k_refactor9 computes L, Dinv and U_unit straight into the
+    // slab from the original values; the maps are built
+    const bool gpu_num = ctx->gpu_numeric;
+    if (gpu_num) ctx->refactor = true;
+    if (!gpu_num) ctx->Av.resize(b2 * nnz_loc);  // every block written below (GPU path: values gathered on the device)
     ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
     if (ctx->refactor) ctx->Asrc.resize(nnz_loc);  // every entry written below
 #pragma omp parallel for schedule(static)
@@ -507,7 +515,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         std::sort(ix, ix + nb, [&](int32_t a, int32_t b) { return cc[a] < cc[b]; });
         for (int64_t t = 0; t < nb; ++t) {
             gcol[Arp[li] + t] = cc[ix[t]];
-            std::memcpy(&ctx->Av[b2 * (Arp[li] + t)], &av[b2 * (rp[m] + ix[t])], b2 * sizeof(double));
+            if (!gpu_num) std::memcpy(&ctx->Av[b2 * (Arp[li] + t)], &av[b2 * (rp[m] + ix[t])], b2 * sizeof(double));
             if (ctx->refactor) ctx->Asrc[Arp[li] + t] = rp[m] + ix[t];
         }
     }
@@ -606,12 +614,14 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     ctx->Lci.resize(ctx->Lrp[nl]);
     ctx->Uci.resize(ctx->Urp[nl]);
-    ctx->Lv.resize(b2 * ctx->Lrp[nl]);  // written by the scatter below
-    ctx->Uv.resize(b2 * ctx->Urp[nl]);
+    if (!gpu_num) {
+        ctx->Lv.resize(b2 * ctx->Lrp[nl]);  // written by the scatter below
+        ctx->Uv.resize(b2 * ctx->Urp[nl]);
+    }
     // DD_ILU0 ablation: keep the non-unit U_ij too (a second slab, BSR3 only)
     const bool want_ilu = bs == 3 && (o->variants & DD_ILU0) != 0;
     if (want_ilu) ctx->Uraw.resize(b2 * ctx->Urp[nl]);
-    ctx->Dinv.resize(b2 * nl);
+    if (!gpu_num) ctx->Dinv.resize(b2 * nl);
     ctx->hmapL.assign(nl, 0);
     ctx->hmapU.assign(nl, 0);
 
@@ -638,10 +648,21 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                     const int64_t g = gcol[p];
                     if (g >= a && g < e) {
                         lci.push_back((int32_t)(g - a));
-                        W.insert(W.end(), &ctx->Av[b2 * p], &ctx->Av[b2 * p] + b2);
+                        if (!gpu_num) W.insert(W.end(), &ctx->Av[b2 * p], &ctx->Av[b2 * p] + b2);
                     }
                 }
                 lrp[i + 1] = (int64_t)lci.size();
+            }
+            if (gpu_num) {
+                // pattern only: the values are factored on the device
+                for (int64_t i = 0; i < P; ++i) {
+                    const int64_t li = la + i;
+                    int64_t qL = ctx->Lrp[li], qU = ctx->Urp[li];
+                    for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) {
+                        if (lci[p] < i) ctx->Lci[qL++] = (int32_t)(la + lci[p]);
+                        else if (lci[p] > i) ctx->Uci[qU++] = (int32_t)(la + lci[p]);
+                    }
+                }
             }
             ldg.assign(P, -1);
             for (int64_t i = 0; i < P; ++i)
@@ -649,7 +670,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
                     if (lci[p] == i) ldg[i] = p;
             pos.assign(P, -1);
             bool failed = false;
-            for (int64_t i = 0; i < P && !failed; ++i) {
+            for (int64_t i = 0; i < P && !failed && !gpu_num; ++i) {
                 for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) pos[lci[p]] = p;
                 for (int64_t p = lrp[i]; p < ldg[i]; ++p) {
                     const int64_t k = lci[p];
@@ -669,7 +690,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             }
             if (failed) continue;
             // scatter: L (strictly lower) and U_unit = Dinv_i * U_ij (j > i)
-            for (int64_t i = 0; i < P; ++i) {
+            for (int64_t i = 0; i < P && !gpu_num; ++i) {
                 const int64_t li = la + i;
                 int64_t qL = ctx->Lrp[li], qU = ctx->Urp[li];
                 for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) {
@@ -889,12 +910,13 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             auto rowL = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Lrp[li + 1] - ctx->Lrp[li]), &ctx->Lci[ctx->Lrp[li]],
-                              &ctx->Lv[b2 * ctx->Lrp[li]], nullptr, ctx->Lrp[li], li};
+                              gpu_num ? nullptr : &ctx->Lv[b2 * ctx->Lrp[li]], nullptr, ctx->Lrp[li], li};
             };
             auto rowU = [&](int64_t i) {
                 const int64_t li = la + i;
                 return RowRef{(int32_t)i, (int32_t)(ctx->Urp[li + 1] - ctx->Urp[li]), &ctx->Uci[ctx->Urp[li]],
-                              &Uvals[b2 * ctx->Urp[li]], &ctx->Dinv[b2 * li], ctx->Urp[li], li};
+                              gpu_num ? nullptr : &Uvals[b2 * ctx->Urp[li]], gpu_num ? nullptr : &ctx->Dinv[b2 * li],
+                              ctx->Urp[li], li};
             };
             std::vector<std::vector<RowRef>> gL, gU;
             std::vector<bool> bL, bU;
