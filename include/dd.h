@@ -223,7 +223,9 @@ void dd_destroy(dd_ctx *ctx);
  * dropped layout, every subdomain is factored (block ILU0 -> ILDU0, Alg. 7
  * P:680-711, same arithmetic order as dd_setup, so identical bits) level by
  * level, and L, Dinv and U_unit are written straight into the apply slab; the
- * SpMV operand is refreshed too. Requires dd_opts.enable_refactor = 1.
+ * SpMV operand is refreshed too. Requires dd_opts.enable_refactor = 1 (or a
+ * context that dd_setup already factored on the GPU, which keeps the maps).
+ * Collective when world > 1 (the pivot status is agreed over the ranks).
  * Returns DD_E_SINGULAR_PIVOT (context unusable until a successful refactor)
  * if a pivot block has |det| < pivot_floor. Ordered on `stream`; returns after
  * the pivot check (one synchronisation). */
@@ -264,8 +266,12 @@ dd_status dd_permute(dd_ctx *ctx, const double *v_orig_host, double *v_reord_dev
 dd_status dd_unpermute(dd_ctx *ctx, const double *v_reord_dev, double *v_orig_host,
                        void *stream);
 
-/* Introspection for parity (caller-allocated host arrays). It reports what
- * dd_setup computed on the host (dd_refactor updates only device state). */
+/* Introspection for parity (caller-allocated host arrays). Partition, levels
+ * and patterns are what dd_setup computed on the host. Factor VALUES: on a
+ * device context with 3x3 blocks (and without DD_ILU0) dd_setup factors on
+ * the GPU and dd_get_factors copies the current device
+ * factors back (so after dd_refactor it reports the new ones); host_only,
+ * scalar CSR, DD_ILU0 or DD_HOST_ILU0=1 contexts factor on the host. */
 dd_status dd_get_partition(const dd_ctx *ctx, int32_t *labels /*[N], original order*/,
                            int32_t *new_to_old /*[N]*/);
 /* The Alg. 2 grid and tile dims the partition used (the chosen ones when

@@ -130,7 +130,7 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
         return DD_E_INVALID_ARG;
     }
     if (!c->refactor) {
-        set_error("dd_refactor: context was set up without enable_refactor");
+        set_error("dd_refactor: context was set up without enable_refactor (and factored on the host)");
         return DD_E_INVALID_ARG;
     }
     TRY(refactor_init(c));

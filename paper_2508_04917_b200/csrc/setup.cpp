@@ -114,6 +114,7 @@ struct RowRef {
 struct SlabMaps {
     int64_t *Loff = nullptr, *Uoff = nullptr, *Doff = nullptr;
     int32_t *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
+    bool on = false;  // (Loff / Uoff are null when a triangle has no blocks, e.g. P = 1)
 };
 
 inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -172,7 +173,7 @@ void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
         if (rows[0].dinv)  // null: the values come from the device (GPU numeric path)
             for (int v = 0; v < b2; ++v)
                 for (int t = 0; t < w; ++t) dv[(size_t)v * w + t] = rows[t].dinv[v];
-        if (mp.Doff)
+        if (mp.on)
             for (int t = 0; t < w; ++t) {
                 mp.Doff[rows[t].li] = (int64_t)(base + off_dinv + 8 * (size_t)t);
                 mp.Dst[rows[t].li] = 8 * w;
@@ -187,7 +188,7 @@ void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
                 for (int t = 0; t < ck; ++t) vv[b2 * pos + (size_t)v * ck + t] = rows[t].vals[b2 * (size_t)k + v];
         int64_t *mo = upper ? mp.Uoff : mp.Loff;
         int32_t *ms = upper ? mp.Ust : mp.Lst;
-        if (mo)
+        if (mp.on)
             for (int t = 0; t < ck; ++t) {
                 mo[rows[t].src0 + k] = (int64_t)(base + off_val + 8 * (b2 * pos + (size_t)t));
                 ms[rows[t].src0 + k] = 8 * ck;
@@ -894,7 +895,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         ctx->SlabDoff.resize(nl);
         ctx->SlabDst.resize(nl);
         mp = SlabMaps{ctx->SlabLoff.data(), ctx->SlabUoff.data(), ctx->SlabDoff.data(),
-                      ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data()};
+                      ctx->SlabLst.data(), ctx->SlabUst.data(), ctx->SlabDst.data(), true};
     }
     auto build_slab = [&](ddi::Slab &slab, bool spin, const uvector<double> &Uvals, const SlabMaps &mp) {
         const int rmax = slab.rows_per_rec;
@@ -981,7 +982,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
             int32_t nrec = 0, u_off = 0;
             int64_t mr = 0;
             pack_sub(q, out, mp, nrec, mr, u_off);
-            if (mp.Loff) {  // stream-relative -> slab-absolute offsets
+            if (mp.on) {  // stream-relative -> slab-absolute offsets
                 const int64_t so = slab.info[q].stream_off;
                 for (int64_t li = slab.info[q].row0; li < slab.info[q].row0 + slab.info[q].nrows; ++li) {
                     mp.Doff[li] += so;

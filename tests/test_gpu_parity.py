@@ -232,6 +232,39 @@ def test_refactor_matches_oracle_on_new_values(grid, tiles):
         assert np.array_equal(y.cpu().numpy(), oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], r))
 
 
+@pytest.mark.parametrize("P,host", [(1, "0"), (1, "1"), (7, "0"), (5, "1")])
+def test_refactor_and_gpu_setup_when_a_triangle_is_empty(P, host, monkeypatch):
+    """Regression (round 2): subdomains whose rows have no lower (or upper)
+    blocks -- P = 1 chunks, or a block-diagonal matrix -- leave the L-block
+    scatter map empty; the slab-absolute offsets of the Dinv / U maps must
+    still be applied, or every subdomain's factors land in the first one's
+    stream. Both the GPU-factored setup (host "0") and a host-factored setup
+    re-factored on the GPU (host "1") must equal the oracle bitwise."""
+    import torch
+    monkeypatch.setenv("DD_HOST_ILU0", host)
+    n = 35
+    rng = np.random.default_rng(P)
+    if P == 7:  # block diagonal: no off-diagonal blocks at all
+        rp = np.arange(n + 1, dtype=np.int64)
+        ci = np.arange(n, dtype=np.int32)
+        v = (np.eye(3)[None] * 4 + rng.uniform(-1, 1, (n, 3, 3))).ravel()
+    else:
+        rp, ci, v = random_block_grid(7, 5, 1, seed=P)
+    S = oracle.setup(rp, ci, v, P=P)
+    ctx = dd.dd_setup(rp, ci, v, P=P, enable_refactor=True)
+    r = apply_input(S["n"], seed=3)
+    rd = torch_vec(r)
+    for rnd in range(2):
+        if rnd == 1:
+            ctx.refactor(v)
+        for var in VARIANTS:
+            z = torch.empty_like(rd)
+            ctx.apply(rd, z, var)
+            torch.cuda.synchronize()
+            assert np.array_equal(z.cpu().numpy(), oracle.apply(S, r)), (var, rnd)
+    assert_setup_bitwise(ctx, S)
+
+
 def test_refactor_singular_pivot_and_recovery():
     import torch
     from tests.helpers import kron_blocks
