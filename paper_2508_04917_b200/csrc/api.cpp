@@ -26,6 +26,9 @@ namespace {
 // Host -> device copy of a large pageable buffer through two pinned 32 MB
 // staging buffers: an OpenMP memcpy fills one while the DMA engine drains the
 // other (pageable cudaMemcpy runs at ~3 GB/s; this at ~10-20 GB/s).
+}  // namespace
+
+namespace ddi {
 // Host -> device copy of a large pageable buffer through pinned staging
 // buffers: an OpenMP memcpy fills one while the DMA engine drains the others
 // (pageable cudaMemcpy runs at ~3 GB/s). The staging buffers are pinned once
@@ -95,6 +98,10 @@ dd_status h2d_big(void *dst, const void *src, size_t bytes) {
     if (rc != DD_OK) set_error("dd_setup: host-to-device upload failed");
     return rc;
 }
+
+}  // namespace ddi
+
+namespace {
 
 dd_status upload_slab(Slab &sl) {
     TRY(dmalloc(&sl.d_bytes, sl.bytes.size() + 16));

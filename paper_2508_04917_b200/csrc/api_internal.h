@@ -40,10 +40,13 @@ dd_status dmalloc(T **p, size_t count) {
     return DD_OK;
 }
 
+// host -> device copy of a large pageable buffer through pinned staging (api.cpp)
+dd_status h2d_big(void *dst, const void *src, size_t bytes);
+
 template <class T, class A>
 dd_status upload_vec(T **d, const std::vector<T, A> &h) {
     TRY(dmalloc(d, std::max<size_t>(1, h.size())));
-    if (!h.empty()) CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!h.empty()) TRY(h2d_big(*d, h.data(), h.size() * sizeof(T)));
     return DD_OK;
 }
 

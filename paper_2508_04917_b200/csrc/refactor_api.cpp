@@ -139,7 +139,10 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
     auto *rf = reinterpret_cast<RfState *>(c->rf);
     const double *src = vals;
     if (!on_device) {
-        CK(cudaMemcpyAsync(rf->stage, vals, 9 * c->nnzb_A * sizeof(double), cudaMemcpyHostToDevice, st));
+        // pageable host values: through the pinned staging pipeline (h2d_big),
+        // ordered before the gathers by a stream synchronisation
+        CK(cudaStreamSynchronize(st));
+        TRY(h2d_big(rf->stage, vals, 9 * c->nnzb_A * sizeof(double)));
         src = rf->stage;
     }
     const int grid = c->num_sms * 8;
