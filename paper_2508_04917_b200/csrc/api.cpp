@@ -46,10 +46,18 @@ Staging &staging() {
     return *s;
 }
 
+// Returns with the copy COMPLETE on the device (a pageable cudaMemcpy may
+// return before its DMA lands, and work on non-blocking streams is not
+// ordered after it), so kernels on any stream may read dst afterwards.
 dd_status h2d_big(void *dst, const void *src, size_t bytes) {
     Staging &S = staging();
     if (bytes < 2 * Staging::STG) {
-        CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        CK(e);
         return DD_OK;
     }
     std::lock_guard<std::mutex> lk(S.m);
@@ -61,6 +69,7 @@ dd_status h2d_big(void *dst, const void *src, size_t bytes) {
     }
     if (!S.ready) {
         CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+        CK(cudaDeviceSynchronize());  // (no pinned staging: rare fallback)
         return DD_OK;
     }
     cudaEvent_t ev[Staging::NB] = {nullptr, nullptr, nullptr, nullptr};
@@ -70,7 +79,10 @@ dd_status h2d_big(void *dst, const void *src, size_t bytes) {
     for (int q = 0; q < Staging::NB && ok; ++q) ok = cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
-        rc = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess ? DD_OK : DD_E_CUDA;
+        rc = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess &&
+                     cudaDeviceSynchronize() == cudaSuccess
+                 ? DD_OK
+                 : DD_E_CUDA;
     } else {
         const uint8_t *s8 = reinterpret_cast<const uint8_t *>(src);
         uint8_t *d8 = reinterpret_cast<uint8_t *>(dst);
