@@ -18,7 +18,18 @@ import numpy as np  # noqa: E402
 from inputs.gen import (apply_input, laplacian_bsr3, manufactured_rhs, random_block_grid,  # noqa: E402
                         spe10_style_bsr3)
 
+def _singular_rank1():
+    """random 8x8x4 grid, one diagonal block of the last chunk (rank 1) zeroed"""
+    rp, ci, v = random_block_grid(8, 8, 4, seed=13)
+    v = v.reshape(-1, 3, 3).copy()
+    row = rp.shape[0] - 1 - 5
+    diag = next(p for p in range(rp[row], rp[row + 1]) if ci[p] == row)
+    v[diag] = 0.0
+    return rp, ci, v.reshape(-1)
+
+
 CASES = {
+    "singular_rank1": (_singular_rank1, dict(P=64)),
     "laplace_16^3": (lambda: laplacian_bsr3(16, 16, 16), dict(grid=(16, 16, 16), tiles=(8, 8, 8))),
     "random_8sub": (lambda: random_block_grid(16, 12, 10, seed=21), dict(grid=(16, 12, 10), tiles=(8, 6, 5))),
     "chunks_ragged_oddP": (lambda: random_block_grid(10, 10, 10, seed=5), dict(P=77)),

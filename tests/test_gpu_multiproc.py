@@ -151,3 +151,20 @@ def test_nccl_world2_parity(tmp_path):
     assert np.array_equal(np.concatenate([q["z"] for q in res]), oracle.apply(S, r))
     assert np.array_equal(np.concatenate([q["y"] for q in res]), oracle.spmv(S["rp_r"], S["ci_r"], S["v_r"], r))
     assert res[0]["iterations"] == res[1]["iterations"]
+
+
+def test_ipc_setup_status_agreed(tmp_path):
+    """The same agreement across PROCESSES (DD_COMM_IPC): one rank's singular
+    pivot fails both ranks with DD_E_SINGULAR_PIVOT, neither hangs."""
+    key = os.urandom(128).hex()
+    outs = [str(tmp_path / f"s{q}.npz") for q in range(2)]
+    procs = [subprocess.Popen([sys.executable, WORKER, "singular_rank1", "2", str(q), "ipc", key, outs[q]],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for q in range(2)]
+    try:
+        logs = [p.communicate(timeout=300)[0] for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    res = [dict(np.load(o)) for o in outs]
+    assert [str(q["status"]) for q in res] == ["DD_E_SINGULAR_PIVOT"] * 2, ([str(q.get("msg")) for q in res], logs)

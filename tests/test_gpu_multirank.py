@@ -210,3 +210,33 @@ def test_fused_halo_and_merged_reduction_equal_plain(name, world, monkeypatch):
                 assert np.array_equal(rep0["resid_hist"], rep1["resid_hist"]), (knobs, tol)
                 if knobs != ("0", "0"):
                     assert l1 < l0, (knobs, q, l0, l1)
+
+
+@pytest.mark.parametrize("host", ["0", "1"])
+def test_local_world_setup_status_agreed(host, monkeypatch):
+    """a singular pivot inside ONE rank's subdomains must
+    fail every rank with the same status -- no rank left waiting in a
+    collective its peers never reach. Rank 1 owns the second half of the
+    chunks; one of its diagonal blocks is made singular. Both the GPU
+    factorisation (host "0") and the host ILU0 (host "1") paths."""
+    monkeypatch.setenv("DD_HOST_ILU0", host)
+    rp, ci, v = random_block_grid(8, 8, 4, seed=13)
+    v = v.reshape(-1, 3, 3).copy()
+    n = rp.shape[0] - 1
+    row = n - 5  # in the last chunk (rank 1 of 2, P = 64)
+    diag = next(p for p in range(rp[row], rp[row + 1]) if ci[p] == row)
+    v[diag] = 0.0
+    v = v.reshape(-1)
+    key = os.urandom(128)
+
+    def rank_fn(rank, bar):
+        try:
+            ctx = dd.dd_setup(rp, ci, v, rank=rank, world=2, nccl_id=key, comm="local", P=64)
+            ctx.destroy()
+            return "DD_OK", ""
+        except dd.DDError as e:
+            return e.name, str(e)
+
+    res = run_ranks(2, rank_fn)
+    assert [r[0] for r in res] == ["DD_E_SINGULAR_PIVOT"] * 2, res
+    assert "peer rank" in res[0][1] or "singular" in res[0][1]
