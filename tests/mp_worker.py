@@ -22,7 +22,7 @@ def _singular_rank1():
     """random 8x8x4 grid, one diagonal block of the last chunk (rank 1) zeroed"""
     rp, ci, v = random_block_grid(8, 8, 4, seed=13)
     v = v.reshape(-1, 3, 3).copy()
-    row = rp.shape[0] - 1 - 5
+    row = rp.shape[0] - 1 - 64  # first row of the last chunk: U_ii = A_ii (lower couplings dropped)
     diag = next(p for p in range(rp[row], rp[row + 1]) if ci[p] == row)
     v[diag] = 0.0
     return rp, ci, v.reshape(-1)

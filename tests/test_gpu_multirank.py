@@ -223,7 +223,9 @@ def test_local_world_setup_status_agreed(host, monkeypatch):
     rp, ci, v = random_block_grid(8, 8, 4, seed=13)
     v = v.reshape(-1, 3, 3).copy()
     n = rp.shape[0] - 1
-    row = n - 5  # in the last chunk (rank 1 of 2, P = 64)
+    # the FIRST row of the last chunk (rank 1 of 2, P = 64): its lower
+    # neighbours lie in other chunks and are dropped, so U_ii = A_ii = 0
+    row = n - 64
     diag = next(p for p in range(rp[row], rp[row + 1]) if ci[p] == row)
     v[diag] = 0.0
     v = v.reshape(-1)
