@@ -11,7 +11,7 @@ _held = []
 
 
 def one(rp, ci, v, kw, csr=False):
-    ctx = (dd.dd_setup_csr if csr else dd.dd_setup)(rp, ci, v, variants=7, **kw)
+    ctx = (dd.dd_setup_csr if csr else dd.dd_setup)(rp, ci, v, variants=7 | (0 if csr else dd.DD_ILU0), **kw)
     bs = 1 if csr else 3
     r = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, bs * ctx.n_local)).cuda()
     z = torch.empty_like(r)
@@ -22,6 +22,8 @@ def one(rp, ci, v, kw, csr=False):
             pass
     if os.environ.get("SAN_SPMV", "1") == "1":
         ctx.spmv(r, z)
+    if not csr and os.environ.get("SAN_REFACTOR", "0") == "1":
+        ctx.refactor(torch.from_numpy(v).cuda())  # k_refactor9 (dd_setup already ran it once)
     x = torch.zeros_like(r)
     rep = ctx.bicgstab(r, x, tol=1e-8, max_iter=200)
     torch.cuda.synchronize()
