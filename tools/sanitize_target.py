@@ -11,7 +11,9 @@ _held = []
 
 
 def one(rp, ci, v, kw, csr=False):
-    ctx = (dd.dd_setup_csr if csr else dd.dd_setup)(rp, ci, v, variants=7 | (0 if csr else dd.DD_ILU0), **kw)
+    ctx = (dd.dd_setup_csr if csr else dd.dd_setup)(rp, ci, v, variants=7 | (0 if csr else dd.DD_ILU0),
+                                                     enable_refactor=not csr and os.environ.get("SAN_REFACTOR") == "1",
+                                                     **kw)
     bs = 1 if csr else 3
     r = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, bs * ctx.n_local)).cuda()
     z = torch.empty_like(r)
