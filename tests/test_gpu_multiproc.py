@@ -168,3 +168,22 @@ def test_ipc_setup_status_agreed(tmp_path):
                 p.kill()
     res = [dict(np.load(o)) for o in outs]
     assert [str(q["status"]) for q in res] == ["DD_E_SINGULAR_PIVOT"] * 2, ([str(q.get("msg")) for q in res], logs)
+
+
+def test_ipc_fused_halo_equals_plain_exchange(tmp_path):
+    """The fused halo (rows stored by the apply epilogue into the peer's
+    ghost block over the IPC mapping) against the plain exchange (gather
+    kernel + put) across processes: identical iterates, bitwise."""
+    old = os.environ.get("DD_HALO_FUSE")
+    try:
+        os.environ["DD_HALO_FUSE"] = "0"
+        plain = run_world("random_8sub", 2, "ipc", tmp_path)
+    finally:
+        if old is None:
+            os.environ.pop("DD_HALO_FUSE", None)
+        else:
+            os.environ["DD_HALO_FUSE"] = old
+    fused = run_world("random_8sub", 2, "ipc", tmp_path)
+    for a, b in zip(plain, fused):
+        assert np.array_equal(a["x"], b["x"]) and float(a["iterations"]) == float(b["iterations"])
+        assert np.array_equal(a["hist"], b["hist"])
