@@ -53,6 +53,17 @@
 
 namespace ddk {
 
+#ifdef DD_TRACE
+// development instrumentation (-DDD_TRACE builds only): per-CTA cycle
+// counters of the level-set ring kernel, and a subdomain remap (s -> s % submod)
+// that makes every CTA stream an L2-resident working set
+__device__ unsigned long long g_dd_trace[1024][16];
+__device__ int g_dd_submod;
+#define DD_SUB(s) (g_dd_submod > 0 ? (s) % g_dd_submod : (s))
+#else
+#define DD_SUB(s) (s)
+#endif
+
 using ddi::RecHdr;
 using ddi::SubInfo;
 // consumer threads = rows per record (Slab::rows_per_rec): 128 for 3x3 rows;
@@ -129,6 +140,103 @@ __device__ __forceinline__ void set_bit(uint32_t *bits, uint32_t i) {
 // U_ij and the row's D = U_ii^-1 is applied AFTER its off-diagonal updates
 // ("unlike ILU0 where scaling follows each row's off-diagonal updates",
 // P:823): acc = z_i - sum U_ij x_j, x_i = D acc (orc_apply_ilu0's order).
+#ifndef DD_R7_XFIRST
+#define DD_R7_XFIRST 1
+#endif
+// The branch-free 7-point row (K <= 3 blocks per triangle, DD_PRED): one
+// straight-line instance per triangle (UP), loads issued in dependency order
+// -- the descriptor, then the gathers of x_j it names (the only dependent
+// loads), the own row, the block values and (UP) Dinv -- all before the
+// first FMA. Absent blocks: the descriptor names the zero slot (x = 0.0) and
+// the values come from record bytes 24..31 (cnt[4..7], zero for K <= 3), an
+// exact +0.0 with no select, so fma(-b, x, a) == a bitwise.
+template <bool SPIN, bool UP, bool NU, class Rd>
+__device__ __forceinline__ void rec7(const Rd &rd, const RecHdr &h, const uint4 &c8, int t, double *__restrict__ vec,
+                                     SpinFlags F) {
+    const uint32_t w = h.w;
+    const uint2 d = rd.template ld<uint2>(32u + 8u * t);
+    const uint32_t i = d.x & 0xffffu;
+    const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
+    const uint32_t cnt[3] = {c8.x & 0xffffu, c8.x >> 16, c8.y & 0xffffu};
+    double x[3][3];
+    if constexpr (!SPIN && DD_R7_XFIRST) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) x[k][c] = vec[3 * col[k] + c];
+    }
+    if (SPIN && UP) spin_bit(F.L, i);  // own L result
+    const double z0 = vec[3 * i], z1 = vec[3 * i + 1], z2 = vec[3 * i + 2];
+    double b[3][9];
+    uint32_t pre = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const bool ok = (uint32_t)t < cnt[k];
+        const uint32_t vb = ok ? h.off_val + 72u * pre + 8u * t : 24u, st = ok ? 8u * cnt[k] : 0u;
+#pragma unroll
+        for (int v = 0; v < 9; ++v) b[k][v] = rd.template ld<double>(vb + st * v);
+        pre += cnt[k];
+    }
+    double D[9];
+    if constexpr (UP) {
+        const uint32_t off_dinv = (47u + 8u * w) & ~15u;  // rec_off_dinv(K <= 3, w)
+#pragma unroll
+        for (int v = 0; v < 9; ++v) D[v] = rd.template ld<double>(off_dinv + 8u * (v * w + t));
+    }
+    if constexpr (SPIN || !DD_R7_XFIRST) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (SPIN && (uint32_t)t < cnt[k]) spin_bit(UP ? F.U : F.L, col[k]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) x[k][c] = vec[3 * col[k] + c];
+        }
+    }
+    double a0, a1, a2;
+    if (UP && !NU) {
+        a0 = D[0] * z0;
+        a0 = __fma_rn(D[1], z1, a0);
+        a0 = __fma_rn(D[2], z2, a0);
+        a1 = D[3] * z0;
+        a1 = __fma_rn(D[4], z1, a1);
+        a1 = __fma_rn(D[5], z2, a1);
+        a2 = D[6] * z0;
+        a2 = __fma_rn(D[7], z1, a2);
+        a2 = __fma_rn(D[8], z2, a2);
+    } else {
+        a0 = z0;
+        a1 = z1;
+        a2 = z2;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a0 = __fma_rn(-b[k][0], x[k][0], a0);
+        a0 = __fma_rn(-b[k][1], x[k][1], a0);
+        a0 = __fma_rn(-b[k][2], x[k][2], a0);
+        a1 = __fma_rn(-b[k][3], x[k][0], a1);
+        a1 = __fma_rn(-b[k][4], x[k][1], a1);
+        a1 = __fma_rn(-b[k][5], x[k][2], a1);
+        a2 = __fma_rn(-b[k][6], x[k][0], a2);
+        a2 = __fma_rn(-b[k][7], x[k][1], a2);
+        a2 = __fma_rn(-b[k][8], x[k][2], a2);
+    }
+    if (UP && NU) {
+        const double q0 = a0, q1 = a1, q2 = a2;
+        a0 = D[0] * q0;
+        a0 = __fma_rn(D[1], q1, a0);
+        a0 = __fma_rn(D[2], q2, a0);
+        a1 = D[3] * q0;
+        a1 = __fma_rn(D[4], q1, a1);
+        a1 = __fma_rn(D[5], q2, a1);
+        a2 = D[6] * q0;
+        a2 = __fma_rn(D[7], q1, a2);
+        a2 = __fma_rn(D[8], q2, a2);
+    }
+    vec[3 * i] = a0;
+    vec[3 * i + 1] = a1;
+    vec[3 * i + 2] = a2;
+    if (SPIN) set_bit(UP ? F.U : F.L, i);
+}
+
 template <bool SPIN, int GEN, class Rd, bool NU = false>
 __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, const uint4 &c8, int t,
                                                 double *__restrict__ vec, SpinFlags F) {
@@ -138,23 +246,35 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
+#if DD_PRED
     if (GEN == 0 || K <= 3) {
-        const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
+        if (upper)
+            rec7<SPIN, true, NU>(rd, h, c8, t, vec, F);
+        else
+            rec7<SPIN, false, NU>(rd, h, c8, t, vec, F);
+        return;
+    }
+#endif
+    if (GEN == 0 || K <= 3) {
+        // K <= 3: the descriptors start at byte 32, Dinv after them at a
+        // 16-byte boundary, and cnt[k] is 0 for k >= K (zeroed count area)
+        const uint2 d = rd.template ld<uint2>(32u + 8u * t);
         const uint32_t i = d.x & 0xffffu;
         const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
-        const uint32_t cnt[3] = {K > 0 ? (c8.x & 0xffffu) : 0u, K > 1 ? (c8.x >> 16) : 0u, K > 2 ? (c8.y & 0xffffu) : 0u};
+        const uint32_t cnt[3] = {c8.x & 0xffffu, c8.x >> 16, c8.y & 0xffffu};
+        const uint32_t off_dinv = (47u + 8u * w) & ~15u;
         double b[3][9];
         uint32_t pre = 0;
 #if DD_PRED
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
+            // absent block: nine loads of record bytes 24..31 (cnt[4..7], zero
+            // for K <= 3), an exact +0.0 -- no select, and the negation folds
+            // into the DFMA
             const bool ok = (uint32_t)t < cnt[k];
-            const uint32_t vb = ok ? off_val + 72u * pre + 8u * t : 0u, st = ok ? 8u * cnt[k] : 0u;
+            const uint32_t vb = ok ? off_val + 72u * pre + 8u * t : 24u, st = ok ? 8u * cnt[k] : 0u;
 #pragma unroll
-            for (int v = 0; v < 9; ++v) {
-                const double q = rd.template ld<double>(vb + st * v);
-                b[k][v] = ok ? q : 0.0;
-            }
+            for (int v = 0; v < 9; ++v) b[k][v] = rd.template ld<double>(vb + st * v);
             pre += cnt[k];
         }
 #else
@@ -199,11 +319,11 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         for (int k = 0; k < 3; ++k) {
 #if DD_PRED
             {
-                const bool ok = (uint32_t)t < cnt[k];
-                const uint32_t j = ok ? col[k] : i;
-                if (SPIN && ok) spin_bit(upper ? F.U : F.L, j);
-                const double y0 = vec[3 * j], y1 = vec[3 * j + 1], y2 = vec[3 * j + 2];
-                const double x0 = ok ? y0 : 0.0, x1 = ok ? y1 : 0.0, x2 = ok ? y2 : 0.0;
+                // absent block: the descriptor names the zero slot (x = 0.0,
+                // b = +0.0: fma(-0, 0, a) == a for every a)
+                const uint32_t j = col[k];
+                if (SPIN && (uint32_t)t < cnt[k]) spin_bit(upper ? F.U : F.L, j);
+                const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
 #else
             if ((uint32_t)t < cnt[k]) {
                 const uint32_t j = col[k];
@@ -685,6 +805,7 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
         const int nd = BS * si.nrows;
         const double *rs = r + BS * (int64_t)si.row0;
         for (int q = t; q < nd; q += TCB<BS>) vec[vslot<BS>(sw, q)] = __ldg(rs + q);
+        if (t < BS) vec[BS * sw.zslot + t] = 0.0;  // the zero slot
         __syncthreads();
         uint32_t ro = 0;
         while (ro < sz) {
@@ -721,6 +842,12 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 // -------------------------------------------------------------------- ring
 #ifndef DD_CH_DIV
 #define DD_CH_DIV 4  // ring chunk = RING / DD_CH_DIV
+#endif
+// r slice of each subdomain: 1 = consumers load it from global memory (the
+// producer prefetches it into L2 when it starts streaming the subdomain's
+// records), 0 = through the ring ahead of the records (round-1/2 form)
+#ifndef DD_RFILL_G
+#define DD_RFILL_G 0
 #endif
 #ifndef DD_PF_AHEAD
 #define DD_PF_AHEAD -1  // L2 prefetch distance of the ring producer: -1 = half a ring, 0 = off, else bytes
@@ -766,6 +893,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     if (SPIN) {
         for (uint32_t q = tid; q < 2 * fw; q += TC + 32) F.L[q] = 0u;
     }
+    if (tid < BS) vec[BS * sw.zslot + tid] = 0.0;  // the zero slot (never overwritten)
     __syncthreads();
 
     if (tid >= TC) {
@@ -773,11 +901,20 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         if (tid == TC) {
             const uint64_t pol = policy_evict_first();
             uint32_t g = 0;
+#ifdef DD_TRACE
+            long long tr_pw = 0;
+            const long long tr_p0 = clock64();
+#endif
             for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
-                const SubInfo si = info[s];
+                const SubInfo si = info[DD_SUB(s)];
                 const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
                 const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
+#if DD_RFILL_G
+                const uint32_t rb = 0u;  // r is not in the ring: prefetch it for the consumers
+                prefetch_l2(reinterpret_cast<const uint8_t *>(r) + rlo, (uint32_t)(rhi - rlo));
+#else
                 const uint32_t rb = (uint32_t)(rhi - rlo);
+#endif
                 // phase 0: the whole stream; 1: the L section; 2: the D+U section
                 const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
                 const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
@@ -795,10 +932,10 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 // the prefetched lines are evicted before use (457 us; 512 KB:
                 // 582 us).
                 auto pf_sub = [&](int ss, uint32_t a, uint32_t b) {
-                    const SubInfo sj = info[ss];
+                    const SubInfo sj = info[DD_SUB(ss)];
                     const int64_t jlo = (8 * BS * (int64_t)sj.row0) & ~(int64_t)15;
                     const int64_t jhi = (8 * BS * ((int64_t)sj.row0 + sj.nrows) + 15) & ~(int64_t)15;
-                    const uint32_t jrb = (uint32_t)(jhi - jlo);
+                    const uint32_t jrb = DD_RFILL_G ? 0u : (uint32_t)(jhi - jlo);
                     const uint32_t jsl = phase == 2 ? (uint32_t)sj.u_off : 0u;
                     const uint32_t jsh = phase == 1 ? (uint32_t)sj.u_off : (uint32_t)sj.stream_bytes;
                     b = min(b, jrb + (jsh - jsl));
@@ -817,7 +954,13 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                         if (b > total && s + (int)gridDim.x < n_sub)
                             pf_sub(s + gridDim.x, a > total ? a - total : 0u, b - total);
                     }
+#ifdef DD_TRACE
+                    const long long tw0 = clock64();
+#endif
                     if (g >= NST) mbar_wait(&empty[st], ((g / NST) - 1u) & 1u);
+#ifdef DD_TRACE
+                    tr_pw += clock64() - tw0;
+#endif
                     const uint32_t lo = c * CH, hi = min(total, lo + CH);
                     mbar_arrive_expect_tx(&full[st], hi - lo);
                     uint8_t *dst = ring + st * CH;
@@ -828,6 +971,12 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                     }
                 }
             }
+#ifdef DD_TRACE
+            if (!SPIN && MODE == AM_VC) {
+                atomicAdd(&g_dd_trace[blockIdx.x & 1023][8], (unsigned long long)tr_pw);
+                atomicAdd(&g_dd_trace[blockIdx.x & 1023][9], (unsigned long long)(clock64() - tr_p0));
+            }
+#endif
         }
         return;
     }
@@ -838,11 +987,28 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     uint32_t gbase = 0;     // chunk index at which the current subdomain starts
     uint32_t ready = 0;     // chunks this thread has seen full
     uint32_t released = 0;  // chunks handed back (SPIN: each warp's lane 0; else t == TC - 32)
+#ifdef DD_TRACE
+    // [0] r fill, [1] L records, [2] U records, [3] z store + halo, [4] full
+    // waits, [5] record barriers, [6] subdomains, [7] records
+    long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long trc = clock64();
+    auto tmark = [&](int k) {
+        const long long c = clock64();
+        tr[k] += c - trc;
+        trc = c;
+    };
+#endif
     auto ensure = [&](uint32_t chunk) {
+#ifdef DD_TRACE
+        const long long w0 = clock64();
+#endif
         while (ready <= chunk) {
             mbar_wait(&full[ready % NST], (ready / NST) & 1u);
             ++ready;
         }
+#ifdef DD_TRACE
+        tr[4] += clock64() - w0;
+#endif
     };
     auto release_to = [&](uint32_t upto) {
         // level set: lane 0 of the LAST consumer warp hands chunks back -- its
@@ -855,11 +1021,23 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             }
         }
     };
+#if DD_RFILL_G == 2
+    // r slice of subdomain ss -> vec with per-thread async copies (thread t:
+    // entries q = t mod TC, the ones it stored to z for the previous
+    // subdomain), issued as soon as the vector is free
+    auto r_issue = [&](int ss) {
+        const SubInfo sj = info[DD_SUB(ss)];
+        const double *rs = r + BS * (int64_t)sj.row0;
+        const uint32_t ndj = (uint32_t)BS * sj.nrows;
+        for (uint32_t q = t; q < ndj; q += TC) cp_async8(vec + vslot<BS>(sw, q), rs + q);
+    };
+    if ((int)blockIdx.x < n_sub) r_issue(blockIdx.x);
+#endif
     for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
-        const SubInfo si = info[s];
+        const SubInfo si = info[DD_SUB(s)];
         const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
         const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
-        const uint32_t rb = (uint32_t)(rhi - rlo);
+        const uint32_t rb = DD_RFILL_G ? 0u : (uint32_t)(rhi - rlo);
         const uint32_t shift = (uint32_t)(8 * BS * (int64_t)si.row0 - rlo);
         const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
         const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
@@ -867,6 +1045,33 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         const uint32_t nch = (total + CH - 1) / CH;
         const uint32_t nd = (uint32_t)BS * si.nrows;
         const uint32_t abs0 = gbase * CH;
+#ifdef DD_TRACE
+        trc = clock64();
+        tr[6] += 1;
+        bool tr_in_u = false;
+#endif
+#if DD_RFILL_G == 2
+        cp_async_wait_all();  // this thread's share of the r slice (issued below)
+        (void)shift;
+#elif DD_RFILL_G
+        // ---- r slice: global (L2-prefetched by the producer) -> vec; thread t
+        // fills the entries q = t (mod TC) -- the ones it stored to z for the
+        // previous subdomain -- so no barrier is needed between that store and
+        // this fill. Loads in batches of 8 (all in flight before the stores).
+        {
+            const double *rs = r + BS * (int64_t)si.row0;
+            uint32_t q = t;
+            for (; q + 7u * TC < nd; q += 8u * TC) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(rs + q + u * TC);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) vec[vslot<BS>(sw, q + u * TC)] = v[u];
+            }
+            for (; q < nd; q += TC) vec[vslot<BS>(sw, q)] = __ldg(rs + q);
+        }
+        (void)shift;
+#endif
         // ---- r slice: ring -> vec, chunk by chunk
         const uint32_t nrc = (rb + CH - 1) / CH;
         for (uint32_t c = 0; c < nrc; ++c) {
@@ -889,6 +1094,9 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             for (uint32_t q = t; q < 2 * fw; q += TC) F.L[q] = 0u;
         named_bar_sync(1, TC);
         release_to(gbase + rb / CH);
+#ifdef DD_TRACE
+        tmark(0);
+#endif
         // ---- records
         uint32_t ro = rb;
         while (true) {
@@ -905,6 +1113,13 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             // L level 0 carries no blocks (z_i = r_i in place): the level set
             // skips it (no work, no barrier); the sync-free sweep publishes flags
             const bool skip = !SPIN && !upper && h.K == 0 && !last;
+#ifdef DD_TRACE
+            if (upper && !tr_in_u) {
+                tmark(1);
+                tr_in_u = true;
+            }
+            tr[7] += 1;
+#endif
             if (mode == 1 || skip) {
             } else if constexpr (MODE == AM_TREE && BS == 3) {
                 if (pos + h.bytes <= RING)
@@ -934,11 +1149,20 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 // a skipped record needs no barrier for the sweep, but when it
                 // ends in a later chunk than it started, the chunk handed back
                 // below may hold headers a lagging warp has not read yet
+#ifdef DD_TRACE
+                const long long b0 = clock64();
+#endif
                 named_bar_sync(1, TC);
+#ifdef DD_TRACE
+                tr[5] += clock64() - b0;
+#endif
             }
             if (last) {
                 if (SPIN) named_bar_sync(1, TC);  // every row final before z is stored
                 release_to(gbase + nch);
+#ifdef DD_TRACE
+                tmark(2);
+#endif
                 break;
             }
             release_to(gbase + ro / CH);
@@ -964,8 +1188,25 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 named_bar_sync(1, TC);
             }
         }
+#if DD_RFILL_G == 2
+        if (s + (int)gridDim.x < n_sub) r_issue(s + gridDim.x);
+#endif
         gbase += nch;
+#ifdef DD_TRACE
+        tmark(3);
+#endif
     }
+#ifdef DD_TRACE
+    if (!SPIN && MODE == AM_VC) {
+        unsigned long long *o = g_dd_trace[blockIdx.x & 1023];
+        if (t == 0)
+            for (int k = 0; k < 8; ++k) atomicAdd(o + k, (unsigned long long)tr[k]);
+        if (t == TC - 32) {  // the releasing (lightest) warp
+            atomicAdd(o + 10, (unsigned long long)tr[5]);
+            atomicAdd(o + 11, (unsigned long long)tr[4]);
+        }
+    }
+#endif
 }
 
 // ------------------------------------------------------------ host side
@@ -1185,6 +1426,20 @@ int tile_slots(int device, int bs, int P, int *per_sm) {
     if (per_sm) *per_sm = best;
     return sms * best;
 }
+
+#ifdef DD_TRACE
+}  // namespace ddi
+extern "C" int dd_debug_trace(unsigned long long *host, int reset, int submod) {
+    if (host && cudaMemcpyFromSymbol(host, ddk::g_dd_trace, sizeof(ddk::g_dd_trace)) != cudaSuccess) return -1;
+    if (reset) {
+        static unsigned long long zero[1024][16];
+        if (cudaMemcpyToSymbol(ddk::g_dd_trace, zero, sizeof(zero)) != cudaSuccess) return -1;
+    }
+    if (submod >= 0 && cudaMemcpyToSymbol(ddk::g_dd_submod, &submod, sizeof(int)) != cudaSuccess) return -1;
+    return 0;
+}
+namespace ddi {
+#endif
 
 dd_status apply_launch(dd_ctx *ctx, int variant, const double *r, double *z, void *stream, const int *skip,
                        const HaloOut *halo) {

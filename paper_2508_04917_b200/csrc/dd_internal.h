@@ -87,7 +87,10 @@ struct RecHdr {
 };
 // descriptor width and offsets (shared by the packer and the kernels)
 inline __host__ __device__ uint32_t rec_dw(uint32_t K) { return K <= 3 ? 8u : ((2u * (1u + K) + 15u) & ~15u); }
-inline __host__ __device__ uint32_t rec_off_desc(uint32_t K) { return 16u + ((2u * K + 15u) & ~15u); }
+// the count area is at least 16 bytes (also for K = 0): bytes 24..31 of a
+// record with K <= 3 are then always zero (cnt[4..7]), the kernels' source
+// of an exact 0.0 for the absent blocks of the branch-free 7-point path
+inline __host__ __device__ uint32_t rec_off_desc(uint32_t K) { return 32u + (K > 8u ? ((2u * K - 1u) & ~15u) : 0u); }
 inline __host__ __device__ uint32_t rec_off_dinv(uint32_t K, uint32_t w) {
     return (rec_off_desc(K) + rec_dw(K) * w + 15u) & ~15u;
 }
@@ -144,6 +147,10 @@ struct HaloOut {
 // element q = bs*i + c to bs*slot(i) + c.
 struct Swz {
     uint32_t s1 = 31, p1 = 0, s2 = 31, p2 = 0;
+    // the zero slot: one vector slot past the rows that holds 0.0 (the
+    // kernels write it once); the descriptors name it for absent blocks, so
+    // the branch-free 7-point path gathers an exact zero without a select
+    uint32_t zslot = 0xFFFFu;
     __host__ __device__ uint32_t slot(uint32_t i) const { return i + (i >> s1) * p1 + (i >> s2) * p2; }
 };
 

@@ -163,7 +163,8 @@ void put_record(Sink &out, const std::vector<RowRef> &rows, bool upper,
     }
     for (int t = 0; t < w; ++t) {
         uint16_t *d = reinterpret_cast<uint16_t *>(p + off_desc + dw * t);
-        for (size_t q = 0; q < dw / 2; ++q) d[q] = 0xFFFF;
+        // absent blocks name the zero slot (Swz::zslot)
+        for (size_t q = 0; q < dw / 2; ++q) d[q] = (uint16_t)sw.zslot;
         // shared-vector slots (Swz), not rows: the kernels index the vector directly
         d[0] = (uint16_t)sw.slot((uint32_t)rows[t].row);
         for (int k = 0; k < rows[t].nblk; ++k) d[1 + k] = (uint16_t)sw.slot((uint32_t)(rows[t].cols[k] - col_base));
@@ -272,8 +273,9 @@ int64_t bank_cost(const dd_ctx *ctx, int64_t la, int64_t P, int rmax, const Swz 
                     for (int c = 0; c < 3; ++c) {
                         for (int q = 0; q < n; ++q) {
                             const int64_t i = rows[w0 + q], li = la + i;
-                            const int64_t j = k < rp[li + 1] - rp[li] ? cl[rp[li] + k] - la : i;
-                            word[q] = 2u * (3u * sw.slot((uint32_t)j) + c);
+                            // absent blocks read the zero slot (a broadcast)
+                            word[q] = k < rp[li + 1] - rp[li] ? 2u * (3u * sw.slot((uint32_t)(cl[rp[li] + k] - la)) + c)
+                                                              : 2u * (3u * (uint32_t)(P + 16) + c);
                         }
                         cost += wave(word, n);
                     }
@@ -292,8 +294,16 @@ int64_t bank_cost(const dd_ctx *ctx, int64_t la, int64_t P, int rmax, const Swz 
 void choose_swizzle(dd_ctx *ctx, int64_t r0) {
     ctx->swz = Swz{};
     ctx->vec_rows = ctx->max_P;
+    // one slot past the rows holds 0.0 (Swz::zslot)
+    auto add_zero_slot = [ctx] {
+        ctx->swz.zslot = (uint32_t)ctx->vec_rows;
+        ctx->vec_rows += 1;
+    };
     const char *e = getenv("DD_SWZ");
-    if (ctx->bs != 3 || ctx->max_P <= 0 || (e && atoi(e) == 0)) return;
+    if (ctx->bs != 3 || ctx->max_P <= 0 || (e && atoi(e) == 0)) {
+        add_zero_slot();
+        return;
+    }
     const int nsl = ctx->sub_last - ctx->sub_first;
     std::vector<Swz> cands{Swz{}};
     for (uint32_t s1 = 4; s1 <= 9; ++s1)
@@ -320,6 +330,7 @@ void choose_swizzle(dd_ctx *ctx, int64_t r0) {
     if (cost[best] * 20 >= cost[0] * 19) best = 0;
     ctx->swz = cands[best];
     ctx->vec_rows = (int32_t)ctx->swz.slot((uint32_t)ctx->max_P - 1) + 1;
+    add_zero_slot();
 }
 
 // ------------------------------------------------------------ host setup

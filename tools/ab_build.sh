@@ -5,4 +5,4 @@ set -e
 name=$1; shift
 DD_NVCC_DEFS="$*" python -m paper_2508_04917_b200.build --force > /dev/null
 mkdir -p exp; cp paper_2508_04917_b200/libdd.so exp/$name.so
-grep -A4 "k_apply_ringILi3ELj65536ELj16384ELb0ELi0E" paper_2508_04917_b200/build/ptxas.log | grep -E "registers" | sed "s/^/$name: /"
+grep -A4 "k_apply_ringILi3ELj65536ELj16384ELb0ELi0ELi0E" paper_2508_04917_b200/build/ptxas.log | grep -E "registers" | sed "s/^/$name: /"
