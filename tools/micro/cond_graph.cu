@@ -10,6 +10,17 @@ __global__ void body(int *ctl, double *v, int n) {
 __global__ void head(int *ctl) { ctl[0] += 1; }
 __global__ void tail(int *ctl, cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, ctl[0] < ctl[1] ? 1u : 0u); }
 
+struct Held {
+    cudaGraphExec_t ge;
+    cudaGraph_t g;
+    cudaStream_t st, cap;
+    int *ctl;
+    double *v;
+};
+static Held held[4];
+static int nheld = 0;
+static bool keep = false;
+
 static int run(int n, int iters) {
     int *ctl;
     double *v;
@@ -45,6 +56,10 @@ static int run(int n, int iters) {
     double v0 = 0;
     cudaMemcpy(&v0, v, sizeof(double), cudaMemcpyDeviceToHost);
     printf("n=%d iters=%d v[0]=%g status=%s\n", n, iters, v0, cudaGetErrorString(e));
+    if (keep) {  // the first "context" stays alive while the next ones run
+        held[nheld++] = Held{ge, g, st, cap, ctl, v};
+        return e == cudaSuccess ? 0 : 1;
+    }
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
     cudaStreamDestroy(cap);
@@ -54,7 +69,8 @@ static int run(int n, int iters) {
     return e == cudaSuccess ? 0 : 1;
 }
 
-int main() {
+int main(int argc, char **argv) {
+    keep = argc > 1 && argv[1][0] == 'k';
     int rc = run(2880, 5);
     rc |= run(3000, 6);
     rc |= run(3000, 6);
