@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "dd_internal.h"
 #include "ptx.cuh"
@@ -247,7 +248,10 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
 #if DD_PRED
-    if (GEN == 0 || K <= 3) {
+    // ring readers: the per-triangle instance; the direct ablation (GlobalRd,
+    // values straight from HBM/L2) keeps the one-instance form below, whose
+    // schedule issues the value loads first (rec7 there: 461 -> 712 us)
+    if (!std::is_same<Rd, GlobalRd>::value && (GEN == 0 || K <= 3)) {
         if (upper)
             rec7<SPIN, true, NU>(rd, h, c8, t, vec, F);
         else
@@ -255,6 +259,7 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         return;
     }
 #endif
+    constexpr bool SEL = std::is_same<Rd, GlobalRd>::value;
     if (GEN == 0 || K <= 3) {
         // K <= 3: the descriptors start at byte 32, Dinv after them at a
         // 16-byte boundary, and cnt[k] is 0 for k >= K (zeroed count area)
@@ -270,11 +275,16 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
         for (int k = 0; k < 3; ++k) {
             // absent block: nine loads of record bytes 24..31 (cnt[4..7], zero
             // for K <= 3), an exact +0.0 -- no select, and the negation folds
-            // into the DFMA
+            // into the DFMA. The direct ablation (GlobalRd) keeps the round-1
+            // selects: without them ptxas schedules its global loads worse
+            // (474 -> 616 us at config 3)
             const bool ok = (uint32_t)t < cnt[k];
-            const uint32_t vb = ok ? off_val + 72u * pre + 8u * t : 24u, st = ok ? 8u * cnt[k] : 0u;
+            const uint32_t vb = ok ? off_val + 72u * pre + 8u * t : (SEL ? 0u : 24u), st = ok ? 8u * cnt[k] : 0u;
 #pragma unroll
-            for (int v = 0; v < 9; ++v) b[k][v] = rd.template ld<double>(vb + st * v);
+            for (int v = 0; v < 9; ++v) {
+                const double q = rd.template ld<double>(vb + st * v);
+                b[k][v] = SEL ? (ok ? q : 0.0) : q;
+            }
             pre += cnt[k];
         }
 #else
@@ -321,9 +331,11 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
             {
                 // absent block: the descriptor names the zero slot (x = 0.0,
                 // b = +0.0: fma(-0, 0, a) == a for every a)
-                const uint32_t j = col[k];
-                if (SPIN && (uint32_t)t < cnt[k]) spin_bit(upper ? F.U : F.L, j);
-                const double x0 = vec[3 * j], x1 = vec[3 * j + 1], x2 = vec[3 * j + 2];
+                const bool ok = (uint32_t)t < cnt[k];
+                const uint32_t j = SEL && !ok ? i : col[k];
+                if (SPIN && ok) spin_bit(upper ? F.U : F.L, j);
+                const double y0 = vec[3 * j], y1 = vec[3 * j + 1], y2 = vec[3 * j + 2];
+                const double x0 = SEL && !ok ? 0.0 : y0, x1 = SEL && !ok ? 0.0 : y1, x2 = SEL && !ok ? 0.0 : y2;
 #else
             if ((uint32_t)t < cnt[k]) {
                 const uint32_t j = col[k];
