@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -22,6 +23,7 @@ struct RfState {
             *UpdT = nullptr, *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
     int64_t *Wrp = nullptr, *Wdiag = nullptr, *Uptr = nullptr, *Lrp = nullptr, *Urp = nullptr, *Loff = nullptr,
             *Uoff = nullptr, *Doff = nullptr, *Wsrc = nullptr, *Esrc = nullptr;
+    int32_t *plan = nullptr;  // row plans of k_refactor_diag (null: k_refactor9)
     double *W = nullptr, *Dinv = nullptr, *stage = nullptr;
     unsigned long long *bad = nullptr;
     unsigned long long *h_bad = nullptr;
@@ -51,6 +53,39 @@ dd_status refactor_init(dd_ctx *c) {
     TRY(upload_vec(&rf->Uoff, c->SlabUoff));
     TRY(upload_vec(&rf->Doff, c->SlabDoff));
     TRY(upload_vec(&rf->Wsrc, c->Wsrc));
+    // diagonal-update class (refactor.cu, k_refactor_diag): <= 3 lower blocks
+    // per row, each with at most one update, on the row's diagonal block
+    {
+        const int64_t nr = (int64_t)c->LevRows.size();
+        std::vector<int32_t> plan((size_t)12 * nr, 0);
+        int fits = (c->Lrp.empty() || c->Lrp.back() < INT32_MAX) && (c->Urp.empty() || c->Urp.back() < INT32_MAX);
+#pragma omp parallel for schedule(static) reduction(&& : fits)
+        for (int64_t idx = 0; idx < nr; ++idx) {
+            int32_t *P = plan.data() + (size_t)12 * idx;
+            const int64_t li = c->LevRows[idx], w0 = c->Wrp[li], dpos = c->Wdiag[li] - w0;
+            bool ok = dpos <= 3;
+            int32_t upd = 0;
+            for (int64_t jp = 0; ok && jp < dpos; ++jp) {
+                const int64_t p = w0 + jp, nu = c->Uptr[p + 1] - c->Uptr[p];
+                P[4 + jp] = c->Wcol[p];
+                P[7 + jp] = -1;
+                if (nu > 1 || (nu == 1 && c->UpdT[c->Uptr[p]] != c->Wdiag[li])) ok = false;
+                if (nu == 1) {
+                    P[7 + jp] = c->UpdQ[c->Uptr[p]];
+                    upd |= 1 << jp;
+                }
+            }
+            P[0] = (int32_t)li;
+            P[1] = (int32_t)w0;
+            P[2] = (int32_t)(dpos | upd << 8);
+            P[3] = (int32_t)c->Lrp[li];
+            P[10] = (int32_t)c->Urp[li];
+            P[11] = (int32_t)(c->Wrp[li + 1] - w0);
+            fits = fits && ok;
+        }
+        static const bool force = getenv("DD_REFACTOR_KERNEL") != nullptr;
+        if (fits && !force) TRY(upload_vec(&rf->plan, plan));
+    }
     // sliced-ELL slot -> original block index (-1 = padding), same layout as device_setup
     {
         const int64_t nl = c->n_local;
@@ -87,7 +122,7 @@ void refactor_free(dd_ctx *c) {
                     (void *)rf->UpdT, (void *)rf->Lst, (void *)rf->Ust, (void *)rf->Dst, (void *)rf->Wrp,
                     (void *)rf->Wdiag, (void *)rf->Uptr, (void *)rf->Lrp, (void *)rf->Urp, (void *)rf->Loff,
                     (void *)rf->Uoff, (void *)rf->Doff, (void *)rf->Wsrc, (void *)rf->Esrc, (void *)rf->W,
-                    (void *)rf->Dinv, (void *)rf->stage, (void *)rf->bad})
+                    (void *)rf->Dinv, (void *)rf->stage, (void *)rf->bad, (void *)rf->plan})
         cudaFree(p);
     cudaFreeHost(rf->h_bad);
     delete rf;
@@ -154,7 +189,12 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
                   rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes, rf->Loff, rf->Uoff, rf->Doff,
                   rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad, c->row_first};
     const int nsl = c->sub_last - c->sub_first;
-    if (nsl > 0) ddk::launch_refactor(nsl, a, st);
+    if (nsl > 0) {
+        if (rf->plan)
+            ddk::launch_refactor_diag(nsl, a, rf->plan, st);
+        else
+            ddk::launch_refactor(nsl, a, st);
+    }
     c->n_launches += 3;
     CK(cudaMemcpyAsync(rf->h_bad, rf->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
