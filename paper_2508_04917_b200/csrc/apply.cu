@@ -48,6 +48,10 @@
 #endif
 // The same inside each group of three of the general-K path (27-point rows):
 // 27-point 96^3, P 2048: level set 723 -> 620 us, direct 713 -> 560 us.
+// the same for scalar CSR rows (rec1); 0 keeps their branching form
+#ifndef DD_PRED1
+#define DD_PRED1 1
+#endif
 #ifndef DD_PRED_GEN
 #define DD_PRED_GEN 1
 #endif
@@ -516,6 +520,46 @@ __device__ __forceinline__ void process_record3(const Rd &rd, const RecHdr &h, c
     }
 }
 
+// The scalar row with K <= 3 blocks per triangle, branch-free (ring readers):
+// absent blocks read the zero slot (x = 0.0) and the zero count bytes 24..31
+// (b = +0.0), as in rec7; one straight-line instance per triangle.
+template <bool SPIN, bool UP, class Rd>
+__device__ __forceinline__ void rec1(const Rd &rd, const RecHdr &h, const uint4 &c8, int t, double *__restrict__ vec,
+                                     SpinFlags F) {
+    const uint32_t w = h.w;
+    const uint2 d = rd.template ld<uint2>(32u + 8u * t);
+    const uint32_t i = d.x & 0xffffu;
+    const uint32_t col[3] = {d.x >> 16, d.y & 0xffffu, d.y >> 16};
+    const uint32_t cnt[3] = {c8.x & 0xffffu, c8.x >> 16, c8.y & 0xffffu};
+    double x[3];
+    if constexpr (!SPIN) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[k] = vec[col[k]];
+    }
+    if (SPIN && UP) spin_bit(F.L, i);
+    const double z = vec[i];
+    double b[3];
+    uint32_t pre = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        b[k] = rd.template ld<double>((uint32_t)t < cnt[k] ? h.off_val + 8u * (pre + t) : 24u);
+        pre += cnt[k];
+    }
+    double a = z;
+    if constexpr (UP) a = rd.template ld<double>(((47u + 8u * w) & ~15u) + 8u * t) * z;
+    if constexpr (SPIN) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if ((uint32_t)t < cnt[k]) spin_bit(UP ? F.U : F.L, col[k]);
+            x[k] = vec[col[k]];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a = __fma_rn(-b[k], x[k], a);
+    vec[i] = a;
+    if (SPIN) set_bit(UP ? F.U : F.L, i);
+}
+
 // Scalar CSR rows: the same record walk with 1x1 blocks --
 // one value plane per k, one Dinv plane, one FMA chain per row
 // (lower: acc = r_i, fma(-l_ij, z_j, acc); upper: acc = dinv_i * z_i,
@@ -529,6 +573,15 @@ __device__ __forceinline__ void process_record1(const Rd &rd, const RecHdr &h, c
     const uint32_t off_desc = ddi::rec_off_desc(K);
     const uint32_t off_dinv = ddi::rec_off_dinv(K, w);
     const uint32_t off_val = h.off_val;
+#if DD_PRED1
+    if (!std::is_same<Rd, GlobalRd>::value && (GEN == 0 || K <= 3)) {
+        if (upper)
+            rec1<SPIN, true>(rd, h, c8, t, vec, F);
+        else
+            rec1<SPIN, false>(rd, h, c8, t, vec, F);
+        return;
+    }
+#endif
     if (GEN == 0 || K <= 3) {
         const uint2 d = rd.template ld<uint2>(off_desc + 8u * t);
         const uint32_t i = d.x & 0xffffu;
