@@ -41,8 +41,9 @@
 // block) and the compiler keeps fewer values live (157 -> 103 registers).
 // fma(-0, 0, a) == a for every a, so the result is bitwise the same.
 // Config 3: 404 -> 385 us. DD_PRED=0 builds the branching form (ablation).
-// Scalar CSR rows keep the branching form: there a row's block is one value
-// and the branch-free form measured 5-8 % slower (tools/csr_bench.py).
+// Scalar CSR rows: with selects the branch-free form measured 5-8 % slower
+// than branching (a row's block is one value); with the zero slot and the zero
+// count bytes (no selects, rec1) it is 3-5 % faster (tools/csr_bench.py).
 #ifndef DD_PRED
 #define DD_PRED 1
 #endif
