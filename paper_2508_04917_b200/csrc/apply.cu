@@ -126,8 +126,25 @@ struct RingRd {  // ring variant, record wraps the ring end
 struct SpinFlags {
     uint32_t *L, *U;
 };
+// Watchdog: a row's dependencies are rows of earlier levels of the same CTA,
+// so a wait can only outlast DD_SPIN_TIMEOUT_NS (default 2 s) if the slab is
+// corrupt; the kernel then traps (the call fails with a launch error) instead
+// of hanging the GPU. The clock is read once per 1024 polls.
+#ifndef DD_SPIN_TIMEOUT_NS
+#define DD_SPIN_TIMEOUT_NS 2000000000ull
+#endif
 __device__ __forceinline__ void spin_bit(const uint32_t *bits, uint32_t j) {
+    uint32_t n = 0;
+    unsigned long long t0 = 0;
     while (!((*reinterpret_cast<const volatile uint32_t *>(bits + (j >> 5)) >> (j & 31u)) & 1u)) {
+        if ((++n & 1023u) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t0 == 0)
+                t0 = t;
+            else if (t - t0 > DD_SPIN_TIMEOUT_NS)
+                __trap();
+        }
     }
     __threadfence_block();
 }
