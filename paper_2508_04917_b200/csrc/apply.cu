@@ -943,7 +943,8 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 //   so the warps pipeline levels. Ring chunks are released per warp (empty
 //   barriers count NW arrivals).
 // mode 1 (DD_APPLY_MODE=1, measurement only): consumers skip the arithmetic --
-//   the streaming ceiling of the ring.
+//   the streaming ceiling of the ring; mode 2: chunks are handed back as they
+//   land (no record walk) -- the raw stream.
 template <int BS, uint32_t RING, uint32_t CH, bool SPIN, int GEN, int MODE = AM_VC>
 __global__ void __launch_bounds__(TCB<BS> + 32, 1)
     k_apply_ring(const uint8_t *__restrict__ slab, const SubInfo *__restrict__ info, int n_sub,
@@ -1181,6 +1182,18 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         tmark(0);
 #endif
         // ---- records
+        if (mode == 2) {
+            // measurement only: take every chunk as it lands and hand it back
+            // at once (no record walk, no barriers) -- the ring's raw stream
+            // (every thread tracks the chunks it has seen full)
+            for (uint32_t c = rb / CH; c < nch; ++c) {
+                ensure(gbase + c);
+                release_to(gbase + c + 1);
+            }
+            named_bar_sync(1, TC);
+            gbase += nch;
+            continue;
+        }
         uint32_t ro = rb;
         while (true) {
             ensure(gbase + ro / CH);
