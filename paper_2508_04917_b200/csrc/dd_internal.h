@@ -225,9 +225,9 @@ struct dd_ctx {
     bool refactor = false;               // refactor maps built (enable_refactor, or the GPU numeric path)
     bool gpu_numeric = false;            // dd_setup factors on the device (k_refactor9), host holds no values
     double pivot_floor = 1e-300;
-    ddi::uvector<int64_t> Asrc;          // reordered local A_r block -> original block index
+    ddi::uvector<int32_t> Asrc;          // reordered local A_r block -> original block index
     std::vector<int64_t> Wrp;            // A_dd working layout (rank-local rows)
-    ddi::uvector<int64_t> Wsrc;
+    ddi::uvector<int32_t> Wsrc;
     ddi::uvector<int32_t> Wcol;
     std::vector<int64_t> Wdiag;
     ddi::uvector<int64_t> Uptr;          // per W position: update range

@@ -74,7 +74,7 @@ __device__ __forceinline__ void rf_scatter(uint8_t *slab, int64_t off, int32_t s
 
 // to[q] = from[src[q]] (9 doubles per block); ELL != 0: `to` is the sliced-ELL
 // value array (slot q -> planes of 32 per block column), src < 0 = padding.
-__global__ void k_gather_blocks(int64_t n, const int64_t *__restrict__ src, const double *__restrict__ from,
+__global__ void k_gather_blocks(int64_t n, const int32_t *__restrict__ src, const double *__restrict__ from,
                                 double *__restrict__ to, int ell) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sidx = src[q];
@@ -363,7 +363,7 @@ void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStr
 // their map and value loads in flight together. 160^3: 1.6 -> 0.78 ms
 // (k_gather_blocks, one thread per block: 36 % of the DRAM peak; one tile per
 // iteration: 1.48 ms, latency-bound)
-__global__ void __launch_bounds__(288) k_gather_w9(int64_t n, const int64_t *__restrict__ src,
+__global__ void __launch_bounds__(288) k_gather_w9(int64_t n, const int32_t *__restrict__ src,
                                                    const double *__restrict__ from, double *__restrict__ to) {
     constexpr int U = 4;
     const int b = threadIdx.x / 9, v = threadIdx.x - 9 * (threadIdx.x / 9);
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(288) k_gather_w9(int64_t n, const int64_t *__r
     }
 }
 
-void launch_gather_blocks(int64_t n, const int64_t *src, const double *from, double *to, int ell, int grid,
+void launch_gather_blocks(int64_t n, const int32_t *src, const double *from, double *to, int ell, int grid,
                           cudaStream_t st) {
     if (!ell) {
         k_gather_w9<<<grid, 288, 0, st>>>(n, src, from, to);

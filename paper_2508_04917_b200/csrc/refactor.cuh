@@ -20,12 +20,12 @@ struct RfArgs {
     int64_t row_first;
 };
 
-void launch_gather_blocks(int64_t n, const int64_t *src, const double *from, double *to, int ell, int grid,
+void launch_gather_blocks(int64_t n, const int32_t *src, const double *from, double *to, int ell, int grid,
                           cudaStream_t st);
 void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st);
 // the diagonal-update class (k_refactor_diag): plan = 12 words per row in
 // LevRows order -- li, w0, dpos | (lower block jp has its U_ki update) << (8 + jp),
-// Lrp[li], k of the lower blocks (3), W position of U_ki (3), Urp[li], blocks in the row
+// Lrp[li], k of the lower blocks (3), W position of U_ki (3, -1: none), 2 unused
 void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStream_t st);
 
 }  // namespace ddk

@@ -22,7 +22,8 @@ struct RfState {
     int32_t *SubLev = nullptr, *LevPtr = nullptr, *LevRows = nullptr, *Wcol = nullptr, *UpdQ = nullptr,
             *UpdT = nullptr, *Lst = nullptr, *Ust = nullptr, *Dst = nullptr;
     int64_t *Wrp = nullptr, *Wdiag = nullptr, *Uptr = nullptr, *Lrp = nullptr, *Urp = nullptr, *Loff = nullptr,
-            *Uoff = nullptr, *Doff = nullptr, *Wsrc = nullptr, *Esrc = nullptr;
+            *Uoff = nullptr, *Doff = nullptr;
+    int32_t *Wsrc = nullptr, *Esrc = nullptr;  // W / sliced-ELL position -> caller's block (-1: padding)
     int32_t *plan = nullptr;  // row plans of k_refactor_diag (null: k_refactor9)
     double *W = nullptr, *Dinv = nullptr, *stage = nullptr;
     unsigned long long *bad = nullptr;
@@ -33,38 +34,24 @@ dd_status refactor_init(dd_ctx *c) {
     if (c->rf) return DD_OK;
     auto *rf = new RfState();
     c->rf = rf;
-    TRY(upload_vec(&rf->SubLev, c->SubLev));
-    TRY(upload_vec(&rf->LevPtr, c->LevPtr));
-    TRY(upload_vec(&rf->LevRows, c->LevRows));
-    TRY(upload_vec(&rf->SubU, c->SubU));
-    TRY(upload_vec(&rf->URows, c->URows));
-    TRY(upload_vec(&rf->Wcol, c->Wcol));
-    TRY(upload_vec(&rf->UpdQ, c->UpdQ));
-    TRY(upload_vec(&rf->UpdT, c->UpdT));
-    TRY(upload_vec(&rf->Lst, c->SlabLst));
-    TRY(upload_vec(&rf->Ust, c->SlabUst));
-    TRY(upload_vec(&rf->Dst, c->SlabDst));
-    TRY(upload_vec(&rf->Wrp, c->Wrp));
-    TRY(upload_vec(&rf->Wdiag, c->Wdiag));
-    TRY(upload_vec(&rf->Uptr, c->Uptr));
-    TRY(upload_vec(&rf->Lrp, c->Lrp));
-    TRY(upload_vec(&rf->Urp, c->Urp));
-    TRY(upload_vec(&rf->Loff, c->SlabLoff));
-    TRY(upload_vec(&rf->Uoff, c->SlabUoff));
-    TRY(upload_vec(&rf->Doff, c->SlabDoff));
-    TRY(upload_vec(&rf->Wsrc, c->Wsrc));
+    static const bool trace = getenv("DD_SETUP_TRACE") != nullptr;
+    const double t0 = now_ms();
+    auto mark = [&](const char *what) {
+        if (trace) fprintf(stderr, "[dd refactor_init] %-22s %9.1f ms\n", what, now_ms() - t0);
+    };
     // diagonal-update class (refactor.cu, k_refactor_diag): <= 3 lower blocks
     // per row, each with at most one update, on the row's diagonal block
     {
         const int64_t nr = (int64_t)c->LevRows.size();
-        std::vector<int32_t> plan((size_t)12 * nr, 0);
-        int fits = (c->Lrp.empty() || c->Lrp.back() < INT32_MAX) && (c->Urp.empty() || c->Urp.back() < INT32_MAX);
+        ddi::uvector<int32_t> plan((size_t)12 * nr);  // every word written below
+        int fits = c->Lrp.empty() || c->Lrp.back() < INT32_MAX;
 #pragma omp parallel for schedule(static) reduction(&& : fits)
         for (int64_t idx = 0; idx < nr; ++idx) {
             int32_t *P = plan.data() + (size_t)12 * idx;
             const int64_t li = c->LevRows[idx], w0 = c->Wrp[li], dpos = c->Wdiag[li] - w0;
             bool ok = dpos <= 3;
             int32_t upd = 0;
+            for (int w = 4; w < 12; ++w) P[w] = w < 7 ? 0 : -1;
             for (int64_t jp = 0; ok && jp < dpos; ++jp) {
                 const int64_t p = w0 + jp, nu = c->Uptr[p + 1] - c->Uptr[p];
                 P[4 + jp] = c->Wcol[p];
@@ -79,30 +66,61 @@ dd_status refactor_init(dd_ctx *c) {
             P[1] = (int32_t)w0;
             P[2] = (int32_t)(dpos | upd << 8);
             P[3] = (int32_t)c->Lrp[li];
-            P[10] = (int32_t)c->Urp[li];
-            P[11] = (int32_t)(c->Wrp[li + 1] - w0);
             fits = fits && ok;
         }
         static const bool force = getenv("DD_REFACTOR_KERNEL") != nullptr;
+        mark("plan built");
         if (fits && !force) TRY(upload_vec(&rf->plan, plan));
     }
+    // maps both kernels read (the U pass, the slab stores, the W gather)
+    TRY(upload_vec(&rf->SubLev, c->SubLev));
+    TRY(upload_vec(&rf->LevPtr, c->LevPtr));
+    TRY(upload_vec(&rf->SubU, c->SubU));
+    TRY(upload_vec(&rf->URows, c->URows));
+    TRY(upload_vec(&rf->Lst, c->SlabLst));
+    TRY(upload_vec(&rf->Ust, c->SlabUst));
+    TRY(upload_vec(&rf->Dst, c->SlabDst));
+    TRY(upload_vec(&rf->Wrp, c->Wrp));
+    TRY(upload_vec(&rf->Wdiag, c->Wdiag));
+    TRY(upload_vec(&rf->Urp, c->Urp));
+    TRY(upload_vec(&rf->Loff, c->SlabLoff));
+    TRY(upload_vec(&rf->Uoff, c->SlabUoff));
+    TRY(upload_vec(&rf->Doff, c->SlabDoff));
+    TRY(upload_vec(&rf->Wsrc, c->Wsrc));
+    // the general elimination's index chains: only k_refactor9 walks them (the
+    // row plans replace them; ~0.45 GB less to upload at 160^3)
+    if (!rf->plan) {
+        TRY(upload_vec(&rf->LevRows, c->LevRows));
+        TRY(upload_vec(&rf->Wcol, c->Wcol));
+        TRY(upload_vec(&rf->UpdQ, c->UpdQ));
+        TRY(upload_vec(&rf->UpdT, c->UpdT));
+        TRY(upload_vec(&rf->Uptr, c->Uptr));
+        TRY(upload_vec(&rf->Lrp, c->Lrp));
+    }
+    mark("maps uploaded");
     // sliced-ELL slot -> original block index (-1 = padding), same layout as device_setup
     {
         const int64_t nl = c->n_local;
         const auto &S = c->spmv;
-        std::vector<int64_t> es(S.n_slots, -1);
-        int64_t base = 0;
+        ddi::uvector<int32_t> es(S.n_slots);  // every slot written below (padding: -1)
+        std::vector<int64_t> base(S.n_slices + 1, 0);
+#pragma omp parallel for schedule(static)
         for (int64_t s = 0; s < S.n_slices; ++s) {
             int64_t K = 0;
             for (int64_t li = 32 * s; li < std::min(nl, 32 * s + 32); ++li) K = std::max(K, c->Arp[li + 1] - c->Arp[li]);
-            for (int lane = 0; lane < 32; ++lane) {
-                const int64_t li = 32 * s + lane;
-                if (li >= nl) break;
-                for (int64_t k = 0; k < c->Arp[li + 1] - c->Arp[li]; ++k) es[base + 32 * k + lane] = c->Asrc[c->Arp[li] + k];
-            }
-            base += 32 * K;
+            base[s + 1] = 32 * K;
         }
+        for (int64_t s = 0; s < S.n_slices; ++s) base[s + 1] += base[s];
+#pragma omp parallel for schedule(static)
+        for (int64_t s = 0; s < S.n_slices; ++s)
+            for (int lane = 0; lane < 32; ++lane) {
+                const int64_t li = 32 * s + lane, K = (base[s + 1] - base[s]) / 32;
+                const int64_t len = li < nl ? c->Arp[li + 1] - c->Arp[li] : 0;
+                for (int64_t k = 0; k < K; ++k) es[base[s] + 32 * k + lane] = k < len ? c->Asrc[c->Arp[li] + k] : -1;
+            }
+        mark("ell map built");
         TRY(upload_vec(&rf->Esrc, es));
+        mark("ell map uploaded");
     }
     TRY(dmalloc(&rf->W, 9 * std::max<size_t>(1, c->Wsrc.size())));
     TRY(dmalloc(&rf->Dinv, 9 * std::max<int64_t>(1, c->n_local)));
@@ -177,7 +195,10 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
         // pageable host values: through the pinned staging pipeline (h2d_big),
         // ordered before the gathers by a stream synchronisation
         CK(cudaStreamSynchronize(st));
+        static const bool trace = getenv("DD_SETUP_TRACE") != nullptr;
+        const double tv = now_ms();
         TRY(h2d_big(rf->stage, vals, 9 * c->nnzb_A * sizeof(double)));
+        if (trace) fprintf(stderr, "[dd refactor] values H2D         %9.1f ms\n", now_ms() - tv);
         src = rf->stage;
     }
     const int grid = c->num_sms * 8;

@@ -505,6 +505,12 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     if (gpu_num) ctx->refactor = true;
     if (!gpu_num) ctx->Av.resize(b2 * nnz_loc);  // every block written below (GPU path: values gathered on the device)
     ctx->pivot_floor = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
+    if (ctx->refactor && A->nnzb >= INT32_MAX) {
+        // the refactor maps index the caller's blocks with int32 (2^31 blocks
+        // would be 155 GB of values alone)
+        set_error("dd_setup: enable_refactor / GPU factorisation needs fewer than 2^31 blocks");
+        return DD_E_INVALID_ARG;
+    }
     if (ctx->refactor) ctx->Asrc.resize(nnz_loc);  // every entry written below
 #pragma omp parallel for schedule(static)
     for (int64_t li = 0; li < nl; ++li) {
@@ -528,7 +534,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         for (int64_t t = 0; t < nb; ++t) {
             gcol[Arp[li] + t] = cc[ix[t]];
             if (!gpu_num) std::memcpy(&ctx->Av[b2 * (Arp[li] + t)], &av[b2 * (rp[m] + ix[t])], b2 * sizeof(double));
-            if (ctx->refactor) ctx->Asrc[Arp[li] + t] = rp[m] + ix[t];
+            if (ctx->refactor) ctx->Asrc[Arp[li] + t] = (int32_t)(rp[m] + ix[t]);
         }
     }
     // global drop statistics (count of same-label blocks over all rows)
@@ -624,6 +630,8 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
         ctx->Lrp[li + 1] += ctx->Lrp[li];
         ctx->Urp[li + 1] += ctx->Urp[li];
     }
+    static const bool trace2 = getenv("DD_SETUP_TRACE") != nullptr;
+    if (trace2) fprintf(stderr, "[dd setup] pattern sizes     %9.1f ms\n", now_ms() - t2);
     ctx->Lci.resize(ctx->Lrp[nl]);
     ctx->Uci.resize(ctx->Urp[nl]);
     if (!gpu_num) {
@@ -636,6 +644,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     if (!gpu_num) ctx->Dinv.resize(b2 * nl);
     ctx->hmapL.assign(nl, 0);
     ctx->hmapU.assign(nl, 0);
+    if (trace2) fprintf(stderr, "[dd setup] factor arrays     %9.1f ms\n", now_ms() - t2);
 
     // ---- per-subdomain block ILU0 -> ILDU0 -> levels
     const double floor_ = o->pivot_floor > 0 ? o->pivot_floor : 1e-300;
@@ -735,6 +744,7 @@ dd_status host_setup(dd_ctx *ctx, const dd_bsr3 *A, const dd_opts *o) {
     }
     const double t3 = now_ms();
     ctx->setup_ms[2] = t3 - t2;
+    if (trace2) fprintf(stderr, "[dd setup] subdomain loop    %9.1f ms\n", t3 - t2);
     // global pivot status must agree across ranks; the API layer reduces it.
     if (bad_pivot != INT64_MAX) {
         set_error("dd_setup: singular pivot block (|det| < pivot_floor) at reordered row " +
