@@ -270,7 +270,8 @@ constexpr int RFD_PLAN_WORDS = 12;
 #ifndef RFD_THREADS
 #define RFD_THREADS 512
 #endif
-__global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs a, const int32_t *__restrict__ plan) {
+__global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs a, const int32_t *__restrict__ plan,
+                                                                     int write_w) {
     const int q = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / 9;
@@ -332,10 +333,12 @@ __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs 
 #pragma unroll
                 for (int jp = 0; jp < 3; ++jp)
                     if (jp < dpos) {
-                        a.W[9 * (size_t)(w0 + jp) + v] = Lk[jp];
+                        if (write_w) a.W[9 * (size_t)(w0 + jp) + v] = Lk[jp];
                         *reinterpret_cast<double *>(a.slab + loff[jp] + (int64_t)lst[jp] * v) = Lk[jp];
                     }
-                a.W[9 * (size_t)(w0 + dpos) + v] = wii;
+                // W keeps the matrix's values in this class (nothing later reads
+                // L or U_ii from it); dd_get_factors re-runs with write_w = 1
+                if (write_w) a.W[9 * (size_t)(w0 + dpos) + v] = wii;
                 if (!okinv) {
                     if (v == 0) atomicMin(a.bad, (unsigned long long)(a.row_first + li));
                 } else {
@@ -352,8 +355,8 @@ __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs 
     rf_upass_rows(a, q);
 }
 
-void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStream_t st) {
-    k_refactor_diag<<<nsl, RFD_THREADS, 0, st>>>(a, plan);
+void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, int write_w, cudaStream_t st) {
+    k_refactor_diag<<<nsl, RFD_THREADS, 0, st>>>(a, plan, write_w);
 }
 
 // to[q] = from[src[q]] for the W layout with nine lanes per block: a

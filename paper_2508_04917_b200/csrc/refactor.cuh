@@ -26,6 +26,7 @@ void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st);
 // the diagonal-update class (k_refactor_diag): plan = 12 words per row in
 // LevRows order -- li, w0, dpos | (lower block jp has its U_ki update) << (8 + jp),
 // Lrp[li], k of the lower blocks (3), W position of U_ki (3, -1: none), 2 unused
-void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStream_t st);
+// write_w: also store L and U_ii into W (dd_get_factors; the factors are the same)
+void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, int write_w, cudaStream_t st);
 
 }  // namespace ddk

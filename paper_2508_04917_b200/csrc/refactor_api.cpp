@@ -30,6 +30,13 @@ struct RfState {
     unsigned long long *h_bad = nullptr;
 };
 
+ddk::RfArgs rf_args(const dd_ctx *c, const RfState *rf) {
+    return ddk::RfArgs{rf->SubLev, rf->LevPtr, rf->LevRows, rf->SubU, rf->URows, rf->Wrp, rf->Wdiag, rf->Uptr,
+                       rf->Lrp, rf->Urp, rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes,
+                       rf->Loff, rf->Uoff, rf->Doff, rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad,
+                       c->row_first};
+}
+
 dd_status refactor_init(dd_ctx *c) {
     if (c->rf) return DD_OK;
     auto *rf = new RfState();
@@ -156,6 +163,16 @@ dd_status refactor_fetch(const dd_ctx *c, std::vector<double> &W, std::vector<do
         set_error("factors are not on the device");
         return DD_E_INVALID_ARG;
     }
+    if (rf->plan && c->sub_last > c->sub_first) {
+        // the diagonal-update kernel leaves the matrix's values in W: run it
+        // once more storing L and U_ii there (W still holds the gathered values,
+        // so the factors, Dinv and the slab come out bit for bit the same)
+        CK(cudaSetDevice(c->device));
+        const ddk::RfArgs a = rf_args(c, rf);
+        ddk::launch_refactor_diag(c->sub_last - c->sub_first, a, rf->plan, 1, nullptr);
+        CK(cudaDeviceSynchronize());
+        CK(cudaGetLastError());
+    }
     W.resize(9 * c->Wsrc.size());
     Dinv.resize(9 * (size_t)c->n_local);
     if (!W.empty()) CK(cudaMemcpy(W.data(), rf->W, W.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -206,13 +223,11 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
     ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
     *rf->h_bad = ~0ull;
     CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    ddk::RfArgs a{rf->SubLev, rf->LevPtr, rf->LevRows, rf->SubU, rf->URows, rf->Wrp, rf->Wdiag, rf->Uptr, rf->Lrp, rf->Urp,
-                  rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes, rf->Loff, rf->Uoff, rf->Doff,
-                  rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad, c->row_first};
+    const ddk::RfArgs a = rf_args(c, rf);
     const int nsl = c->sub_last - c->sub_first;
     if (nsl > 0) {
         if (rf->plan)
-            ddk::launch_refactor_diag(nsl, a, rf->plan, st);
+            ddk::launch_refactor_diag(nsl, a, rf->plan, 0, st);
         else
             ddk::launch_refactor(nsl, a, st);
     }
