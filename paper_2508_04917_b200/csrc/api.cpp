@@ -763,7 +763,23 @@ dd_status dd_get_factors(const dd_ctx *c, int64_t *nL, int64_t *nU, int64_t *Lrp
         // kernel's and the host ILU0's, section 4)
         std::vector<double> W, D;
         TRY(refactor_fetch(c, W, D));
-        for (int64_t li = 0; li < c->n_local; ++li) {
+        if (W.empty() && (Lv || Uv)) {
+            // diagonal-update path (no W buffer): L and U_unit as the slab holds
+            // them, through the scatter maps
+            size_t nb = 0;  // the host copy is gone after the upload: size from the stream table
+            for (const auto &si : c->slab_lvl.info) nb = std::max(nb, (size_t)(si.stream_off + si.stream_bytes));
+            uvector<uint8_t> sb(nb);
+            CK(cudaSetDevice(c->device));
+            if (!sb.empty()) CK(cudaMemcpy(sb.data(), c->slab_lvl.d_bytes, sb.size(), cudaMemcpyDeviceToHost));
+            auto blk = [&](int64_t off, int32_t st, double *out) {
+                for (int v = 0; v < 9; ++v) std::memcpy(out + v, sb.data() + off + (int64_t)st * v, 8);
+            };
+            if (Lv)
+                for (size_t b = 0; b < c->Lci.size(); ++b) blk(c->SlabLoff[b], c->SlabLst[b], Lv + 9 * b);
+            if (Uv)
+                for (size_t b = 0; b < c->Uci.size(); ++b) blk(c->SlabUoff[b], c->SlabUst[b], Uv + 9 * b);
+        }
+        for (int64_t li = 0; li < c->n_local && !W.empty(); ++li) {
             const int64_t w0 = c->Wrp[li], d = c->Wdiag[li], w1 = c->Wrp[li + 1];
             if (Lv)
                 for (int64_t p = w0; p < d; ++p) std::memcpy(Lv + 9 * (c->Lrp[li] + (p - w0)), &W[9 * p], 72);

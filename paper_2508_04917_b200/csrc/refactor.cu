@@ -164,6 +164,7 @@ __device__ __forceinline__ int warp_max(int x) { return __reduce_max_sync(0xffff
 // writes consecutive plane elements (full 32-byte sectors; nine lanes per
 // block wrote three rows' elements per warp store: 4.69 -> 4.28 ms per
 // dd_refactor at 160^3). rf_mul3's FMA order.
+template <bool FROM_A>
 __device__ __forceinline__ void rf_upass_rows(const RfArgs &a, int q) {
     const int ulo = a.SubU[q], uhi = a.SubU[q + 1];
     for (int idx = ulo + threadIdx.x; idx < uhi; idx += blockDim.x) {
@@ -176,7 +177,8 @@ __device__ __forceinline__ void rf_upass_rows(const RfArgs &a, int q) {
         const int64_t ub = a.Urp[li];
         for (int64_t p = d + 1; p < w1; ++p) {
             double Uu[9];
-            rf_mul3(inv, a.W + 9 * p, Uu);  // U_unit_ij = Dinv_i * U_ij
+            // U_unit_ij = Dinv_i * U_ij (FROM_A: U_ij is still the caller's block)
+            rf_mul3(inv, FROM_A ? a.A + 9 * (int64_t)a.Wsrc[p] : a.W + 9 * p, Uu);
             const int64_t b = ub + (p - d - 1);
             rf_scatter(a.slab, a.Uoff[b], a.Ust[b], Uu);
         }
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(RF9_THREADS) k_refactor9(RfArgs a) {
         }
         __syncthreads();
     }
-    rf_upass_rows(a, q);
+    rf_upass_rows<false>(a, q);
 }
 
 // Diagonal-update class (every row has <= 3 lower blocks and every ILU0 update
@@ -263,15 +265,13 @@ __global__ void __launch_bounds__(RF9_THREADS) k_refactor9(RfArgs a) {
 // a 9-lane group issues all of its loads at once and keeps U_ii in registers
 // through the updates. Per element the FMA order is rf_mul3 / rf_sub_mul /
 // rf_inv3's (the host's): identical bits. The U pass is k_refactor9's.
-constexpr int RFD_PLAN_WORDS = 12;
 #ifndef RFD_MINB
 #define RFD_MINB 2
 #endif
 #ifndef RFD_THREADS
 #define RFD_THREADS 512
 #endif
-__global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs a, const int32_t *__restrict__ plan,
-                                                                     int write_w) {
+__global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs a, const int32_t *__restrict__ plan) {
     const int q = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / 9;
@@ -286,20 +286,21 @@ __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs 
             const int idx = base + grp;
             const bool has = live && idx < hi;
             const int4 *P = reinterpret_cast<const int4 *>(plan + (size_t)RFD_PLAN_WORDS * (has ? idx : lo));
-            const int4 p0 = __ldg(P), p1 = __ldg(P + 1), p2 = __ldg(P + 2);
-            // p0: li, w0, dpos | upd-mask << 8, Lb; p1: k0, k1, k2, q0; p2: q1, q2, -, -
-            const int li = p0.x, w0 = p0.y, Lb = p0.w;
+            const int4 p0 = __ldg(P), p1 = __ldg(P + 1), p2 = __ldg(P + 2), p3 = __ldg(P + 3);
+            // p0: li, w0, dpos | upd-mask << 8, Lb; p1: k0, k1, k2, q0; p2: q1, q2, a0, a1;
+            // p3: a2, aii, -, -  (q, a: the caller's blocks of U_ki, W_ik; aii: U_ii)
+            const int li = p0.x, Lb = p0.w;
             const int dpos = has ? (p0.z & 255) : 0, upd = p0.z >> 8;
-            const int kk[3] = {p1.x, p1.y, p1.z}, qq[3] = {p1.w, p2.x, p2.y};
+            const int kk[3] = {p1.x, p1.y, p1.z}, qq[3] = {p1.w, p2.x, p2.y}, aa[3] = {p2.z, p2.w, p3.x};
             double wik[3], dk[3], uki[3];
 #pragma unroll
             for (int jp = 0; jp < 3; ++jp) {
                 const bool ok = jp < dpos;
-                wik[jp] = ok ? a.W[9 * (size_t)(w0 + jp) + v] : 0.0;
+                wik[jp] = ok ? __ldg(a.A + 9 * (size_t)aa[jp] + v) : 0.0;
                 dk[jp] = ok ? a.Dinv[9 * (size_t)kk[jp] + v] : 0.0;
-                uki[jp] = ok && ((upd >> jp) & 1) ? a.W[9 * (size_t)qq[jp] + v] : 0.0;
+                uki[jp] = ok && ((upd >> jp) & 1) ? __ldg(a.A + 9 * (size_t)qq[jp] + v) : 0.0;
             }
-            double wii = has ? a.W[9 * (size_t)(w0 + dpos) + v] : 0.0;
+            double wii = has ? __ldg(a.A + 9 * (size_t)p3.y + v) : 0.0;
             int64_t loff[3];
             int32_t lst[3];
 #pragma unroll
@@ -332,13 +333,7 @@ __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs 
             if (has) {
 #pragma unroll
                 for (int jp = 0; jp < 3; ++jp)
-                    if (jp < dpos) {
-                        if (write_w) a.W[9 * (size_t)(w0 + jp) + v] = Lk[jp];
-                        *reinterpret_cast<double *>(a.slab + loff[jp] + (int64_t)lst[jp] * v) = Lk[jp];
-                    }
-                // W keeps the matrix's values in this class (nothing later reads
-                // L or U_ii from it); dd_get_factors re-runs with write_w = 1
-                if (write_w) a.W[9 * (size_t)(w0 + dpos) + v] = wii;
+                    if (jp < dpos) *reinterpret_cast<double *>(a.slab + loff[jp] + (int64_t)lst[jp] * v) = Lk[jp];
                 if (!okinv) {
                     if (v == 0) atomicMin(a.bad, (unsigned long long)(a.row_first + li));
                 } else {
@@ -352,11 +347,11 @@ __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs 
         }
         __syncthreads();
     }
-    rf_upass_rows(a, q);
+    rf_upass_rows<true>(a, q);
 }
 
-void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, int write_w, cudaStream_t st) {
-    k_refactor_diag<<<nsl, RFD_THREADS, 0, st>>>(a, plan, write_w);
+void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStream_t st) {
+    k_refactor_diag<<<nsl, RFD_THREADS, 0, st>>>(a, plan);
 }
 
 // to[q] = from[src[q]] for the W layout with nine lanes per block: a

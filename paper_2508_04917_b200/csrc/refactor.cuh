@@ -18,15 +18,20 @@ struct RfArgs {
     double floor_;
     unsigned long long *bad;  // min failing (reordered global) row
     int64_t row_first;
+    // the caller's blocks and W position -> caller's block (k_refactor_diag
+    // reads the matrix's values straight from A: no W buffer)
+    const double *A;
+    const int32_t *Wsrc;
 };
 
 void launch_gather_blocks(int64_t n, const int32_t *src, const double *from, double *to, int ell, int grid,
                           cudaStream_t st);
 void launch_refactor(int nsl, const RfArgs &a, cudaStream_t st);
-// the diagonal-update class (k_refactor_diag): plan = 12 words per row in
+// the diagonal-update class (k_refactor_diag): plan = 16 words per row in
 // LevRows order -- li, w0, dpos | (lower block jp has its U_ki update) << (8 + jp),
-// Lrp[li], k of the lower blocks (3), W position of U_ki (3, -1: none), 2 unused
-// write_w: also store L and U_ii into W (dd_get_factors; the factors are the same)
-void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, int write_w, cudaStream_t st);
+// Lrp[li], k of the lower blocks (3), caller's block of U_ki (3, -1: none),
+// caller's blocks of W_ik (3, -1: none), caller's block of U_ii, 2 unused
+constexpr int RFD_PLAN_WORDS = 16;
+void launch_refactor_diag(int nsl, const RfArgs &a, const int32_t *plan, cudaStream_t st);
 
 }  // namespace ddk

@@ -30,11 +30,11 @@ struct RfState {
     unsigned long long *h_bad = nullptr;
 };
 
-ddk::RfArgs rf_args(const dd_ctx *c, const RfState *rf) {
+ddk::RfArgs rf_args(const dd_ctx *c, const RfState *rf, const double *A) {
     return ddk::RfArgs{rf->SubLev, rf->LevPtr, rf->LevRows, rf->SubU, rf->URows, rf->Wrp, rf->Wdiag, rf->Uptr,
                        rf->Lrp, rf->Urp, rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes,
                        rf->Loff, rf->Uoff, rf->Doff, rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad,
-                       c->row_first};
+                       c->row_first, A, rf->Wsrc};
 }
 
 dd_status refactor_init(dd_ctx *c) {
@@ -50,22 +50,22 @@ dd_status refactor_init(dd_ctx *c) {
     // per row, each with at most one update, on the row's diagonal block
     {
         const int64_t nr = (int64_t)c->LevRows.size();
-        ddi::uvector<int32_t> plan((size_t)12 * nr);  // every word written below
+        ddi::uvector<int32_t> plan((size_t)ddk::RFD_PLAN_WORDS * nr);  // every word written below
         int fits = c->Lrp.empty() || c->Lrp.back() < INT32_MAX;
 #pragma omp parallel for schedule(static) reduction(&& : fits)
         for (int64_t idx = 0; idx < nr; ++idx) {
-            int32_t *P = plan.data() + (size_t)12 * idx;
+            int32_t *P = plan.data() + (size_t)ddk::RFD_PLAN_WORDS * idx;
             const int64_t li = c->LevRows[idx], w0 = c->Wrp[li], dpos = c->Wdiag[li] - w0;
             bool ok = dpos <= 3;
             int32_t upd = 0;
-            for (int w = 4; w < 12; ++w) P[w] = w < 7 ? 0 : -1;
+            for (int w = 4; w < ddk::RFD_PLAN_WORDS; ++w) P[w] = w < 7 ? 0 : -1;
             for (int64_t jp = 0; ok && jp < dpos; ++jp) {
                 const int64_t p = w0 + jp, nu = c->Uptr[p + 1] - c->Uptr[p];
                 P[4 + jp] = c->Wcol[p];
-                P[7 + jp] = -1;
+                P[10 + jp] = c->Wsrc[p];  // W_ik: the caller's block
                 if (nu > 1 || (nu == 1 && c->UpdT[c->Uptr[p]] != c->Wdiag[li])) ok = false;
                 if (nu == 1) {
-                    P[7 + jp] = c->UpdQ[c->Uptr[p]];
+                    P[7 + jp] = c->Wsrc[c->UpdQ[c->Uptr[p]]];  // U_ki: the caller's block
                     upd |= 1 << jp;
                 }
             }
@@ -73,6 +73,7 @@ dd_status refactor_init(dd_ctx *c) {
             P[1] = (int32_t)w0;
             P[2] = (int32_t)(dpos | upd << 8);
             P[3] = (int32_t)c->Lrp[li];
+            P[13] = c->Wsrc[c->Wdiag[li]];  // U_ii: the caller's block
             fits = fits && ok;
         }
         static const bool force = getenv("DD_REFACTOR_KERNEL") != nullptr;
@@ -129,7 +130,9 @@ dd_status refactor_init(dd_ctx *c) {
         TRY(upload_vec(&rf->Esrc, es));
         mark("ell map uploaded");
     }
-    TRY(dmalloc(&rf->W, 9 * std::max<size_t>(1, c->Wsrc.size())));
+    // the working layout W: only the general kernel needs it (the
+    // diagonal-update kernel reads the caller's blocks directly)
+    if (!rf->plan) TRY(dmalloc(&rf->W, 9 * std::max<size_t>(1, c->Wsrc.size())));
     TRY(dmalloc(&rf->Dinv, 9 * std::max<int64_t>(1, c->n_local)));
     TRY(dmalloc(&rf->stage, 9 * std::max<int64_t>(1, c->nnzb_A)));
     TRY(dmalloc(&rf->bad, 1));
@@ -157,21 +160,23 @@ dd_status refactor_values(dd_ctx *c, const double *vals, bool on_device, cudaStr
     return refactor_run(c, vals, on_device ? 1 : 0, st);
 }
 
+bool refactor_has_w(const dd_ctx *c) {
+    auto *rf = reinterpret_cast<const RfState *>(c->rf);
+    return rf && rf->W;
+}
+
 dd_status refactor_fetch(const dd_ctx *c, std::vector<double> &W, std::vector<double> &Dinv) {
     auto *rf = reinterpret_cast<const RfState *>(c->rf);
     if (!rf) {
         set_error("factors are not on the device");
         return DD_E_INVALID_ARG;
     }
-    if (rf->plan && c->sub_last > c->sub_first) {
-        // the diagonal-update kernel leaves the matrix's values in W: run it
-        // once more storing L and U_ii there (W still holds the gathered values,
-        // so the factors, Dinv and the slab come out bit for bit the same)
-        CK(cudaSetDevice(c->device));
-        const ddk::RfArgs a = rf_args(c, rf);
-        ddk::launch_refactor_diag(c->sub_last - c->sub_first, a, rf->plan, 1, nullptr);
-        CK(cudaDeviceSynchronize());
-        CK(cudaGetLastError());
+    W.clear();
+    if (!rf->W) {
+        // diagonal-update path: no W; the factors are read from the slab
+        Dinv.resize(9 * (size_t)c->n_local);
+        if (!Dinv.empty()) CK(cudaMemcpy(Dinv.data(), rf->Dinv, Dinv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        return DD_OK;
     }
     W.resize(9 * c->Wsrc.size());
     Dinv.resize(9 * (size_t)c->n_local);
@@ -219,15 +224,15 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
         src = rf->stage;
     }
     const int grid = c->num_sms * 8;
-    ddk::launch_gather_blocks((int64_t)c->Wsrc.size(), rf->Wsrc, src, rf->W, 0, grid, st);
+    if (!rf->plan) ddk::launch_gather_blocks((int64_t)c->Wsrc.size(), rf->Wsrc, src, rf->W, 0, grid, st);
     ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
     *rf->h_bad = ~0ull;
     CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    const ddk::RfArgs a = rf_args(c, rf);
+    const ddk::RfArgs a = rf_args(c, rf, src);
     const int nsl = c->sub_last - c->sub_first;
     if (nsl > 0) {
         if (rf->plan)
-            ddk::launch_refactor_diag(nsl, a, rf->plan, 0, st);
+            ddk::launch_refactor_diag(nsl, a, rf->plan, st);
         else
             ddk::launch_refactor(nsl, a, st);
     }
