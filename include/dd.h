@@ -219,11 +219,12 @@ void dd_destroy(dd_ctx *ctx);
 /* Numeric re-factorisation with the SAME sparsity pattern (nonlinear solvers
  * re-factor one pattern many times): new block values
  * vals[9*nnzb] in A's ORIGINAL block order (host or device memory per
- * vals_on_device). Runs on the GPU: values are gathered into the reordered /
- * dropped layout, every subdomain is factored (block ILU0 -> ILDU0, Alg. 7
- * P:680-711, same arithmetic order as dd_setup, so identical bits) level by
- * level, and L, Dinv and U_unit are written straight into the apply slab; the
- * SpMV operand is refreshed too. Requires dd_opts.enable_refactor = 1 (or a
+ * vals_on_device). Runs on the GPU: every subdomain is factored (block ILU0
+ * -> ILDU0, Alg. 7, same arithmetic order as dd_setup, so identical
+ * bits) level by level -- straight from vals when every ILU0 update lands on
+ * a diagonal block (7-point stencils), else from a reordered / dropped copy --
+ * and L, Dinv and U_unit are written straight into the apply slab; the SpMV
+ * operand is refreshed too. vals is read until the call returns. Requires dd_opts.enable_refactor = 1 (or a
  * context that dd_setup already factored on the GPU, which keeps the maps).
  * Collective when world > 1 (the pivot status is agreed over the ranks).
  * Returns DD_E_SINGULAR_PIVOT (context unusable until a successful refactor)
