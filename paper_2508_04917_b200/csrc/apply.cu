@@ -926,12 +926,6 @@ __global__ void __launch_bounds__(TCB<BS>) k_apply_direct(const uint8_t *__restr
 #ifndef DD_CH_DIV
 #define DD_CH_DIV 4  // ring chunk = RING / DD_CH_DIV
 #endif
-// r slice of each subdomain: 1 = consumers load it from global memory (the
-// producer prefetches it into L2 when it starts streaming the subdomain's
-// records), 0 = through the ring ahead of the records (round-1/2 form)
-#ifndef DD_RFILL_G
-#define DD_RFILL_G 0
-#endif
 #ifndef DD_PF_AHEAD
 #define DD_PF_AHEAD -1  // L2 prefetch distance of the ring producer: -1 = half a ring, 0 = off, else bytes
 #endif
@@ -993,12 +987,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 const SubInfo si = info[DD_SUB(s)];
                 const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
                 const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
-#if DD_RFILL_G
-                const uint32_t rb = 0u;  // r is not in the ring: prefetch it for the consumers
-                prefetch_l2(reinterpret_cast<const uint8_t *>(r) + rlo, (uint32_t)(rhi - rlo));
-#else
                 const uint32_t rb = (uint32_t)(rhi - rlo);
-#endif
                 // phase 0: the whole stream; 1: the L section; 2: the D+U section
                 const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
                 const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
@@ -1019,7 +1008,7 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                     const SubInfo sj = info[DD_SUB(ss)];
                     const int64_t jlo = (8 * BS * (int64_t)sj.row0) & ~(int64_t)15;
                     const int64_t jhi = (8 * BS * ((int64_t)sj.row0 + sj.nrows) + 15) & ~(int64_t)15;
-                    const uint32_t jrb = DD_RFILL_G ? 0u : (uint32_t)(jhi - jlo);
+                    const uint32_t jrb = (uint32_t)(jhi - jlo);
                     const uint32_t jsl = phase == 2 ? (uint32_t)sj.u_off : 0u;
                     const uint32_t jsh = phase == 1 ? (uint32_t)sj.u_off : (uint32_t)sj.stream_bytes;
                     b = min(b, jrb + (jsh - jsl));
@@ -1105,23 +1094,11 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
             }
         }
     };
-#if DD_RFILL_G == 2
-    // r slice of subdomain ss -> vec with per-thread async copies (thread t:
-    // entries q = t mod TC, the ones it stored to z for the previous
-    // subdomain), issued as soon as the vector is free
-    auto r_issue = [&](int ss) {
-        const SubInfo sj = info[DD_SUB(ss)];
-        const double *rs = r + BS * (int64_t)sj.row0;
-        const uint32_t ndj = (uint32_t)BS * sj.nrows;
-        for (uint32_t q = t; q < ndj; q += TC) cp_async8(vec + vslot<BS>(sw, q), rs + q);
-    };
-    if ((int)blockIdx.x < n_sub) r_issue(blockIdx.x);
-#endif
     for (int s = blockIdx.x; s < n_sub; s += gridDim.x) {
         const SubInfo si = info[DD_SUB(s)];
         const int64_t rlo = (8 * BS * (int64_t)si.row0) & ~(int64_t)15;
         const int64_t rhi = (8 * BS * ((int64_t)si.row0 + si.nrows) + 15) & ~(int64_t)15;
-        const uint32_t rb = DD_RFILL_G ? 0u : (uint32_t)(rhi - rlo);
+        const uint32_t rb = (uint32_t)(rhi - rlo);
         const uint32_t shift = (uint32_t)(8 * BS * (int64_t)si.row0 - rlo);
         const uint32_t sec_lo = phase == 2 ? (uint32_t)si.u_off : 0u;
         const uint32_t sec_hi = phase == 1 ? (uint32_t)si.u_off : (uint32_t)si.stream_bytes;
@@ -1133,28 +1110,6 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
         trc = clock64();
         tr[6] += 1;
         bool tr_in_u = false;
-#endif
-#if DD_RFILL_G == 2
-        cp_async_wait_all();  // this thread's share of the r slice (issued below)
-        (void)shift;
-#elif DD_RFILL_G
-        // ---- r slice: global (L2-prefetched by the producer) -> vec; thread t
-        // fills the entries q = t (mod TC) -- the ones it stored to z for the
-        // previous subdomain -- so no barrier is needed between that store and
-        // this fill. Loads in batches of 8 (all in flight before the stores).
-        {
-            const double *rs = r + BS * (int64_t)si.row0;
-            uint32_t q = t;
-            for (; q + 7u * TC < nd; q += 8u * TC) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldg(rs + q + u * TC);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) vec[vslot<BS>(sw, q + u * TC)] = v[u];
-            }
-            for (; q < nd; q += TC) vec[vslot<BS>(sw, q)] = __ldg(rs + q);
-        }
-        (void)shift;
 #endif
         // ---- r slice: ring -> vec, chunk by chunk
         const uint32_t nrc = (rb + CH - 1) / CH;
@@ -1284,9 +1239,6 @@ __global__ void __launch_bounds__(TCB<BS> + 32, 1)
                 named_bar_sync(1, TC);
             }
         }
-#if DD_RFILL_G == 2
-        if (s + (int)gridDim.x < n_sub) r_issue(s + gridDim.x);
-#endif
         gbase += nch;
 #ifdef DD_TRACE
         tmark(3);
