@@ -9,7 +9,9 @@ solve (Alg. 1) from x0 = 0 -- every iteration runs the fused apply
 (sec. 4.4), the BSR3 SpMV and the BLAS-1/dot kernels. The preconditioner
 setup (partition, reorder, drop, ILU0/ILDU0, levels, slab packing) is done
 once per matrix before the timed region and reported as setup_ms (the paper
-reports it separately as "overhead", Tables 6/7 P:1055-1062).
+reports it separately as "overhead", Tables 6/7 P:1055-1062): the second of two
+setups at N = 1, the first -- which also pays the process's one-time CUDA costs
+-- as setup_ms_first_in_process.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3|cfg4|cfg5]
   python bench.py --impl reference ...   # the CPU oracle, bounded sample
@@ -241,10 +243,21 @@ def run_ours(args, cfg):
         dist.all_reduce(one)
         comm_info = {"transport": args.comm, "nranks": int(one.item()), "nranks_ok": int(one.item()) == world,
                      "devices": torch.cuda.device_count()}
-    t0 = time.perf_counter()
-    ctx = dd.dd_setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"], device=local, rank=rank, world=world,
-                      nccl_id=nccl_id, enable_refactor=True, comm=args.comm if world > 1 else "nccl")
-    setup_ms = 1e3 * (time.perf_counter() - t0)
+    # dd_setup twice: the first in a fresh process also pays its one-time costs
+    # (lazy kernel loading, the pinned staging buffers, the first large device
+    # allocations) -- reported as setup_ms_first_in_process; setup_ms is the
+    # second, the cost of setting up a matrix in a running process
+    # (world 1 only: a multi-rank group key -- NCCL id, peer-memory rendezvous --
+    # is used once)
+    setup_runs = []
+    for _ in range(2 if world == 1 else 1):
+        t0 = time.perf_counter()
+        ctx = dd.dd_setup(rp, ci, v, grid=cfg["grid"], tiles=cfg["tiles"], device=local, rank=rank, world=world,
+                          nccl_id=nccl_id, enable_refactor=True, comm=args.comm if world > 1 else "nccl")
+        setup_runs.append(1e3 * (time.perf_counter() - t0))
+        if world == 1 and len(setup_runs) == 1:
+            ctx.destroy()
+    setup_ms = setup_runs[-1]
     cfg = dict(cfg, tiles=ctx.tiles)  # "auto" resolved by dd_choose_tiles
     # GPU numeric re-factorisation of the same pattern, values already on the device
     vd = torch.from_numpy(v).cuda()
@@ -364,6 +377,7 @@ def run_ours(args, cfg):
                    "l2": "inputs > L2 (2.2 GB factors + 2.2 GB matrix per apply/SpMV vs 126 MB L2); no flush"},
         "iterations": r0["iterations"], "n_applies": r0["n_applies"], "true_rel_resid": r0["true_rel_resid"],
         "setup_ms": round(setup_ms, 1),
+        "setup_ms_first_in_process": round(setup_runs[0], 1),
         "setup_phases_ms": {k[:-3]: round(st[k], 1) for k in ("partition_ms", "reorder_drop_ms", "ilu0_ms", "levels_ms",
                                                              "pack_ms", "upload_ms")},
         "refactor_ms": round(refactor_ms, 2),
