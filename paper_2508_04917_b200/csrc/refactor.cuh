@@ -4,6 +4,10 @@
 
 #include <cstdint>
 
+namespace ddi {
+struct SubInfo;
+}
+
 namespace ddk {
 
 struct RfArgs {
@@ -22,6 +26,12 @@ struct RfArgs {
     // reads the matrix's values straight from A: no W buffer)
     const double *A;
     const int32_t *Wsrc;
+    // fused sliced-ELL gather (k_refactor_diag): the CTA of a subdomain also
+    // refreshes the SpMV operand's slices that start in its rows
+    const ddi::SubInfo *info;
+    const int64_t *ell_slot_ptr;
+    const int32_t *Esrc;
+    double *ell_vals;
 };
 
 void launch_gather_blocks(int64_t n, const int32_t *src, const double *from, double *to, int ell, int grid,

@@ -34,7 +34,7 @@ ddk::RfArgs rf_args(const dd_ctx *c, const RfState *rf, const double *A) {
     return ddk::RfArgs{rf->SubLev, rf->LevPtr, rf->LevRows, rf->SubU, rf->URows, rf->Wrp, rf->Wdiag, rf->Uptr,
                        rf->Lrp, rf->Urp, rf->Wcol, rf->UpdQ, rf->UpdT, rf->W, rf->Dinv, c->slab_lvl.d_bytes,
                        rf->Loff, rf->Uoff, rf->Doff, rf->Lst, rf->Ust, rf->Dst, c->pivot_floor, rf->bad,
-                       c->row_first, A, rf->Wsrc};
+                       c->row_first, A, rf->Wsrc, c->slab_lvl.d_info, nullptr, nullptr, nullptr};
 }
 
 dd_status refactor_init(dd_ctx *c) {
@@ -225,10 +225,18 @@ dd_status refactor_run(dd_ctx *c, const double *vals, int32_t on_device, cudaStr
     }
     const int grid = c->num_sms * 8;
     if (!rf->plan) ddk::launch_gather_blocks((int64_t)c->Wsrc.size(), rf->Wsrc, src, rf->W, 0, grid, st);
-    ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
+    // the diagonal-update kernel refreshes the SpMV operand itself (fused gather)
+    static const bool sep_ell = getenv("DD_REFACTOR_ELL") && atoi(getenv("DD_REFACTOR_ELL")) == 0;
+    const bool fuse_ell = rf->plan && !sep_ell;
+    if (!fuse_ell) ddk::launch_gather_blocks(c->spmv.n_slots, rf->Esrc, src, c->spmv.vals, 1, grid, st);
     *rf->h_bad = ~0ull;
     CK(cudaMemcpyAsync(rf->bad, rf->h_bad, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-    const ddk::RfArgs a = rf_args(c, rf, src);
+    ddk::RfArgs a = rf_args(c, rf, src);
+    if (fuse_ell) {
+        a.ell_slot_ptr = c->spmv.slot_ptr;
+        a.Esrc = rf->Esrc;
+        a.ell_vals = c->spmv.vals;
+    }
     const int nsl = c->sub_last - c->sub_first;
     if (nsl > 0) {
         if (rf->plan)
