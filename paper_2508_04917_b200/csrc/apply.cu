@@ -35,24 +35,26 @@
 #include "dd_internal.h"
 #include "ptx.cuh"
 
-// Branch-free K <= 3 record path for 3x3 rows (default): absent blocks of a row load from
-// the record start and are replaced by zero values and a zero x, so every
-// lane runs the same instruction stream (no BSSY/BSYNC reconvergence per
-// block) and the compiler keeps fewer values live (157 -> 103 registers).
-// fma(-0, 0, a) == a for every a, so the result is bitwise the same.
-// Config 3: 404 -> 385 us. DD_PRED=0 builds the branching form (ablation).
-// Scalar CSR rows: with selects the branch-free form measured 5-8 % slower
-// than branching (a row's block is one value); with the zero slot and the zero
-// count bytes (no selects, rec1) it is 3-5 % faster (tools/csr_bench.py).
+// Branch-free K <= 3 record path for 3x3 rows (default): every lane runs the
+// same instruction stream (no BSSY/BSYNC reconvergence per block). Round 1:
+// absent blocks loaded from the record start and were replaced by zero values
+// and a zero x with selects (404 -> 385 us at config 3). Round 2 (rec7): the
+// descriptors name a zero slot of the shared vector for absent blocks and the
+// values come from the record's zero count bytes 24..31, so no select is left
+// and the negation folds into the DFMA; one straight-line instance per
+// triangle (388 -> 354 us). fma(-0, 0, a) == a for every a: bitwise the same.
+// DD_PRED=0 builds the branching form (ablation).
 #ifndef DD_PRED
 #define DD_PRED 1
 #endif
-// The same inside each group of three of the general-K path (27-point rows):
-// 27-point 96^3, P 2048: level set 723 -> 620 us, direct 713 -> 560 us.
-// the same for scalar CSR rows (rec1); 0 keeps their branching form
+// The same for scalar CSR rows (rec1): with selects the branch-free form was
+// 5-8 % slower than branching (a row's block is one value); with the zero slot
+// it is 3-5 % faster (tools/csr_bench.py). 0 keeps their branching form.
 #ifndef DD_PRED1
 #define DD_PRED1 1
 #endif
+// Branch-free inside each group of three of the general-K path (27-point
+// rows): 27-point 96^3, P 2048: level set 723 -> 620 us, direct 713 -> 560 us.
 #ifndef DD_PRED_GEN
 #define DD_PRED_GEN 1
 #endif
