@@ -36,6 +36,9 @@ METRIC = "ILU0 apply ms & HBM GB/s (frac of roofline) at 1/2/4/8 B200; BiCGSTAB 
 CONFIGS = {
     "cfg3": dict(workload="laplacian_160^3_bsr3_P2048", kind="laplacian", grid=(160, 160, 160),
                  tiles=(16, 16, 8), tol=1e-8, golden="cfg3_laplacian160_P2048"),
+    # config 3 with the subdomain size dd_setup chooses ((10,10,20), P 2000 on this grid)
+    "cfg3auto": dict(workload="laplacian_160^3_bsr3_autotiles", kind="laplacian", grid=(160, 160, 160),
+                     tiles="auto", tol=1e-8, golden=None),
     "cfg4": dict(workload="spe10style_60x220x85_bsr3_P3400", kind="spe10", grid=(60, 220, 85),
                  tiles=(10, 20, 17), tol=1e-8, golden="cfg4_spe10style_P3400"),
     # config 4 with the subdomain size chosen to fill whole waves (dd_choose_tiles)
