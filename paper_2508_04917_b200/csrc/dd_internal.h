@@ -211,6 +211,7 @@ struct dd_ctx {
     double setup_ms[6] = {0, 0, 0, 0, 0, 0};
     // --- device state
     void *d_new_to_old_local = nullptr;  // int32 [n_local]: global orig row of local row
+    void *d_setup_tmp[3] = {nullptr, nullptr, nullptr};  // sliced-ELL build inputs, freed at dd_destroy
     double *d_stage = nullptr;           // staging for permute (3N doubles)
     double *d_vecg = nullptr;            // DD_EDGE_GLOBAL / DD_DIRECT_GLOBAL: global vector (slot layout)
     double *d_xghost = nullptr;          // spmv input with ghost space (world>1)
