@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(RF9_THREADS) k_refactor9(RfArgs a) {
 #define RFD_MINB 2
 #endif
 #ifndef RFD_THREADS
-#define RFD_THREADS 512
+#define RFD_THREADS 384
 #endif
 __global__ void __launch_bounds__(RFD_THREADS, RFD_MINB) k_refactor_diag(RfArgs a, const int32_t *__restrict__ plan) {
     const int q = blockIdx.x;
