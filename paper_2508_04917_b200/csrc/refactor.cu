@@ -148,7 +148,13 @@ __global__ void __launch_bounds__(128) k_refactor(RfArgs a) {
 // warp's maximum trip count with predicated memory operations, so every
 // shuffle is warp-uniform. Per element the FMA order is rf_mul3 /
 // rf_sub_mul / rf_inv3's (= the host setup's): identical bits.
-constexpr int RF9_THREADS = 512;
+#ifndef RF9_THREADS_DEF
+#define RF9_THREADS_DEF 256
+#endif
+#ifndef RF9_MINB
+#define RF9_MINB 4
+#endif
+constexpr int RF9_THREADS = RF9_THREADS_DEF;
 
 __device__ __forceinline__ double g9(double x, int gbase, int src) {
     return __shfl_sync(0xffffffffu, x, (gbase + src) & 31);
@@ -185,7 +191,7 @@ __device__ __forceinline__ void rf_upass_rows(const RfArgs &a, int q) {
     }
 }
 
-__global__ void __launch_bounds__(RF9_THREADS) k_refactor9(RfArgs a) {
+__global__ void __launch_bounds__(RF9_THREADS, RF9_MINB) k_refactor9(RfArgs a) {
     const int q = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / 9;  // 0..2 active, 3 = idle lanes 27..31
