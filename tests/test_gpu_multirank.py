@@ -242,3 +242,49 @@ def test_local_world_setup_status_agreed(host, monkeypatch):
     res = run_ranks(2, rank_fn)
     assert [r[0] for r in res] == ["DD_E_SINGULAR_PIVOT"] * 2, res
     assert "peer rank" in res[0][1] or "singular" in res[0][1]
+
+
+@pytest.mark.parametrize("name,world", [("random_8sub", 2), ("chunks_ragged_oddP", 3), ("stencil27", 2)])
+def test_local_world_refactor(name, world):
+    """dd_refactor at world > 1 (collective): every rank re-factors its
+    subdomains from new values of the same pattern (7-point: the diagonal-update
+    kernel with the fused SpMV-operand copy; 27-point: k_refactor9); the apply
+    and the halo SpMV then equal a fresh oracle setup of the new values, bit for
+    bit, on every rank."""
+    import torch
+    gen, kw = CASES[name]
+    rp, ci, v1 = gen()
+    # new values of the same pattern: a 5 % perturbation keeps every pivot block regular
+    v2 = v1 * (1.0 + 0.05 * np.random.default_rng(9).uniform(-1.0, 1.0, v1.shape))
+    S2 = oracle.setup(rp, ci, v2, **kw)
+    N = S2["n"]
+    r_glob = apply_input(N)
+    z_ref = oracle.apply(S2, r_glob)
+    y_ref = oracle.spmv(S2["rp_r"], S2["ci_r"], S2["v_r"], r_glob)
+    key = os.urandom(128)
+
+    def rank_fn(rank, bar):
+        torch.cuda.set_device(0)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx = dd.dd_setup(rp, ci, v1, rank=rank, world=world, nccl_id=key, comm="local", enable_refactor=True,
+                              **kw)
+            ctx.refactor(torch.from_numpy(v2.reshape(-1).copy()).cuda(), stream=st)  # collective
+            f, n = ctx.row_first, ctx.n_local
+            sl = slice(3 * f, 3 * (f + n))
+            r = torch.from_numpy(r_glob[sl].copy()).cuda()
+            z = torch.empty_like(r)
+            y = torch.empty_like(r)
+            ctx.apply(r, z, stream=st)
+            ctx.spmv(r, y, stream=st)  # collective: halo
+            st.synchronize()
+            out = {"first": f, "n": n, "z": z.cpu().numpy(), "y": y.cpu().numpy()}
+            bar.wait()
+            ctx.destroy()
+            return out
+
+    outs = run_ranks(world, rank_fn)
+    for o in outs:
+        sl = slice(3 * o["first"], 3 * (o["first"] + o["n"]))
+        assert np.array_equal(o["z"], z_ref[sl])
+        assert np.array_equal(o["y"], y_ref[sl])
