@@ -5,6 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import raw, stalls
 
 d = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
+dst = sys.argv[2] if len(sys.argv) > 2 else "profiles/round1_cfg2.md"
 KEYS = [("gpu__time_duration.sum", "time"), ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
         ("dram__bytes_read.sum", "DRAM read"), ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
         ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
@@ -43,5 +44,5 @@ for c in ("2a", "2b"):
         elif m is None:
             out.append(f"* {v}: not available at this config")
     out.append("")
-open("profiles/round1_cfg2.md", "w").write("\n".join(out) + "\n")
+open(dst, "w").write("\n".join(out) + "\n")
 print("\n".join(out))
