@@ -631,7 +631,12 @@ void launch_spmv(int mode, const dd_ctx *ctx, const double *x, const double *xg,
 #endif
 }
 
-int blas_grid(const dd_ctx *ctx) { return ctx->num_sms * 8; }
+// BLAS-1 grid: 4 CTAs of 256 threads per SM (config 3: 27.3 ms of BLAS-1 per
+// solve; 8 per SM 28.3 ms, 16 28.9, 2 34.1); DD_BLAS_GRID_MULT overrides (1-16)
+int blas_grid(const dd_ctx *ctx) {
+    static const int mult = std::max(1, std::min(16, env_i("DD_BLAS_GRID_MULT", 4)));
+    return ctx->num_sms * mult;
+}
 
 __global__ void k_iter_head(int *ctl) {
     if (ctl[C_STATE] == ST_RUN) ctl[C_ITER] += 1;
@@ -730,7 +735,7 @@ void launch_scatter3(const dd_ctx *ctx, int64_t n, const int32_t *idx, const dou
 }
 size_t partials_bytes(const dd_ctx *ctx) {
     // block partials of any grid_reduce; split SpMV reduction: 2 per slice + its block partials
-    return sizeof(DD) * 2 * (size_t)std::max<int64_t>(ctx->num_sms * 8, spmv_fused_grid(ctx)) +
+    return sizeof(DD) * 2 * (size_t)std::max<int64_t>(ctx->num_sms * 16, spmv_fused_grid(ctx)) +
            sizeof(DD) * 2 * (size_t)(ctx->spmv.n_slices + reduce_grid(ctx));
 }
 
