@@ -428,3 +428,18 @@ def test_cfg5_full_size_sampled_parity():
         ya = oracle.spmv(np.array(arp, np.int64), np.array(aci, np.int32), np.concatenate(av).ravel(), r)
         assert np.array_equal(y[sl], ya[:3 * P]), f"SpMV, subdomain {s}"
     ctx.destroy()
+
+
+@pytest.mark.parametrize("name", ["cfg1_16^3", "stencil27_geo"])
+def test_factors_after_refactor_bitwise(name):
+    """dd_get_factors after dd_refactor with new values reports the new factors,
+    bit for bit against a fresh oracle setup of those values: the 7-point case
+    reads L and U_unit back from the slab (diagonal-update kernel, no W buffer),
+    the 27-point case from W (k_refactor9)."""
+    gen, kw = CASES[name]
+    rp, ci, v1 = gen()
+    v2 = v1 * (1.0 + 0.05 * np.random.default_rng(17).uniform(-1.0, 1.0, v1.shape))
+    ctx = dd.dd_setup(rp, ci, v1, enable_refactor=True, **kw)
+    ctx.refactor(v2)
+    assert_setup_bitwise(ctx, oracle.setup(rp, ci, v2, **kw))
+    ctx.destroy()
